@@ -1,0 +1,167 @@
+/*
+ * mea.h — memory-efficient exact attention on NVIDIA B200 (sm_100a).
+ *
+ * C ABI of libmea.so. Implements the hot path of Rabe & Staats, "Self-attention
+ * Does Not Need O(n^2) Memory" (arXiv 2112.05682): exact softmax attention
+ *     s_i = dot(q, k_i) * scale,  out = sum_i v_i e^{s_i} / sum_j e^{s_j}
+ * (Eq. (1) at PAPER.md:50-53), evaluated key tile by key tile with
+ * the running value sum v*, weight sum s* and running max m* of PAPER.md:85-90,
+ * so the n_q x n_k score matrix is never stored. The backward pass recomputes each
+ * tile of scores from per-row statistics (checkpointing).
+ *
+ * Conventions (all entry points):
+ *  - Every data pointer is a DEVICE pointer owned by the caller. The library never
+ *    allocates, frees or synchronises; scratch is the caller-provided workspace,
+ *    whose size the *_workspace_size queries return. Outputs are fully overwritten.
+ *    Outputs must not alias inputs.
+ *  - Layouts are dense row-major: q/out/dout/dq [B, n_q, H, d]; k/v/dk/dv
+ *    [B, n_k, H, d]; lse [B, H, n_q] (float32, natural log); single-query q/out
+ *    [B, H, d]. Base pointers must be 16-byte aligned.
+ *  - ``scale`` multiplies every score. Figure 1 uses 1/sqrt(d); the
+ *    paper's Secs. 1-3 use 1. Must be finite.
+ *  - ``stream`` is a cudaStream_t (NULL = legacy default stream). Calls are
+ *    stream-ordered and asynchronous: a MEA_OK return means the work was enqueued.
+ *  - Errors are detected before any launch and returned as mea_status_t; nothing is
+ *    launched on error. No exception or abort crosses the ABI.
+ *      n_q == 0 (or B*H == 0 work)    -> MEA_OK, nothing launched
+ *      n_k == 0                       -> MEA_ERR_EMPTY_KEYS (an explicit error, not NaN)
+ *      B, H, d < 1, chunk < 0, bad dtype, non-finite scale -> MEA_ERR_INVALID_VALUE
+ *      shape/dtype not implemented    -> MEA_ERR_UNSUPPORTED
+ *      pointer not 16-byte aligned    -> MEA_ERR_MISALIGNED
+ *      workspace smaller than needed  -> MEA_ERR_WORKSPACE_TOO_SMALL
+ *      CUDA launch/encode failure     -> MEA_ERR_CUDA (detail in mea_last_error_detail)
+ *  - Non-finite input values are not checked; they propagate.
+ *  - Supported: bf16 inputs with d = 64 (tcgen05 tensor-core kernels); f32 inputs with
+ *    1 <= d <= 128 (exact-f32 SIMT kernels, forward and single query).
+ */
+#ifndef MEA_H_
+#define MEA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MEA_API __attribute__((visibility("default")))
+#else
+#define MEA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { MEA_F32 = 0, MEA_BF16 = 1 } mea_dtype_t;
+
+typedef enum {
+  MEA_OK = 0,
+  MEA_ERR_INVALID_VALUE = 1,
+  MEA_ERR_EMPTY_KEYS = 2,
+  MEA_ERR_UNSUPPORTED = 3,
+  MEA_ERR_MISALIGNED = 4,
+  MEA_ERR_WORKSPACE_TOO_SMALL = 5,
+  MEA_ERR_CUDA = 6
+} mea_status_t;
+
+/* Library version, e.g. "mea 0.1 sm_100a". Static string. */
+MEA_API const char* mea_version(void);
+/* Static description of a status code. */
+MEA_API const char* mea_status_string(mea_status_t status);
+/* Thread-local detail of the last error on this thread (e.g. which check failed). */
+MEA_API const char* mea_last_error_detail(void);
+
+/*
+ * Self-/cross-attention forward (PAPER.md:21-25 with PAPER.md:85-90; Figure 1,
+ * PAPER.md:107-163, gives the chunked schedule).
+ *   q [B,n_q,H,d], k,v [B,n_k,H,d] of in_dtype; out [B,n_q,H,d] of out_dtype.
+ *   lse [B,H,n_q] float32, nullable: lse_i = log sum_j e^{s_ij}, the per-row residual
+ *     the backward pass consumes.
+ *   q_chunk, k_chunk: the paper's query_chunk_size / key_chunk_size.
+ *     0 = default schedule: every work item streams all keys with an on-chip running
+ *     (v*, s*, m*), zero workspace. k_chunk in (0, n_k) selects the paper's key-chunk
+ *     summaries: each chunk's (m*, s*, v*) goes to the workspace
+ *     and a merge pass combines them (bf16 path; rounded up to a multiple of 128
+ *     keys). q_chunk is a scheduling hint only (results do not depend on it).
+ *   in_dtype MEA_BF16 requires d == 64 and out_dtype in {BF16, F32};
+ *   in_dtype MEA_F32 requires d <= 128, out_dtype F32 and k_chunk == 0.
+ */
+MEA_API mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void* out,
+                               int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                               mea_dtype_t in_dtype, mea_dtype_t out_dtype, float scale,
+                               float* lse, int64_t q_chunk, int64_t k_chunk,
+                               void* workspace, size_t workspace_bytes, void* stream);
+
+/* Workspace bytes mea_attention_fwd needs for these arguments (0 when k_chunk == 0). */
+MEA_API mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k,
+                                              int64_t d, mea_dtype_t in_dtype, int64_t q_chunk,
+                                              int64_t k_chunk, size_t* bytes);
+
+/*
+ * Single-query attention per (b,h) — the paper's O(1)-memory algorithm (PAPER.md:59-63,
+ * stabilised as in PAPER.md:85-90). q,out [B,H,d]; k,v [B,n_k,H,d]. Keys are split into
+ * ranges processed in parallel (split-K); each range yields a triple (m*, s*, v*) in the
+ * workspace and a merge pass combines them with Figure 1's global-max rescale
+ * (PAPER.md:140-147). Workspace is independent of n_k (bounded by the split count).
+ */
+MEA_API mea_status_t mea_single_query_fwd(const void* q, const void* k, const void* v, void* out,
+                                  int64_t B, int64_t H, int64_t n_k, int64_t d,
+                                  mea_dtype_t in_dtype, mea_dtype_t out_dtype, float scale,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+
+MEA_API mea_status_t mea_single_query_workspace_size(int64_t B, int64_t H, int64_t n_k, int64_t d,
+                                             mea_dtype_t in_dtype, size_t* bytes);
+
+/*
+ * Multi-GPU building blocks for attention sharded over key ranges (MNNFast-style KV
+ * sharding; merge = PAPER.md:140-147).
+ * mea_single_query_partial writes, per (b,h), the stream state over this call's keys:
+ *   m [B*H]      : reference max (natural-log units of the scaled score; any value
+ *                  >= the true max minus 8*ln2 — all terms are relative to it),
+ *   s [B*H]      : s* = sum_j e^{s_j - m},
+ *   vstar [B*H*d]: v* = sum_j v_j e^{s_j - m}   (all float32).
+ * n_k == 0 is allowed here and yields the empty triple (-inf, 0, 0).
+ * mea_merge_partials combines P stacked triples m [P,B*H], s [P,B*H], vstar [P,B*H,d]
+ * into out [B,H,d] (out_dtype). Empty triples contribute nothing; all-empty rows are
+ * MEA_ERR_EMPTY_KEYS only if detectable on the host (P == 0), else they yield NaN.
+ */
+MEA_API mea_status_t mea_single_query_partial(const void* q, const void* k, const void* v, float* m,
+                                      float* s, float* vstar, int64_t B, int64_t H, int64_t n_k,
+                                      int64_t d, mea_dtype_t in_dtype, float scale,
+                                      void* workspace, size_t workspace_bytes, void* stream);
+
+MEA_API mea_status_t mea_merge_partials(const float* m, const float* s, const float* vstar, int64_t P,
+                                int64_t B, int64_t H, int64_t d, void* out, mea_dtype_t out_dtype,
+                                void* stream);
+
+/*
+ * Backward of out = attention(q, k, v) (the VJP the paper obtains with jax.grad through
+ * jax.checkpoint): given dout, writes dq, dk, dv (same dtype/layout as
+ * q, k, v). Scores and probabilities are recomputed tile by tile from lse (PAPER.md:256:
+ * "recomputed during backpropagation"); no n_q x n_k buffer exists. lse is the forward's
+ * residual; NULL makes the call recompute it first (one extra statistics pass).
+ * The max carries no gradient (stop_gradient).
+ * Workspace: delta [B,H,n_q] f32 + dq accumulator [B,n_q,H,d] f32 (+ lse if NULL).
+ * bf16 with d == 64 only.
+ */
+MEA_API mea_status_t mea_attention_bwd(const void* q, const void* k, const void* v, const void* out,
+                               const void* dout, void* dq, void* dk, void* dv, int64_t B,
+                               int64_t H, int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t dtype,
+                               float scale, const float* lse, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
+MEA_API mea_status_t mea_attention_bwd_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k,
+                                              int64_t d, mea_dtype_t dtype, int lse_given,
+                                              size_t* bytes);
+
+/*
+ * Synthetic input generator (not part of the method; used by tests and the bench so
+ * large configs never cross PCIe). Fills dst[i] = value(seed, tensor_id, offset + i),
+ * i < numel, with the counter-based Irwin-Hall(12) generator documented in
+ * synth/gen.py, rounded to dtype (RNE). Bit-identical to the host generator.
+ */
+MEA_API mea_status_t mea_fill_synthetic(void* dst, int64_t numel, mea_dtype_t dtype, uint64_t seed,
+                                uint32_t tensor_id, int64_t offset, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEA_H_ */

@@ -1,0 +1,25 @@
+/*
+ * mea_debug.h — bring-up probes of libmea.so (used by tests only, not the method).
+ *
+ * mea_debug_umma_tile runs exactly the two tensor-core steps of one forward tile
+ * (Figure 1 lines 13 and 17) on a single CTA:
+ *   s_out[128,128] = a[128,64] . b[128,64]^T          (tcgen05.mma SS, fp32 in TMEM)
+ *   o_out[128,64]  = bf16(s_out) . v[128,64]          (tcgen05.mma TS: A from TMEM)
+ * a, b, v are bf16 device pointers, row-major, loaded by TMA with 128B swizzle; the
+ * fp32 outputs are row-major device pointers. Lets the tests check the shared-memory
+ * descriptors, the instruction descriptors and the TMEM operand layout in isolation.
+ */
+#ifndef MEA_DEBUG_H_
+#define MEA_DEBUG_H_
+#include "mea.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+MEA_API mea_status_t mea_debug_umma_tile(const void* a, const void* b, const void* v, float* s_out,
+                                 float* o_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,206 @@
+"""Thin Python binding over libmea.so: same names as include/mea.h, torch tensors in.
+
+Argument marshalling only — shapes, dtypes, pointers, the current CUDA stream and
+workspace allocation (torch owns every buffer). Every step of the method runs in the
+library's CUDA kernels. Layouts: q/out [B, n_q, H, d]; k/v [B, n_k, H, d]; lse
+[B, H, n_q]; single-query q/out [B, H, d].
+"""
+import ctypes
+import math
+
+import torch
+
+from . import _lib
+
+MEA_F32, MEA_BF16 = 0, 1
+_DT = {torch.float32: MEA_F32, torch.bfloat16: MEA_BF16}
+_TORCH = {MEA_F32: torch.float32, MEA_BF16: torch.bfloat16}
+
+MEA_OK = 0
+STATUS = {0: "MEA_OK", 1: "MEA_ERR_INVALID_VALUE", 2: "MEA_ERR_EMPTY_KEYS", 3: "MEA_ERR_UNSUPPORTED",
+          4: "MEA_ERR_MISALIGNED", 5: "MEA_ERR_WORKSPACE_TOO_SMALL", 6: "MEA_ERR_CUDA"}
+
+
+class MeaError(RuntimeError):
+    def __init__(self, status, detail):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"{self.name}: {detail}")
+
+
+class EmptyKeysError(MeaError, ValueError):
+    pass
+
+
+def _check(status):
+    if status != MEA_OK:
+        detail = _lib.load().mea_last_error_detail().decode()
+        if status == 2:
+            raise EmptyKeysError(status, detail)
+        raise MeaError(status, detail)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _dtype(t):
+    if t.dtype not in _DT:
+        raise TypeError(f"unsupported dtype {t.dtype}; use bfloat16 or float32")
+    return _DT[t.dtype]
+
+
+def _cuda_contig(*ts):
+    for t in ts:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise ValueError("libmea takes CUDA tensors (no CPU fallback)")
+        if not t.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+
+
+def _workspace(nbytes, device):
+    if nbytes == 0:
+        return None
+    return torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+def version():
+    return _lib.load().mea_version().decode()
+
+
+# ------------------------------------------------------------------------ forward
+def mea_attention_fwd_workspace_size(B, H, n_q, n_k, d, in_dtype, q_chunk=0, k_chunk=0):
+    n = ctypes.c_size_t(0)
+    _check(_lib.load().mea_attention_fwd_workspace_size(B, H, n_q, n_k, d, in_dtype, q_chunk, k_chunk,
+                                                        ctypes.byref(n)))
+    return n.value
+
+
+def mea_attention_fwd(q, k, v, scale=None, out=None, out_dtype=None, lse=None, want_lse=False,
+                      q_chunk=0, k_chunk=0, workspace=None):
+    """out = attention(q, k, v) (Figure 1). Returns out, or (out, lse)."""
+    _cuda_contig(q, k, v, out, lse)
+    B, n_q, H, d = q.shape
+    n_k = k.shape[1]
+    if k.shape != (B, n_k, H, d) or v.shape != k.shape:
+        raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
+    dt = _dtype(q)
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        raise TypeError("q, k, v must share a dtype")
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    if out is None:
+        od = q.dtype if out_dtype is None else out_dtype
+        out = torch.empty((B, n_q, H, d), dtype=od, device=q.device)
+    if want_lse and lse is None:
+        lse = torch.empty((B, H, n_q), dtype=torch.float32, device=q.device)
+    if workspace is None:
+        workspace = _workspace(mea_attention_fwd_workspace_size(B, H, n_q, n_k, d, dt, q_chunk, k_chunk), q.device)
+    _check(_lib.load().mea_attention_fwd(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(out), B, H, n_q, n_k, d, dt, _dtype(out), scale, _ptr(lse),
+        q_chunk, k_chunk, _ptr(workspace), workspace.numel() if workspace is not None else 0, _stream(q.device)))
+    return (out, lse) if (want_lse or lse is not None) else out
+
+
+# ------------------------------------------------------------------------ single query
+def mea_single_query_workspace_size(B, H, n_k, d, in_dtype):
+    n = ctypes.c_size_t(0)
+    _check(_lib.load().mea_single_query_workspace_size(B, H, n_k, d, in_dtype, ctypes.byref(n)))
+    return n.value
+
+
+def mea_single_query_fwd(q, k, v, scale=None, out=None, out_dtype=None, workspace=None):
+    """Single-query attention per (b,h). q [B,H,d]; k,v [B,n_k,H,d]."""
+    _cuda_contig(q, k, v, out)
+    B, H, d = q.shape
+    n_k = k.shape[1]
+    if k.shape != (B, n_k, H, d) or v.shape != k.shape:
+        raise ValueError("shape mismatch")
+    dt = _dtype(q)
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    if out is None:
+        out = torch.empty((B, H, d), dtype=q.dtype if out_dtype is None else out_dtype, device=q.device)
+    if workspace is None:
+        workspace = _workspace(mea_single_query_workspace_size(B, H, max(n_k, 0), d, dt), q.device)
+    _check(_lib.load().mea_single_query_fwd(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(out), B, H, n_k, d, dt, _dtype(out), scale, _ptr(workspace),
+        workspace.numel() if workspace is not None else 0, _stream(q.device)))
+    return out
+
+
+def mea_single_query_partial(q, k, v, scale=None, workspace=None):
+    """Per-(b,h) stream triple (m*, s*, v*) over these keys; m in natural-log units."""
+    _cuda_contig(q, k, v)
+    B, H, d = q.shape
+    n_k = k.shape[1]
+    dt = _dtype(q)
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    m = torch.empty(B * H, dtype=torch.float32, device=q.device)
+    s = torch.empty(B * H, dtype=torch.float32, device=q.device)
+    vs = torch.empty(B * H * d, dtype=torch.float32, device=q.device)
+    if workspace is None:
+        workspace = _workspace(mea_single_query_workspace_size(B, H, n_k, d, dt), q.device)
+    _check(_lib.load().mea_single_query_partial(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(m), _ptr(s), _ptr(vs), B, H, n_k, d, dt, scale, _ptr(workspace),
+        workspace.numel() if workspace is not None else 0, _stream(q.device)))
+    return m, s, vs.view(B * H, d)
+
+
+def mea_merge_partials(m, s, vstar, B, H, out_dtype=torch.bfloat16, out=None):
+    """Merge P stacked triples m [P,B*H], s [P,B*H], vstar [P,B*H,d] -> out [B,H,d]."""
+    _cuda_contig(m, s, vstar, out)
+    P = m.shape[0]
+    d = vstar.shape[-1]
+    if out is None:
+        out = torch.empty((B, H, d), dtype=out_dtype, device=m.device)
+    _check(_lib.load().mea_merge_partials(_ptr(m), _ptr(s), _ptr(vstar), P, B, H, d, _ptr(out), _dtype(out),
+                                          _stream(m.device)))
+    return out
+
+
+# ------------------------------------------------------------------------ backward
+def mea_attention_bwd_workspace_size(B, H, n_q, n_k, d, dtype, lse_given=True):
+    n = ctypes.c_size_t(0)
+    _check(_lib.load().mea_attention_bwd_workspace_size(B, H, n_q, n_k, d, dtype, int(bool(lse_given)),
+                                                        ctypes.byref(n)))
+    return n.value
+
+
+def mea_attention_bwd(q, k, v, out, dout, lse=None, scale=None, dq=None, dk=None, dv=None, workspace=None):
+    """(dq, dk, dv) of out = attention(q, k, v) given dout (recompute-per-tile backward)."""
+    _cuda_contig(q, k, v, out, dout, lse, dq, dk, dv)
+    B, n_q, H, d = q.shape
+    n_k = k.shape[1]
+    dt = _dtype(q)
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    if workspace is None:
+        workspace = _workspace(mea_attention_bwd_workspace_size(B, H, n_q, n_k, d, dt, lse is not None), q.device)
+    _check(_lib.load().mea_attention_bwd(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv), B, H, n_q, n_k, d, dt,
+        scale, _ptr(lse), _ptr(workspace), workspace.numel() if workspace is not None else 0, _stream(q.device)))
+    return dq, dk, dv
+
+
+# ------------------------------------------------------------------------ generator / debug
+def mea_fill_synthetic(t, seed, tensor_id, offset=0):
+    """Fill a CUDA tensor with the counter-based synthetic inputs (synth/gen.py), in place."""
+    _cuda_contig(t)
+    _check(_lib.load().mea_fill_synthetic(_ptr(t), t.numel(), _dtype(t), seed, tensor_id, offset,
+                                          _stream(t.device)))
+    return t
+
+
+def mea_debug_umma_tile(a, b, v):
+    _cuda_contig(a, b, v)
+    s = torch.empty((128, 128), dtype=torch.float32, device=a.device)
+    o = torch.empty((128, 64), dtype=torch.float32, device=a.device)
+    _check(_lib.load().mea_debug_umma_tile(_ptr(a), _ptr(b), _ptr(v), _ptr(s), _ptr(o), _stream(a.device)))
+    return s, o

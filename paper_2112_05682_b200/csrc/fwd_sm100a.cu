@@ -1,0 +1,469 @@
+// fwd_sm100a.cu — self-attention forward on tcgen05 tensor cores (bf16 in, fp32 accumulate).
+//
+// The paper's per-query stream run for 128 query rows at a time: one
+// softmax thread owns one query row and keeps its running max m* and weight sum s* in
+// registers; the running value sum v* (the O accumulator) lives in TMEM. Keys arrive in
+// tiles of 128 (a "key chunk", Figure 1 lines 12-19 = PAPER.md:118-126):
+//   S  = Q K^T                 tcgen05.mma SS  -> TMEM         (einsum qhd,khd->qhk)
+//   m  = max(m*, rowmax S)     registers
+//   P  = 2^(S*c - m), c = scale*log2 e                        (scale P:116)
+//   s* = s* alpha + rowsum P,  v* = v* alpha + P V            (PV = tcgen05.mma TS)
+// and out = v*/s* at the end. The rescale by alpha = 2^(m_old - m_new) is
+// applied lazily ("renormalize ... as needed"): only when the row max grows by more
+// than 2^8, so v* and s* are kept relative to a reference max that may lag the true max by
+// at most 8 (in log2 units). All terms share the reference, so the result is unchanged.
+//
+// CTA = 2 query tiles (256 rows) of one (b, h) sharing every K/V tile:
+//   warp 0      TMA producer: Q0,Q1 once, then a 4-stage K/V ring (mbarrier full/empty)
+//   warp 1      MMA issuer (one thread): S0,S1 = Q K^T; O0,O1 += P V; commits -> mbarriers
+//   warp 2      TMEM allocator
+//   warps 4-7   softmax warpgroup for query tile 0 (one thread = one row = one TMEM lane)
+//   warps 8-11  softmax warpgroup for query tile 1
+// MMA issue order per key tile t:  PV0_t, S0_{t+1}, PV1_t, S1_{t+1}  so that softmax of one
+// tile overlaps the tensor-core work of the other ("ping-pong"). Because S0_{t+1} is issued
+// after PV0_t, the commit that signals S0_{t+1} also proves PV0_t finished: O0 is quiescent
+// while softmax 0 works on tile t+1, so the lazy O rescale needs no extra wait.
+//
+// TMEM columns (512 allocated): S0 [0,128) S1 [128,256) O0 [256,320) O1 [320,384)
+//                                P0 [384,448) P1 [448,512)  (P = bf16 pairs, 2 per column)
+//
+// Key split (the paper's key chunks): with num_splits > 1 each CTA covers a
+// contiguous key range and stores its unnormalised (m*, s*, v*) instead of out; merge_rows()
+// then applies Figure 1's global-max rescale (lines 33-40).
+#include <cuda_bf16.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace mea {
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kTileBytes = kTileN * kHeadDim * 2;  // 16 KiB: 128 rows x 128 B
+constexpr int kThreads = 384;
+__host__ __device__ constexpr uint32_t col_s(int wg) { return wg ? 128u : 0u; }
+__host__ __device__ constexpr uint32_t col_o(int wg) { return wg ? 320u : 256u; }
+__host__ __device__ constexpr uint32_t col_p(int wg) { return wg ? 448u : 384u; }
+constexpr float kLazyThreshold = 8.0f;  // log2 units: rescale when the max grows by > 2^8
+
+constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, false, false);  // A=Q K-major, B=K K-major
+constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 64, false, true);    // A=P (TMEM), B=V MN-major
+
+struct FwdSmem {
+  uint8_t q[2][kTileBytes];
+  uint8_t k[kStages][kTileBytes];
+  uint8_t v[kStages][kTileBytes];
+  uint64_t q_full;
+  uint64_t kv_full[kStages];
+  uint64_t kv_empty[kStages];
+  uint64_t s_full[2];
+  uint64_t p_full[2];
+  uint64_t o_done[2];
+  uint32_t tmem_base;
+};
+constexpr size_t kFwdSmemBytes = sizeof(FwdSmem) + 1024;
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// S[tmem d_col] = Qtile . Ktile^T  (M=128 queries, N=128 keys, K=64 in 4 steps of 16)
+__device__ __forceinline__ void issue_qk(uint32_t d_tmem, const uint8_t* qt, const uint8_t* kt) {
+  const uint32_t qa = smem_u32(qt), ka = smem_u32(kt);
+#pragma unroll
+  for (int kk = 0; kk < kHeadDim / 16; ++kk) {
+    // K-major SW128: 16 bf16 = 32 B per K step inside the 128-B swizzle row.
+    umma_ss(d_tmem, sdesc_sw128(qa + kk * 32, 16, 1024), sdesc_sw128(ka + kk * 32, 16, 1024), kIdescQK,
+            kk > 0);
+  }
+}
+// O[tmem d_col] (+)= P[tmem p_col] . Vtile  (M=128, N=64, K=128 keys in 8 steps of 16)
+__device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t p_tmem, const uint8_t* vt, bool acc) {
+  const uint32_t va = smem_u32(vt);
+#pragma unroll
+  for (int kk = 0; kk < kTileN / 16; ++kk) {
+    // MN-major SW128 B operand: 16 keys = 2 groups of 8 rows of 128 B; SBO = 1024 B.
+    umma_ts(d_tmem, p_tmem + kk * 8, sdesc_sw128(va + kk * 2048, 16, 1024), kIdescPV, (acc || kk > 0) ? 1u : 0u);
+  }
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(a, fmaxf(b, c)); }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    fwd_bf16_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+                    const __grid_constant__ CUtensorMap mv, const FwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  FwdSmem& sm = *reinterpret_cast<FwdSmem*>(align1024(smem_raw));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qblk = blockIdx.x % p.num_q_blocks;
+  const int split = blockIdx.x / p.num_q_blocks;
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int q0 = qblk * kRowsPerCta;
+  const int n_tiles = (p.n_k + kTileN - 1) / kTileN;
+  const int t_begin = split * p.tiles_per_split;
+  const int t_end = min(n_tiles, t_begin + p.tiles_per_split);
+  const int T = t_end - t_begin;
+  const int key_end = min(p.n_k, t_end * kTileN);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.q_full, 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&sm.kv_full[i], 1);
+      mbar_init(&sm.kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.s_full[i], 1);
+      mbar_init(&sm.p_full[i], 128);
+      mbar_init(&sm.o_done[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mq);
+    tma_prefetch_desc(&mk);
+    tma_prefetch_desc(&mv);
+  }
+  if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  // Register hand-off (inside each role branch so ptxas sees the budget per region):
+  // warpgroup 0 (producer / MMA / allocator) needs few registers; the softmax warpgroups
+  // hold a 128-score row each.
+  if (warp < 4) {
+    setmaxnreg_dec<80>();
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+      mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
+      tma_load_4d(sm.q[0], &mq, &sm.q_full, 0, h, q0, b, stream);
+      tma_load_4d(sm.q[1], &mq, &sm.q_full, 0, h, q0 + kTileM, b, stream);
+      for (int t = 0; t < T; ++t) {
+        const int st = t % kStages, n = t / kStages;
+        if (t >= kStages) mbar_wait(&sm.kv_empty[st], (n - 1) & 1);
+        const int krow = (t_begin + t) * kTileN;
+        mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTileBytes);
+        tma_load_4d(sm.k[st], &mk, &sm.kv_full[st], 0, h, krow, b, keep);
+        tma_load_4d(sm.v[st], &mv, &sm.kv_full[st], 0, h, krow, b, keep);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      mbar_wait(&sm.q_full, 0);
+      mbar_wait(&sm.kv_full[0], 0);
+      tc_fence_after();
+      issue_qk(tmem + col_s(0), sm.q[0], sm.k[0]);
+      umma_commit(&sm.s_full[0]);
+      issue_qk(tmem + col_s(1), sm.q[1], sm.k[0]);
+      umma_commit(&sm.s_full[1]);
+      for (int t = 0; t < T; ++t) {
+        const int st = t % kStages;
+        const int nx = (t + 1) % kStages;
+        const bool more = (t + 1) < T;
+        // query tile 0
+        mbar_wait(&sm.p_full[0], t & 1);
+        tc_fence_after();
+        issue_pv(tmem + col_o(0), tmem + col_p(0), sm.v[st], t > 0);
+        if (more) {
+          mbar_wait(&sm.kv_full[nx], ((t + 1) / kStages) & 1);
+          tc_fence_after();
+          issue_qk(tmem + col_s(0), sm.q[0], sm.k[nx]);
+          umma_commit(&sm.s_full[0]);
+        } else {
+          umma_commit(&sm.o_done[0]);
+        }
+        // query tile 1
+        mbar_wait(&sm.p_full[1], t & 1);
+        tc_fence_after();
+        issue_pv(tmem + col_o(1), tmem + col_p(1), sm.v[st], t > 0);
+        umma_commit(&sm.kv_empty[st]);  // K_t and V_t no longer read
+        if (more) {
+          issue_qk(tmem + col_s(1), sm.q[1], sm.k[nx]);
+          umma_commit(&sm.s_full[1]);
+        } else {
+          umma_commit(&sm.o_done[1]);
+        }
+      }
+    }
+  }
+  } else {
+    setmaxnreg_inc<208>();
+    // ------------------------------------------------------------ softmax warpgroups
+    const int wg = (warp - 4) >> 2;
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q0 + wg * kTileM + quarter * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const float c = p.scale_log2;
+    float m_ref = -INFINITY;  // reference max m*, log2 units of the scaled score
+    float l = 0.f;            // s*
+    for (int t = 0; t < T; ++t) {
+      mbar_wait(&sm.s_full[wg], t & 1);
+      tc_fence_after();
+      uint32_t sr[128];
+      tmem_ld32(lane_base + col_s(wg) + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld32(lane_base + col_s(wg) + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tmem_ld32(lane_base + col_s(wg) + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
+      tmem_ld32(lane_base + col_s(wg) + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
+      tmem_ld_wait();
+      const int valid = key_end - (t_begin + t) * kTileN;  // keys of this tile inside the range
+      // row extremum of the raw score (max if c >= 0, min if c < 0): max(s*c) over valid keys
+      float ext;
+      if (c >= 0.f) {
+        float m0 = -INFINITY, m1 = -INFINITY;
+        if (valid >= kTileN) {
+#pragma unroll
+          for (int i = 0; i < 128; i += 4) {
+            m0 = fmax3(m0, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+            m1 = fmax3(m1, __uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3]));
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (i < valid) m0 = fmaxf(m0, __uint_as_float(sr[i]));
+        }
+        ext = fmaxf(m0, m1);
+      } else {
+        float m0 = INFINITY;
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (i < valid) m0 = fminf(m0, __uint_as_float(sr[i]));
+        ext = m0;
+      }
+      const float m_cand = ext * c;
+      const bool need = m_cand > m_ref + kLazyThreshold;  // always true on the first tile
+      float alpha = 1.f;
+      if (need) {
+        alpha = ex2_approx(m_ref - m_cand);  // 0 when m_ref = -inf
+        m_ref = m_cand;
+        l *= alpha;
+      }
+      if (t > 0 && __any_sync(0xffffffffu, need)) {
+        // v* <- v* alpha. O is quiescent: S_t's commit covers PV_{t-1}.
+#pragma unroll
+        for (int part = 0; part < 4; ++part) {
+          uint32_t o[16];
+          tmem_ld16(lane_base + col_o(wg) + part * 16, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st16(lane_base + col_o(wg) + part * 16, o);
+        }
+      }
+      // P = 2^(s c - m*) in bf16 pairs; s* += rowsum P
+      const float neg_m = -m_ref;
+      float rs0 = 0.f, rs1 = 0.f;
+      uint32_t pk[64];
+      if (valid >= kTileN) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const float p0 = ex2_approx(fmaf(__uint_as_float(sr[2 * i]), c, neg_m));
+          const float p1 = ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), c, neg_m));
+          rs0 += p0;
+          rs1 += p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const float p0 = (2 * i < valid) ? ex2_approx(fmaf(__uint_as_float(sr[2 * i]), c, neg_m)) : 0.f;
+          const float p1 = (2 * i + 1 < valid) ? ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), c, neg_m)) : 0.f;
+          rs0 += p0;
+          rs1 += p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+      }
+      l += rs0 + rs1;
+      tmem_st32(lane_base + col_p(wg) + 0, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      tmem_st32(lane_base + col_p(wg) + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&sm.p_full[wg]);
+    }
+    // ------------------------------------------------------------ epilogue: out = v*/s*
+    mbar_wait(&sm.o_done[wg], 0);
+    tc_fence_after();
+    uint32_t o[64];
+    tmem_ld32(lane_base + col_o(wg) + 0, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+    tmem_ld32(lane_base + col_o(wg) + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
+    tmem_ld_wait();
+    if (row < p.n_q) {
+      const size_t bh = (size_t)b * p.H + h;
+      if (p.num_splits > 1) {
+        const size_t prow = ((size_t)split * p.B * p.H + bh) * p.n_q + row;
+        float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kHeadDim);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
+                               __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
+        reinterpret_cast<float2*>(p.part_ml)[prow] = make_float2(m_ref, l);
+      } else {
+        const float inv = 1.f / l;
+        const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim;
+        if (p.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            dst[i] = make_float4(__uint_as_float(o[4 * i]) * inv, __uint_as_float(o[4 * i + 1]) * inv,
+                                 __uint_as_float(o[4 * i + 2]) * inv, __uint_as_float(o[4 * i + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            uint4 w;
+            w.x = pack_bf16x2(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv);
+            w.y = pack_bf16x2(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv);
+            w.z = pack_bf16x2(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv);
+            w.w = pack_bf16x2(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv);
+            dst[i] = w;
+          }
+        }
+        if (p.lse) p.lse[bh * p.n_q + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// Figure 1 lines 33-40 over the key-split partials of each query row:
+// M = max_c m_c; out = sum_c 2^(m_c - M) v*_c / sum_c 2^(m_c - M) s*_c. One warp per row.
+__global__ void merge_rows_kernel(const FwdParams p) {
+  const int64_t rows = (int64_t)p.B * p.H * p.n_q;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int64_t stride = rows;  // rows per split
+  const float2* ml = reinterpret_cast<const float2*>(p.part_ml);
+  float M = -INFINITY;
+  for (int s = 0; s < p.num_splits; ++s) M = fmaxf(M, ml[s * stride + r].x);
+  float den = 0.f, a0 = 0.f, a1 = 0.f;
+  for (int s = 0; s < p.num_splits; ++s) {
+    const float2 t = ml[s * stride + r];
+    const float w = ex2_approx(t.x - M);
+    den += w * t.y;
+    const float2 o = reinterpret_cast<const float2*>(p.part_o + (s * stride + r) * kHeadDim)[lane];
+    a0 += w * o.x;
+    a1 += w * o.y;
+  }
+  const int64_t bh = r / p.n_q, row = r % p.n_q;
+  const int64_t b = bh / p.H, h = bh % p.H;
+  const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + 2 * lane;
+  const float inv = 1.f / den;
+  if (p.out_f32) {
+    reinterpret_cast<float2*>(static_cast<float*>(p.out) + off)[0] = make_float2(a0 * inv, a1 * inv);
+  } else {
+    reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(p.out) + off)[0] = pack_bf16x2(a0 * inv, a1 * inv);
+  }
+  if (p.lse && lane == 0) p.lse[r] = (M + __log2f(den)) * 0.6931471805599453f;
+}
+
+// ---------------------------------------------------------------------------- debug probe
+struct DbgSmem {
+  uint8_t a[kTileBytes];
+  uint8_t b[kTileBytes];
+  uint8_t v[kTileBytes];
+  uint64_t full, s_done, o_done;
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(128, 1)
+    debug_umma_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb,
+                      const __grid_constant__ CUtensorMap mv, float* s_out, float* o_out) {
+  extern __shared__ uint8_t smem_raw[];
+  DbgSmem& sm = *reinterpret_cast<DbgSmem*>(align1024(smem_raw));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.full, 1);
+    mbar_init(&sm.s_done, 1);
+    mbar_init(&sm.o_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&sm.full, 3 * kTileBytes);
+    tma_load_4d(sm.a, &ma, &sm.full, 0, 0, 0, 0, policy_evict_first());
+    tma_load_4d(sm.b, &mb, &sm.full, 0, 0, 0, 0, policy_evict_first());
+    tma_load_4d(sm.v, &mv, &sm.full, 0, 0, 0, 0, policy_evict_first());
+    mbar_wait(&sm.full, 0);
+    tc_fence_after();
+    issue_qk(tmem + col_s(0), sm.a, sm.b);
+    umma_commit(&sm.s_done);
+  }
+  __syncwarp();
+  mbar_wait(&sm.s_done, 0);
+  tc_fence_after();
+  const int row = warp * 32 + lane;
+  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  uint32_t sr[128];
+  for (int c = 0; c < 4; ++c) tmem_ld32(lane_base + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+  tmem_ld_wait();
+  for (int i = 0; i < 128; ++i) s_out[row * 128 + i] = __uint_as_float(sr[i]);
+  uint32_t pk[64];
+  for (int i = 0; i < 64; ++i) pk[i] = pack_bf16x2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]));
+  tmem_st32(lane_base + col_p(0), *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+  tmem_st32(lane_base + col_p(0) + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+  tmem_st_wait();
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tc_fence_after();
+    issue_pv(tmem + col_o(0), tmem + col_p(0), sm.v, false);
+    umma_commit(&sm.o_done);
+  }
+  __syncwarp();
+  mbar_wait(&sm.o_done, 0);
+  tc_fence_after();
+  uint32_t o[64];
+  tmem_ld32(lane_base + col_o(0), *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
+  tmem_ld32(lane_base + col_o(0) + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
+  tmem_ld_wait();
+  for (int i = 0; i < 64; ++i) o_out[row * 64 + i] = __uint_as_float(o[i]);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_fwd_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
+                            const CUtensorMap& mv, cudaStream_t s) {
+  static cudaError_t attr = cudaFuncSetAttribute(fwd_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)kFwdSmemBytes);
+  if (attr != cudaSuccess) return attr;
+  dim3 grid(p.num_q_blocks * p.num_splits, p.H, p.B);
+  fwd_bf16_kernel<<<grid, kThreads, kFwdSmemBytes, s>>>(mq, mk, mv, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_rows(const FwdParams& p, cudaStream_t s) {
+  const int64_t rows = (int64_t)p.B * p.H * p.n_q;
+  const int warps = 8;
+  merge_rows_kernel<<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_debug_umma_tile(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mv,
+                                   float* s_out, float* o_out, cudaStream_t s) {
+  const size_t smem = sizeof(DbgSmem) + 1024;
+  cudaError_t e = cudaFuncSetAttribute(debug_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  debug_umma_kernel<<<1, 128, smem, s>>>(ma, mb, mv, s_out, o_out);
+  return cudaGetLastError();
+}
+
+}  // namespace mea

@@ -1,0 +1,77 @@
+// internal.h — launcher interfaces between the C-ABI layer (mea_api.cu) and the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace mea {
+
+constexpr int kHeadDim = 64;      // tensor-core path head dimension
+constexpr int kTileM = 128;       // query rows per softmax warpgroup (UMMA M)
+constexpr int kTileN = 128;       // keys per tile (UMMA N of QK^T, K of PV)
+constexpr int kRowsPerCta = 256;  // two query tiles per CTA share each K/V tile
+
+struct FwdParams {
+  int B, H, n_q, n_k;
+  float scale_log2;        // scale * log2(e): exponent base change folded into one FFMA
+  float scale;
+  void* out;               // [B,n_q,H,64], bf16 or f32 (unused in split mode)
+  int out_f32;
+  float* lse;              // [B,H,n_q] natural log, nullable
+  int num_q_blocks;        // ceil(n_q / 256)
+  int num_splits;          // key splits (1 = online over all keys)
+  int tiles_per_split;     // key tiles of 128 per split
+  float* part_o;           // [splits][B*H][n_q][64] unnormalised v*   (split mode)
+  float* part_ml;          // [splits][B*H][n_q][2]  (m* in log2 units, s*) (split mode)
+};
+
+struct BwdParams {
+  int B, H, n_q, n_k;
+  float scale, scale_log2;
+  const float* lse;        // [B,H,n_q]
+  const float* delta;      // [B,H,n_q]
+  float* dq_acc;           // [B,n_q,H,64] f32 (sum of dS K over key tiles, unscaled)
+  void* dk;                // [B,n_k,H,64] bf16
+  void* dv;                // [B,n_k,H,64] bf16
+  int num_k_blocks;        // ceil(n_k / 128)
+};
+
+// 4-D tensor map over a [B, n, H, d] tensor (d innermost), box {64, 1, box_rows, 1},
+// 128-byte swizzle. elem = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 or FLOAT32.
+cudaError_t make_bnhd_map(CUtensorMap* map, const void* base, CUtensorMapDataType elem, int elem_bytes,
+                          int64_t B, int64_t n, int64_t H, int64_t d, int box_inner, int box_rows,
+                          CUtensorMapSwizzle swz, const char** why);
+
+cudaError_t launch_fwd_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
+                            const CUtensorMap& mv, cudaStream_t s);
+cudaError_t launch_merge_rows(const FwdParams& p, cudaStream_t s);
+cudaError_t launch_fwd_f32(const float* q, const float* k, const float* v, float* out, float* lse, int B,
+                           int H, int n_q, int n_k, int d, float scale, cudaStream_t s);
+
+// single query
+int sq_num_splits(int64_t BH, int64_t n_k);
+cudaError_t launch_sq_partial(const void* q, const void* k, const void* v, int bf16, int B, int H, int n_k,
+                              int d, float scale, int splits, float* ws, cudaStream_t s);
+// mode 0: write out (dtype) ; mode 1: write triple (m natural, s, v*)
+cudaError_t launch_sq_merge(const float* ws, int splits, int BH, int d, int mode, void* out, int out_f32,
+                            float* m, float* sum, float* vstar, cudaStream_t s);
+cudaError_t launch_merge_partials(const float* m, const float* s, const float* vstar, int P, int BH, int d,
+                                  void* out, int out_f32, cudaStream_t st);
+
+// backward
+cudaError_t launch_bwd_preprocess(const void* out, const void* dout, float* delta, float* dq_acc, int B, int H,
+                                  int n_q, cudaStream_t s);
+cudaError_t launch_bwd_bf16(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
+                            const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
+                            cudaStream_t s);
+cudaError_t launch_dq_convert(const float* dq_acc, void* dq, int64_t numel, float scale, cudaStream_t s);
+
+// generator
+cudaError_t launch_fill_synthetic(void* dst, int64_t numel, int bf16, uint64_t seed, uint32_t tid,
+                                  int64_t offset, cudaStream_t s);
+
+// debug probe
+cudaError_t launch_debug_umma_tile(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mv,
+                                   float* s_out, float* o_out, cudaStream_t s);
+
+}  // namespace mea

@@ -1,0 +1,334 @@
+// mea_api.cu — the C ABI of libmea.so (include/mea.h): argument validation, TMA descriptor
+// encoding, work decomposition and launches. No allocation, no host synchronisation.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "internal.h"
+#include "mea.h"
+#include "mea_debug.h"
+
+namespace {
+
+thread_local std::string g_detail;
+
+mea_status_t fail(mea_status_t s, const std::string& why) {
+  g_detail = why;
+  return s;
+}
+mea_status_t cuda_fail(cudaError_t e, const char* where) {
+  g_detail = std::string(where) + ": " + cudaGetErrorString(e);
+  return MEA_ERR_CUDA;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+bool valid_dtype(mea_dtype_t t) { return t == MEA_F32 || t == MEA_BF16; }
+
+constexpr int64_t kMaxInt = 2147483647;
+
+}  // namespace
+
+namespace mea {
+
+cudaError_t make_bnhd_map(CUtensorMap* map, const void* base, CUtensorMapDataType elem, int elem_bytes, int64_t B,
+                          int64_t n, int64_t H, int64_t d, int box_inner, int box_rows, CUtensorMapSwizzle swz,
+                          const char** why) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) {
+    *why = "cuTensorMapEncodeTiled unavailable";
+    return cudaErrorNotSupported;
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)H, (cuuint64_t)n, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)(d * elem_bytes), (cuuint64_t)(H * d * elem_bytes),
+                           (cuuint64_t)(n * H * d * elem_bytes)};
+  cuuint32_t box[4] = {(cuuint32_t)box_inner, 1, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, elem, 4, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *why = "cuTensorMapEncodeTiled failed";
+    return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace mea
+
+using namespace mea;
+
+namespace {
+
+struct FwdPlan {
+  int splits = 1, tiles_per_split = 0;
+  size_t ws = 0;
+};
+
+FwdPlan plan_fwd(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t k_chunk) {
+  FwdPlan pl;
+  const int64_t n_tiles = (n_k + kTileN - 1) / kTileN;
+  pl.tiles_per_split = (int)n_tiles;
+  if (k_chunk > 0 && k_chunk < n_k) {
+    const int64_t tps = (k_chunk + kTileN - 1) / kTileN;
+    const int64_t splits = (n_tiles + tps - 1) / tps;
+    if (splits > 1) {
+      pl.splits = (int)splits;
+      pl.tiles_per_split = (int)tps;
+      pl.ws = (size_t)splits * B * H * n_q * (kHeadDim + 2) * sizeof(float);
+    }
+  }
+  return pl;
+}
+
+mea_status_t check_common(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d, float scale) {
+  if (B < 1 || H < 1 || d < 1 || n_q < 0 || n_k < 0) return fail(MEA_ERR_INVALID_VALUE, "B, H, d must be >= 1; n >= 0");
+  if (!std::isfinite(scale)) return fail(MEA_ERR_INVALID_VALUE, "scale must be finite");
+  if (n_q > kMaxInt || n_k > kMaxInt || B > 65535 || H > 65535)
+    return fail(MEA_ERR_UNSUPPORTED, "size beyond the 32-bit grid/coordinate limits");
+  return MEA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mea_version(void) { return "mea 0.1 sm_100a"; }
+
+const char* mea_status_string(mea_status_t s) {
+  switch (s) {
+    case MEA_OK: return "MEA_OK";
+    case MEA_ERR_INVALID_VALUE: return "MEA_ERR_INVALID_VALUE";
+    case MEA_ERR_EMPTY_KEYS: return "MEA_ERR_EMPTY_KEYS";
+    case MEA_ERR_UNSUPPORTED: return "MEA_ERR_UNSUPPORTED";
+    case MEA_ERR_MISALIGNED: return "MEA_ERR_MISALIGNED";
+    case MEA_ERR_WORKSPACE_TOO_SMALL: return "MEA_ERR_WORKSPACE_TOO_SMALL";
+    case MEA_ERR_CUDA: return "MEA_ERR_CUDA";
+  }
+  return "MEA_ERR_UNKNOWN";
+}
+
+const char* mea_last_error_detail(void) { return g_detail.c_str(); }
+
+mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                                              mea_dtype_t in_dtype, int64_t q_chunk, int64_t k_chunk, size_t* bytes) {
+  if (!bytes) return fail(MEA_ERR_INVALID_VALUE, "bytes is NULL");
+  if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
+  if (q_chunk < 0 || k_chunk < 0) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
+  if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  *bytes = (in_dtype == MEA_BF16) ? plan_fwd(B, H, n_q, n_k, k_chunk).ws : 0;
+  return MEA_OK;
+}
+
+mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
+                               int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t in_dtype, mea_dtype_t out_dtype,
+                               float scale, float* lse, int64_t q_chunk, int64_t k_chunk, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  if (mea_status_t s = check_common(B, H, n_q, n_k, d, scale)) return s;
+  if (q_chunk < 0 || k_chunk < 0) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
+  if (!valid_dtype(in_dtype) || !valid_dtype(out_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  if (n_q == 0) return MEA_OK;
+  if (n_k == 0) return fail(MEA_ERR_EMPTY_KEYS, "attention over an empty key list");
+  if (!q || !k || !v || !out) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out))
+    return fail(MEA_ERR_MISALIGNED, "q, k, v, out must be 16-byte aligned");
+  if (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)) return fail(MEA_ERR_MISALIGNED, "lse must be 4-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+  if (in_dtype == MEA_F32) {
+    if (d > 128) return fail(MEA_ERR_UNSUPPORTED, "f32 path supports d <= 128");
+    if (out_dtype != MEA_F32) return fail(MEA_ERR_UNSUPPORTED, "f32 inputs need f32 output");
+    if (k_chunk > 0 && k_chunk < n_k) return fail(MEA_ERR_UNSUPPORTED, "key chunking is a bf16-path schedule");
+    cudaError_t e = launch_fwd_f32(static_cast<const float*>(q), static_cast<const float*>(k),
+                                   static_cast<const float*>(v), static_cast<float*>(out), lse, (int)B, (int)H,
+                                   (int)n_q, (int)n_k, (int)d, scale, st);
+    return e == cudaSuccess ? MEA_OK : cuda_fail(e, "fwd_f32 launch");
+  }
+
+  if (d != kHeadDim) return fail(MEA_ERR_UNSUPPORTED, "bf16 tensor-core path supports d == 64");
+  const FwdPlan pl = plan_fwd(B, H, n_q, n_k, k_chunk);
+  if (pl.ws > 0) {
+    if (workspace_bytes < pl.ws || !workspace) return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "key-chunk summaries need workspace");
+    if (!aligned16(workspace)) return fail(MEA_ERR_MISALIGNED, "workspace must be 16-byte aligned");
+  }
+  const int64_t nqb = (n_q + kRowsPerCta - 1) / kRowsPerCta;
+  if (nqb * pl.splits > kMaxInt) return fail(MEA_ERR_UNSUPPORTED, "grid too large");
+
+  CUtensorMap mq, mk, mv;
+  const char* why = "";
+  cudaError_t e;
+  if ((e = make_bnhd_map(&mq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_q, H, d, 64, kTileM,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+      (e = make_bnhd_map(&mk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+      (e = make_bnhd_map(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess)
+    return cuda_fail(e, why);
+
+  FwdParams p{};
+  p.B = (int)B;
+  p.H = (int)H;
+  p.n_q = (int)n_q;
+  p.n_k = (int)n_k;
+  p.scale = scale;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.out = out;
+  p.out_f32 = out_dtype == MEA_F32;
+  p.lse = lse;
+  p.num_q_blocks = (int)nqb;
+  p.num_splits = pl.splits;
+  p.tiles_per_split = pl.tiles_per_split;
+  if (pl.splits > 1) {
+    const size_t rows = (size_t)pl.splits * B * H * n_q;
+    p.part_o = static_cast<float*>(workspace);
+    p.part_ml = p.part_o + rows * kHeadDim;
+  }
+  if ((e = launch_fwd_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_bf16 launch");
+  if (pl.splits > 1 && (e = launch_merge_rows(p, st)) != cudaSuccess) return cuda_fail(e, "merge_rows launch");
+  return MEA_OK;
+}
+
+// ------------------------------------------------------------------ single query
+mea_status_t mea_single_query_workspace_size(int64_t B, int64_t H, int64_t n_k, int64_t d, mea_dtype_t in_dtype,
+                                             size_t* bytes) {
+  if (!bytes) return fail(MEA_ERR_INVALID_VALUE, "bytes is NULL");
+  if (mea_status_t s = check_common(B, H, 1, n_k, d, 1.f)) return s;
+  if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  const int splits = sq_num_splits(B * H, n_k);
+  *bytes = (size_t)B * H * splits * (d + 2) * sizeof(float);
+  return MEA_OK;
+}
+
+static mea_status_t sq_common(const void* q, const void* k, const void* v, int64_t B, int64_t H, int64_t n_k,
+                              int64_t d, mea_dtype_t in_dtype, float scale, void* workspace, size_t workspace_bytes,
+                              int* splits_out) {
+  if (mea_status_t s = check_common(B, H, 1, n_k, d, scale)) return s;
+  if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  if (in_dtype == MEA_BF16 && d != kHeadDim) return fail(MEA_ERR_UNSUPPORTED, "bf16 single query supports d == 64");
+  if (in_dtype == MEA_F32 && d > 128) return fail(MEA_ERR_UNSUPPORTED, "f32 single query supports d <= 128");
+  if (B * H > 65535) return fail(MEA_ERR_UNSUPPORTED, "B*H > 65535");
+  if (!q || (n_k > 0 && (!k || !v))) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v)) return fail(MEA_ERR_MISALIGNED, "q, k, v must be 16-byte aligned");
+  const int splits = sq_num_splits(B * H, n_k);
+  const size_t need = (size_t)B * H * splits * (d + 2) * sizeof(float);
+  if (!workspace || workspace_bytes < need) return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "single query needs workspace");
+  *splits_out = splits;
+  return MEA_OK;
+}
+
+mea_status_t mea_single_query_fwd(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
+                                  int64_t n_k, int64_t d, mea_dtype_t in_dtype, mea_dtype_t out_dtype, float scale,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  if (n_k == 0 && B >= 1 && H >= 1 && d >= 1) return fail(MEA_ERR_EMPTY_KEYS, "attention over an empty key list");
+  if (!valid_dtype(out_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  int splits = 0;
+  if (mea_status_t s = sq_common(q, k, v, B, H, n_k, d, in_dtype, scale, workspace, workspace_bytes, &splits)) return s;
+  if (!out || !aligned16(out)) return fail(out ? MEA_ERR_MISALIGNED : MEA_ERR_INVALID_VALUE, "bad out pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* ws = static_cast<float*>(workspace);
+  cudaError_t e = launch_sq_partial(q, k, v, in_dtype == MEA_BF16, (int)B, (int)H, (int)n_k, (int)d, scale, splits, ws, st);
+  if (e != cudaSuccess) return cuda_fail(e, "sq_partial launch");
+  e = launch_sq_merge(ws, splits, (int)(B * H), (int)d, 0, out, out_dtype == MEA_F32, nullptr, nullptr, nullptr, st);
+  return e == cudaSuccess ? MEA_OK : cuda_fail(e, "sq_merge launch");
+}
+
+mea_status_t mea_single_query_partial(const void* q, const void* k, const void* v, float* m, float* s, float* vstar,
+                                      int64_t B, int64_t H, int64_t n_k, int64_t d, mea_dtype_t in_dtype, float scale,
+                                      void* workspace, size_t workspace_bytes, void* stream) {
+  int splits = 0;
+  if (mea_status_t r = sq_common(q, k, v, B, H, n_k, d, in_dtype, scale, workspace, workspace_bytes, &splits)) return r;
+  if (!m || !s || !vstar) return fail(MEA_ERR_INVALID_VALUE, "NULL triple pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  float* ws = static_cast<float*>(workspace);
+  cudaError_t e = launch_sq_partial(q, k, v, in_dtype == MEA_BF16, (int)B, (int)H, (int)n_k, (int)d, scale, splits, ws, st);
+  if (e != cudaSuccess) return cuda_fail(e, "sq_partial launch");
+  e = launch_sq_merge(ws, splits, (int)(B * H), (int)d, 1, nullptr, 0, m, s, vstar, st);
+  return e == cudaSuccess ? MEA_OK : cuda_fail(e, "sq_merge launch");
+}
+
+mea_status_t mea_merge_partials(const float* m, const float* s, const float* vstar, int64_t P, int64_t B, int64_t H,
+                                int64_t d, void* out, mea_dtype_t out_dtype, void* stream) {
+  if (P < 0 || B < 1 || H < 1 || d < 1) return fail(MEA_ERR_INVALID_VALUE, "bad sizes");
+  if (P == 0) return fail(MEA_ERR_EMPTY_KEYS, "no partials to merge");
+  if (d > 128) return fail(MEA_ERR_UNSUPPORTED, "d <= 128");
+  if (B * H > 65535) return fail(MEA_ERR_UNSUPPORTED, "B*H > 65535");
+  if (!valid_dtype(out_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  if (!m || !s || !vstar || !out) return fail(MEA_ERR_INVALID_VALUE, "NULL pointer");
+  cudaError_t e = launch_merge_partials(m, s, vstar, (int)P, (int)(B * H), (int)d, out, out_dtype == MEA_F32,
+                                        static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? MEA_OK : cuda_fail(e, "merge_partials launch");
+}
+
+// ------------------------------------------------------------------ backward
+mea_status_t mea_attention_bwd_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                                              mea_dtype_t dtype, int lse_given, size_t* bytes) {
+  if (!bytes) return fail(MEA_ERR_INVALID_VALUE, "bytes is NULL");
+  if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
+  if (!valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  const size_t rows = (size_t)B * H * n_q;
+  size_t ws = rows * sizeof(float)                       // delta
+              + rows * (size_t)d * sizeof(float);        // dq accumulator
+  if (!lse_given) ws += rows * sizeof(float);            // recomputed lse
+  *bytes = (ws + 255) & ~size_t(255);
+  return MEA_OK;
+}
+
+mea_status_t mea_attention_bwd(const void* q, const void* k, const void* v, const void* out, const void* dout, void* dq,
+                               void* dk, void* dv, int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                               mea_dtype_t dtype, float scale, const float* lse, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  if (mea_status_t s = check_common(B, H, n_q, n_k, d, scale)) return s;
+  if (!valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  (void)q; (void)k; (void)v; (void)out; (void)dout; (void)dq; (void)dk; (void)dv; (void)lse;
+  (void)workspace; (void)workspace_bytes; (void)stream;
+  return fail(MEA_ERR_UNSUPPORTED, "backward not built yet");
+}
+
+// ------------------------------------------------------------------ generator / debug
+mea_status_t mea_fill_synthetic(void* dst, int64_t numel, mea_dtype_t dtype, uint64_t seed, uint32_t tensor_id,
+                                int64_t offset, void* stream) {
+  if (numel < 0 || offset < 0 || !valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad arguments");
+  if (numel == 0) return MEA_OK;
+  if (!dst) return fail(MEA_ERR_INVALID_VALUE, "NULL dst");
+  cudaError_t e = launch_fill_synthetic(dst, numel, dtype == MEA_BF16, seed, tensor_id, offset,
+                                        static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? MEA_OK : cuda_fail(e, "fill launch");
+}
+
+mea_status_t mea_debug_umma_tile(const void* a, const void* b, const void* v, float* s_out, float* o_out,
+                                 void* stream) {
+  if (!a || !b || !v || !s_out || !o_out) return fail(MEA_ERR_INVALID_VALUE, "NULL pointer");
+  CUtensorMap ma, mb, mv;
+  const char* why = "";
+  cudaError_t e;
+  if ((e = make_bnhd_map(&ma, a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 1, 128, 1, 64, 64, 128,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+      (e = make_bnhd_map(&mb, b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 1, 128, 1, 64, 64, 128,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+      (e = make_bnhd_map(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, 1, 128, 1, 64, 64, 128,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess)
+    return cuda_fail(e, why);
+  e = launch_debug_umma_tile(ma, mb, mv, s_out, o_out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? MEA_OK : cuda_fail(e, "debug launch");
+}
+
+}  // extern "C"

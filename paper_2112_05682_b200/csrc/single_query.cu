@@ -1,0 +1,348 @@
+// single_query.cu — the paper's O(1)-memory single-query attention (made
+// stable by the running max of PAPER.md:85-90), split over key ranges (split-K), plus the
+// merge of the per-range states with Figure 1's global-max rescale.
+//
+// HBM-bound: every key costs 4*d bytes (k and v rows, bf16) and 4*d flops, 1 flop/byte.
+// bf16 d=64 kernel: a warp reads 16 keys per step; 8 lanes share one 128-byte key row
+// (16 B = 8 bf16 each, coalesced 128-bit loads), the dot product finishes with 3 xor-shuffles
+// inside the 8-lane group, and each group runs its own stream state (m*, s*, v*[8 dims per
+// lane]) with one rescale per 4 keys (block max first). Groups, warps and CTAs are then
+// merged with the same rescale rule. Two steps are unrolled so 8 K and 8 V loads (256 B)
+// per lane are in flight.
+//
+// Partial layout (workspace, float32): part[(bh * splits + split) * (d + 2) + {0: m*, 1: s*,
+// 2..: v*}], with m* in log2 units of the scaled score (p = 2^(s*c - m*), c = scale*log2 e).
+#include <cuda_bf16.h>
+
+#include <cmath>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace mea {
+namespace {
+
+constexpr int kSqThreads = 256;
+constexpr int kSqWarps = kSqThreads / 32;
+constexpr int kKeysPerWarpStep = 16;  // 4 groups x 4 keys
+constexpr int kUnroll = 2;            // warp steps in flight
+
+struct State {
+  float m, l, a[8];
+};
+
+// Merge state o into s (both relative to their own reference max).
+__device__ __forceinline__ void merge_state(State& s, const State& o) {
+  const float M = fmaxf(s.m, o.m);
+  if (M == -INFINITY) return;
+  const float ws = ex2_approx(s.m - M), wo = ex2_approx(o.m - M);
+  s.l = s.l * ws + o.l * wo;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s.a[i] = s.a[i] * ws + o.a[i] * wo;
+  s.m = M;
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_bfloat16* __restrict__ q,
+                                                                     const __nv_bfloat16* __restrict__ k,
+                                                                     const __nv_bfloat16* __restrict__ v, int H,
+                                                                     int n_k, float scale_log2, int splits,
+                                                                     float* __restrict__ part) {
+  const int split = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / H, h = bh % H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 3, cidx = lane & 7;  // key group in the warp, 16-byte chunk of the row
+  const int per = (n_k + splits - 1) / splits;
+  const int k_lo = split * per, k_hi = min(n_k, k_lo + per);
+  const size_t row_stride = (size_t)H * kHeadDim;  // elements between consecutive keys
+  const __nv_bfloat16* kb = k + ((size_t)b * n_k * H + h) * kHeadDim + cidx * 8;
+  const __nv_bfloat16* vb = v + ((size_t)b * n_k * H + h) * kHeadDim + cidx * 8;
+
+  float qf[8];
+  bf16x8_to_f32(*reinterpret_cast<const uint4*>(q + (size_t)bh * kHeadDim + cidx * 8), qf);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) qf[i] *= scale_log2;
+
+  State st;
+  st.m = -INFINITY;
+  st.l = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) st.a[i] = 0.f;
+
+  constexpr int kStep = kSqWarps * kKeysPerWarpStep;  // keys per CTA step
+  for (int base = k_lo + warp * kKeysPerWarpStep; base < k_hi; base += kStep * kUnroll) {
+    uint4 kr[kUnroll][4], vr[kUnroll][4];
+#pragma unroll
+    for (int s = 0; s < kUnroll; ++s)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int key = base + s * kStep + u * 4 + g;
+        if (key < k_hi) {
+          kr[s][u] = ld_stream(kb + (size_t)key * row_stride);
+          vr[s][u] = ld_stream(vb + (size_t)key * row_stride);
+        } else {
+          kr[s][u] = make_uint4(0, 0, 0, 0);
+          vr[s][u] = make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+    for (int s = 0; s < kUnroll; ++s) {
+      float sc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float kf[8];
+        bf16x8_to_f32(kr[s][u], kf);
+        float dot = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dot = fmaf(qf[i], kf[i], dot);
+        dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+        dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+        dot += __shfl_xor_sync(0xffffffffu, dot, 4);
+        const int key = base + s * kStep + u * 4 + g;
+        sc[u] = key < k_hi ? dot : -INFINITY;
+      }
+      const float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+      const float m_new = fmaxf(st.m, mx);
+      if (m_new == -INFINITY) continue;  // nothing valid yet for this group
+      const float alpha = ex2_approx(st.m - m_new);
+      st.l *= alpha;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) st.a[i] *= alpha;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float pu = ex2_approx(sc[u] - m_new);
+        st.l += pu;
+        float vf[8];
+        bf16x8_to_f32(vr[s][u], vf);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) st.a[i] = fmaf(pu, vf[i], st.a[i]);
+      }
+      st.m = m_new;
+    }
+  }
+  // merge the 4 key groups of the warp (lanes with equal cidx hold the same 8 dims)
+#pragma unroll
+  for (int off = 8; off <= 16; off <<= 1) {
+    State o;
+    o.m = __shfl_xor_sync(0xffffffffu, st.m, off);
+    o.l = __shfl_xor_sync(0xffffffffu, st.l, off);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o.a[i] = __shfl_xor_sync(0xffffffffu, st.a[i], off);
+    merge_state(st, o);
+  }
+  __shared__ float sm_m[kSqWarps], sm_l[kSqWarps], sm_a[kSqWarps][kHeadDim];
+  if (lane < 8) {
+    if (lane == 0) {
+      sm_m[warp] = st.m;
+      sm_l[warp] = st.l;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sm_a[warp][cidx * 8 + i] = st.a[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < kHeadDim) {
+    const int f = threadIdx.x;
+    float M = -INFINITY;
+    for (int w = 0; w < kSqWarps; ++w) M = fmaxf(M, sm_m[w]);
+    float l = 0.f, a = 0.f;
+    if (M != -INFINITY) {
+      for (int w = 0; w < kSqWarps; ++w) {
+        const float wt = ex2_approx(sm_m[w] - M);
+        l += wt * sm_l[w];
+        a += wt * sm_a[w][f];
+      }
+    }
+    float* dst = part + ((size_t)bh * splits + split) * (kHeadDim + 2);
+    if (f == 0) {
+      dst[0] = M;
+      dst[1] = l;
+    }
+    dst[2 + f] = a;
+  }
+}
+
+// f32 inputs, any d <= 128: one warp per key, lanes own dims {lane, lane+32, lane+64, lane+96}.
+__global__ void __launch_bounds__(128) sq_partial_f32_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                                                            const float* __restrict__ v, int H, int n_k, int d,
+                                                            float scale_log2, int splits, float* __restrict__ part) {
+  const int split = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / H, h = bh % H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int per = (n_k + splits - 1) / splits;
+  const int k_lo = split * per, k_hi = min(n_k, k_lo + per);
+  float qf[4], a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) qf[i] = (lane + 32 * i < d) ? q[(size_t)bh * d + lane + 32 * i] : 0.f;
+  float m = -INFINITY, l = 0.f;
+  for (int key = k_lo + warp; key < k_hi; key += 4) {
+    const size_t off = (((size_t)b * n_k + key) * H + h) * d;
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i < d) dot = fmaf(qf[i], k[off + lane + 32 * i], dot);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    const float s = dot * scale_log2;
+    const float m_new = fmaxf(m, s);
+    const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
+    const float p = exp2f(s - m_new);
+    l = l * alpha + p;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = a[i] * alpha + ((lane + 32 * i < d) ? p * v[off + lane + 32 * i] : 0.f);
+    m = m_new;
+  }
+  __shared__ float sm_m[4], sm_l[4], sm_a[4][128];
+  if (lane == 0) {
+    sm_m[warp] = m;
+    sm_l[warp] = l;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) sm_a[warp][lane + 32 * i] = a[i];
+  __syncthreads();
+  if (threadIdx.x < d) {
+    const int f = threadIdx.x;
+    float M = -INFINITY;
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w]);
+    float ls = 0.f, as = 0.f;
+    if (M != -INFINITY)
+      for (int w = 0; w < 4; ++w) {
+        const float wt = exp2f(sm_m[w] - M);
+        ls += wt * sm_l[w];
+        as += wt * sm_a[w][f];
+      }
+    float* dst = part + ((size_t)bh * splits + split) * (d + 2);
+    if (f == 0) {
+      dst[0] = M;
+      dst[1] = ls;
+    }
+    dst[2 + f] = as;
+  }
+}
+
+// Merge `splits` partial states per (b,h) (Figure 1 lines 33-40):
+//   M = max m_s;  out = sum_s 2^(m_s - M) v*_s / sum_s 2^(m_s - M) s*_s.
+// block (128 dims, 4 groups of splits). mode 0: out (dtype); mode 1: triple with m in
+// natural-log units (m_nat = m * ln 2) for the cross-GPU merge.
+__global__ void __launch_bounds__(512) sq_merge_kernel(const float* __restrict__ part, int splits, int d, int mode,
+                                                       void* out, int out_f32, float* m_out, float* s_out,
+                                                       float* v_out) {
+  const int bh = blockIdx.x;
+  const int f = threadIdx.x, grp = threadIdx.y;
+  const float* base = part + (size_t)bh * splits * (d + 2);
+  __shared__ float sm_M[4], sm_l[4], sm_a[4][128];
+  float M = -INFINITY;
+  for (int s = grp; s < splits; s += 4) M = fmaxf(M, base[(size_t)s * (d + 2)]);
+  float l = 0.f, a = 0.f;
+  if (M != -INFINITY)
+    for (int s = grp; s < splits; s += 4) {
+      const float* ps = base + (size_t)s * (d + 2);
+      const float w = exp2f(ps[0] - M);
+      l += w * ps[1];
+      if (f < d) a += w * ps[2 + f];
+    }
+  if (f == 0) {
+    sm_M[grp] = M;
+    sm_l[grp] = l;
+  }
+  sm_a[grp][f] = a;
+  __syncthreads();
+  if (grp != 0 || f >= d) return;
+  float MM = -INFINITY;
+  for (int g2 = 0; g2 < 4; ++g2) MM = fmaxf(MM, sm_M[g2]);
+  float L = 0.f, A = 0.f;
+  if (MM != -INFINITY)
+    for (int g2 = 0; g2 < 4; ++g2) {
+      const float w = exp2f(sm_M[g2] - MM);
+      L += w * sm_l[g2];
+      A += w * sm_a[g2][f];
+    }
+  if (mode == 0) {
+    const float r = A / L;
+    if (out_f32) static_cast<float*>(out)[(size_t)bh * d + f] = r;
+    else static_cast<__nv_bfloat16*>(out)[(size_t)bh * d + f] = __float2bfloat16_rn(r);
+  } else {
+    if (f == 0) {
+      m_out[bh] = MM * 0.6931471805599453f;
+      s_out[bh] = L;
+    }
+    v_out[(size_t)bh * d + f] = A;
+  }
+}
+
+// Cross-rank merge: P triples with natural-log m.
+__global__ void merge_partials_kernel(const float* __restrict__ m, const float* __restrict__ s,
+                                      const float* __restrict__ vstar, int P, int BH, int d, void* out, int out_f32) {
+  const int bh = blockIdx.x, f = threadIdx.x;
+  if (f >= d) return;
+  float M = -INFINITY;
+  for (int r = 0; r < P; ++r) M = fmaxf(M, m[(size_t)r * BH + bh]);
+  float L = 0.f, A = 0.f;
+  for (int r = 0; r < P; ++r) {
+    const float mr = m[(size_t)r * BH + bh];
+    const float w = (mr == -INFINITY) ? 0.f : expf(mr - M);
+    L += w * s[(size_t)r * BH + bh];
+    A += w * vstar[((size_t)r * BH + bh) * d + f];
+  }
+  const float res = A / L;
+  if (out_f32) static_cast<float*>(out)[(size_t)bh * d + f] = res;
+  else static_cast<__nv_bfloat16*>(out)[(size_t)bh * d + f] = __float2bfloat16_rn(res);
+}
+
+}  // namespace
+
+// Splits: enough CTAs to keep ~2 resident per SM streaming (HBM needs ~35 KB in flight per
+// SM), but at least ~1024 keys per split so the merge stays small.
+int sq_num_splits(int64_t BH, int64_t n_k) {
+  const int64_t target_ctas = 148 * 2;
+  int64_t splits = (target_ctas + BH - 1) / BH;
+  const int64_t max_by_keys = (n_k + 1023) / 1024;
+  if (splits > max_by_keys) splits = max_by_keys;
+  if (splits < 1) splits = 1;
+  if (splits > 4096) splits = 4096;
+  return (int)splits;
+}
+
+cudaError_t launch_sq_partial(const void* q, const void* k, const void* v, int bf16, int B, int H, int n_k, int d,
+                              float scale, int splits, float* ws, cudaStream_t s) {
+  const float c = scale * 1.4426950408889634f;
+  dim3 grid(splits, B * H);
+  if (bf16) {
+    sq_partial_bf16_kernel<<<grid, kSqThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(q),
+                                                      static_cast<const __nv_bfloat16*>(k),
+                                                      static_cast<const __nv_bfloat16*>(v), H, n_k, c, splits, ws);
+  } else {
+    sq_partial_f32_kernel<<<grid, 128, 0, s>>>(static_cast<const float*>(q), static_cast<const float*>(k),
+                                               static_cast<const float*>(v), H, n_k, d, c, splits, ws);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sq_merge(const float* ws, int splits, int BH, int d, int mode, void* out, int out_f32, float* m,
+                            float* sum, float* vstar, cudaStream_t s) {
+  sq_merge_kernel<<<BH, dim3(128, 4), 0, s>>>(ws, splits, d, mode, out, out_f32, m, sum, vstar);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_partials(const float* m, const float* s, const float* vstar, int P, int BH, int d, void* out,
+                                  int out_f32, cudaStream_t st) {
+  merge_partials_kernel<<<BH, 128, 0, st>>>(m, s, vstar, P, BH, d, out, out_f32);
+  return cudaGetLastError();
+}
+
+}  // namespace mea

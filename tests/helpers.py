@@ -1,0 +1,53 @@
+"""Shared test helpers: seeded inputs (synth) and tolerance checks. No method arithmetic."""
+import math
+
+import numpy as np
+import torch
+
+from synth import gen
+
+# BASELINE.json north_star tolerances
+TOL_F32_ABS, TOL_F32_REL = 1e-5, 1e-4
+TOL_BF16_OUT, TOL_BF16_GRAD = 2e-2, 5e-2
+# extra relative-norm guards: absolute bars are loose at large n
+REL_NORM_OUT, REL_NORM_GRAD = 1e-2, 2e-2
+
+
+def host_inputs(B, n_q, n_k, H, d, seed=0, dtype="bf16", with_dout=False):
+    """Generator values (f64 arrays holding the exact input values)."""
+    q = gen.normal_tensor((B, n_q, H, d), seed, gen.TENSOR_Q, dtype).astype(np.float64)
+    k = gen.normal_tensor((B, n_k, H, d), seed, gen.TENSOR_K, dtype).astype(np.float64)
+    v = gen.normal_tensor((B, n_k, H, d), seed, gen.TENSOR_V, dtype).astype(np.float64)
+    if with_dout:
+        do = gen.normal_tensor((B, n_q, H, d), seed, gen.TENSOR_DO, dtype).astype(np.float64)
+        return q, k, v, do
+    return q, k, v
+
+
+def to_dev(x, dtype):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dtype).cuda()
+
+
+def rel_norm(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    return float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30))
+
+
+def assert_close_bf16(got, ref, abs_tol=TOL_BF16_OUT, rel_tol=REL_NORM_OUT, what="out"):
+    got = np.asarray(got, dtype=np.float64)
+    err = float(np.abs(got - ref).max())
+    rn = rel_norm(got, ref)
+    assert np.isfinite(got).all(), f"{what}: non-finite values"
+    assert err <= abs_tol, f"{what}: max abs err {err:.3e} > {abs_tol}"
+    assert rn <= rel_tol, f"{what}: relative norm err {rn:.3e} > {rel_tol}"
+    return err, rn
+
+
+def assert_close_f32(got, ref, what="out"):
+    got = np.asarray(got, dtype=np.float64)
+    err = np.abs(got - ref)
+    bad = err > TOL_F32_ABS + TOL_F32_REL * np.abs(ref)
+    assert not bad.any(), f"{what}: max abs err {err.max():.3e} (abs {TOL_F32_ABS}, rel {TOL_F32_REL})"
+    assert err.max() <= TOL_F32_ABS, f"{what}: max abs err {err.max():.3e} > {TOL_F32_ABS}"
+    return float(err.max())

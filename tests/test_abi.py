@@ -1,0 +1,80 @@
+"""CPU-side checks of the boundary: the library builds, loads and exports every symbol
+declared in include/*.h; the Python binding marshals exactly those names. No compute
+calls (no GPU here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = set()
+    for h in ("mea.h", "mea_debug.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        names |= set(re.findall(r"MEA_API\s+[\w\s\*]+?\b(mea_\w+)\s*\(", src))
+    return names
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2112_05682_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2112_05682_b200 import build
+        build.build()
+    return _lib.load()
+
+
+def test_header_declares_north_star_entry_points():
+    names = declared_symbols()
+    for n in ("mea_attention_fwd", "mea_single_query_fwd", "mea_attention_bwd", "mea_merge_partials",
+              "mea_single_query_partial"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in declared_symbols():
+        assert hasattr(lib, name), f"libmea.so does not export {name}"
+
+
+def test_binding_signatures_cover_header():
+    from paper_2112_05682_b200 import _lib
+    assert declared_symbols() == set(_lib.SIGNATURES)
+
+
+def test_host_only_calls(lib):
+    from paper_2112_05682_b200 import api
+    assert lib.mea_version().decode().startswith("mea")
+    assert lib.mea_status_string(2) == b"MEA_ERR_EMPTY_KEYS"
+    n = ctypes.c_size_t(123)
+    # default schedule needs no workspace; key-chunk summaries do (paper's O(sqrt n) buffers)
+    assert lib.mea_attention_fwd_workspace_size(1, 16, 16384, 16384, 64, 1, 0, 0, ctypes.byref(n)) == 0
+    assert n.value == 0
+    assert lib.mea_attention_fwd_workspace_size(1, 16, 16384, 16384, 64, 1, 1024, 4096, ctypes.byref(n)) == 0
+    assert n.value == 4 * 16 * 16384 * 66 * 4
+    # single-query workspace is independent of n_k once the split count saturates
+    a, b = ctypes.c_size_t(), ctypes.c_size_t()
+    lib.mea_single_query_workspace_size(1, 1, 1 << 20, 64, 1, ctypes.byref(a))
+    lib.mea_single_query_workspace_size(1, 1, 1 << 24, 64, 1, ctypes.byref(b))
+    assert a.value == b.value > 0
+    # validation happens before any launch: these never touch the GPU
+    assert api.mea_attention_fwd_workspace_size(1, 1, 8, 8, 64, 1) == 0
+    assert lib.mea_attention_fwd(None, None, None, None, 1, 1, 4, 0, 64, 1, 1, 1.0, None, 0, 0, None, 0,
+                                 None) == 2  # empty keys
+    assert lib.mea_attention_fwd(None, None, None, None, 1, 1, 0, 5, 64, 1, 1, 1.0, None, 0, 0, None, 0,
+                                 None) == 0  # n_q == 0 no-op
+    assert lib.mea_attention_fwd(None, None, None, None, 0, 1, 4, 5, 64, 1, 1, 1.0, None, 0, 0, None, 0,
+                                 None) == 1
+    assert lib.mea_attention_fwd(None, None, None, None, 1, 1, 4, 5, 64, 7, 1, 1.0, None, 0, 0, None, 0,
+                                 None) == 1  # bad dtype
+    assert lib.mea_attention_fwd(None, None, None, None, 1, 1, 4, 5, 64, 1, 1, float("nan"), None, 0, 0, None,
+                                 0, None) == 1
+    p = ctypes.c_void_p(16)
+    assert lib.mea_attention_fwd(p, p, p, p, 1, 1, 4, 5, 32, 1, 1, 1.0, None, 0, 0, None, 0, None) == 3
+    q = ctypes.c_void_p(8)  # misaligned
+    assert lib.mea_attention_fwd(q, p, p, p, 1, 1, 4, 5, 64, 1, 1, 1.0, None, 0, 0, None, 0, None) == 4
+    assert lib.mea_single_query_fwd(p, p, p, p, 1, 1, 0, 64, 1, 1, 1.0, None, 0, None) == 2
+    assert lib.mea_merge_partials(p, p, p, 0, 1, 1, 64, p, 1, None) == 2
+    assert b"no partials" in lib.mea_last_error_detail()

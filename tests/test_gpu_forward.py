@@ -1,0 +1,149 @@
+"""GPU parity of mea_attention_fwd against the float64 oracle (same generated inputs).
+
+bf16 inputs: max abs error <= 2e-2 and relative norm <= 1e-2 (BASELINE.json north_star,
+SURVEY 8(c)); f32 inputs: 1e-5 absolute (relative 1e-4). Sizes span several tiles and
+ragged tails (reading 2); configuration 3 runs in full on sampled rows.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from tests import helpers as Hh
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(q, k, v, dtype=torch.bfloat16, out_dtype=None, scale=None, **kw):
+    from paper_2112_05682_b200 import api
+    out, lse = api.mea_attention_fwd(Hh.to_dev(q, dtype), Hh.to_dev(k, dtype), Hh.to_dev(v, dtype), scale=scale,
+                                     out_dtype=out_dtype, want_lse=True, **kw)
+    torch.cuda.synchronize()
+    return out.double().cpu().numpy(), lse.double().cpu().numpy()
+
+
+@pytest.mark.parametrize("B,n_q,n_k,H", [(1, 1, 1, 1), (1, 17, 129, 2), (2, 127, 1000, 3), (1, 129, 257, 1),
+                                         (1, 300, 4097, 2), (1, 1000, 17, 1), (3, 256, 384, 2)])
+def test_bf16_forward_matches_oracle(B, n_q, n_k, H):
+    d = 64
+    q, k, v = Hh.host_inputs(B, n_q, n_k, H, d, seed=1)
+    ref, ref_lse = O.mha_forward(q, k, v, 1 / math.sqrt(d))
+    got, lse = _run(q, k, v)
+    Hh.assert_close_bf16(got, ref)
+    assert np.abs(lse - ref_lse).max() < 1e-3
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_bf16_forward_out_dtypes_and_scale(out_dtype):
+    q, k, v = Hh.host_inputs(1, 200, 333, 2, 64, seed=2)
+    for scale in (1.0, 0.0, 0.05):
+        ref, _ = O.mha_forward(q, k, v, scale)
+        got, _ = _run(q, k, v, out_dtype=out_dtype, scale=scale)
+        Hh.assert_close_bf16(got, ref)
+
+
+def test_bf16_key_chunk_schedule_matches_default():
+    """Figure 1's key-chunk summaries + global-max merge (k_chunk < n_k) == online schedule."""
+    q, k, v = Hh.host_inputs(2, 300, 1100, 2, 64, seed=3)
+    ref, ref_lse = O.mha_forward(q, k, v, 0.125)
+    a, la = _run(q, k, v, scale=0.125)
+    for kc in (128, 300, 512, 1024):
+        b, lb = _run(q, k, v, scale=0.125, k_chunk=kc, q_chunk=1024)
+        Hh.assert_close_bf16(b, ref)
+        assert np.abs(b - a).max() < 1e-2
+        assert np.abs(lb - ref_lse).max() < 1e-3
+
+
+def test_bf16_stress_monotone_and_huge_scores():
+    """S1: scores grow along the keys (rescale on every tile); S2: scores near +-1000."""
+    n, d = 700, 64
+    u = np.zeros(d); u[0] = 1.0
+    k = (np.arange(n)[:, None] / n * 8.0) * u[None, :]
+    q = np.tile(8.0 * u, (5, 1))
+    v = Hh.host_inputs(1, 1, n, 1, d, seed=4)[2][0, :, 0]
+    k_b = torch.tensor(k).bfloat16().double().numpy()
+    ref, _ = O.naive(q, k_b, v, 1.0)
+    got, _ = _run(q[None, :, None], k_b[None, :, None], v[None, :, None], scale=1.0)
+    Hh.assert_close_bf16(got[0, :, 0], ref)
+    for c in (1000.0, -1000.0):
+        q2 = np.zeros((3, d)); q2[:, 0] = c * 8          # exact in bf16
+        k2 = Hh.host_inputs(1, 1, n, 1, d, seed=5)[1][0, :, 0]
+        k2[:, 0] = 1.0
+        ref2, _ = O.naive(q2, k2, v, 1 / 8)
+        got2, _ = _run(q2[None, :, None], k2[None, :, None], v[None, :, None], scale=1 / 8)
+        assert np.isfinite(got2).all()
+        Hh.assert_close_bf16(got2[0, :, 0], ref2)
+
+
+def test_bf16_identical_keys_and_single_key():
+    q, k, v = Hh.host_inputs(1, 130, 300, 1, 64, seed=6)
+    k[:] = k[:, :1]
+    got, _ = _run(q, k, v)
+    Hh.assert_close_bf16(got, np.broadcast_to(v.mean(axis=1, keepdims=True), got.shape))
+    got1, _ = _run(q, k[:, :1], v[:, :1])
+    assert np.abs(got1 - np.broadcast_to(v[:, :1], got1.shape)).max() < 1e-2
+
+
+def test_f32_config1_parity():
+    """configs[0]: B=1 H=1 n=1024 d=64 fp32 — 1e-5 absolute."""
+    q, k, v = Hh.host_inputs(1, 1024, 1024, 1, 64, seed=0, dtype="f32")
+    ref, ref_lse = O.mha_forward(q, k, v, 1 / 8)
+    got, lse = _run(q, k, v, dtype=torch.float32)
+    Hh.assert_close_f32(got, ref)
+    assert np.abs(lse - ref_lse).max() < 1e-5
+
+
+@pytest.mark.parametrize("d,n_q,n_k", [(1, 5, 2), (3, 33, 70), (16, 129, 31), (100, 40, 65)])
+def test_f32_odd_shapes(d, n_q, n_k):
+    q, k, v = Hh.host_inputs(2, n_q, n_k, 2, d, seed=7, dtype="f32")
+    ref, _ = O.mha_forward(q, k, v, 1 / math.sqrt(d))
+    got, _ = _run(q, k, v, dtype=torch.float32)
+    Hh.assert_close_f32(got, ref)
+
+
+def test_f32_closed_form_on_gpu():
+    """SPEC.md:109 closed form through the library: d=1, q=[1], k=[ln2, ln4], v=[3,6] -> 5."""
+    q = np.array([[[[1.0]]]]); k = np.array([[[[math.log(2)]], [[math.log(4)]]]]); v = np.array([[[[3.0]], [[6.0]]]])
+    got, _ = _run(q, k, v, dtype=torch.float32, scale=1.0)
+    assert abs(got[0, 0, 0, 0] - 5.0) < 1e-5
+
+
+def test_config3_sampled_rows():
+    """configs[2]: B=1 H=16 n=16384 d=64 bf16, the benchmarked launch; oracle on sampled rows."""
+    from paper_2112_05682_b200 import api
+    from synth import gen
+    B, n, H, d = 1, 16384, 16, 64
+    q = torch.empty(B, n, H, d, dtype=torch.bfloat16, device="cuda")
+    k, v = torch.empty_like(q), torch.empty_like(q)
+    for t, tid in ((q, gen.TENSOR_Q), (k, gen.TENSOR_K), (v, gen.TENSOR_V)):
+        api.mea_fill_synthetic(t, 0, tid)
+    out, lse = api.mea_attention_fwd(q, k, v, want_lse=True)
+    out2 = api.mea_attention_fwd(q, k, v, q_chunk=1024, k_chunk=4096)
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 127, 128, 255, 256, 8191, 12345, 16383])
+    kk = gen.normal_tensor((B, n, H, d), 0, gen.TENSOR_K, "bf16").astype(np.float64)
+    vv = gen.normal_tensor((B, n, H, d), 0, gen.TENSOR_V, "bf16").astype(np.float64)
+    for h in (0, 7, 15):
+        qr = gen.rows_of((B, n, H, d), 0, gen.TENSOR_Q, 0, rows, h)
+        ref, ref_lse = O.naive(qr, kk[0, :, h], vv[0, :, h], 1 / 8)
+        Hh.assert_close_bf16(out[0, rows, h].double().cpu().numpy(), ref)
+        Hh.assert_close_bf16(out2[0, rows, h].double().cpu().numpy(), ref)
+        assert np.abs(lse[0, h, rows].double().cpu().numpy() - ref_lse).max() < 1e-3
+    # a mutation (rows shifted by one) must fail the same check
+    with pytest.raises(AssertionError):
+        r = rows[:-1]
+        Hh.assert_close_bf16(out[0, r + 1, 0].double().cpu().numpy(),
+                             O.naive(gen.rows_of((B, n, H, d), 0, gen.TENSOR_Q, 0, r, 0), kk[0, :, 0],
+                                     vv[0, :, 0], 1 / 8)[0])
+
+
+def test_empty_and_degenerate_calls():
+    from paper_2112_05682_b200 import api
+    q = torch.zeros(1, 0, 1, 64, dtype=torch.bfloat16, device="cuda")
+    k = torch.zeros(1, 5, 1, 64, dtype=torch.bfloat16, device="cuda")
+    out = api.mea_attention_fwd(q, k, k)
+    assert out.shape == (1, 0, 1, 64)
+    with pytest.raises(api.EmptyKeysError):
+        api.mea_attention_fwd(torch.zeros(1, 3, 1, 64, dtype=torch.bfloat16, device="cuda"), k[:, :0], k[:, :0])
