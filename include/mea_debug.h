@@ -16,6 +16,16 @@
 extern "C" {
 #endif
 
+/*
+ * Launch profiling (bench.py's roofline and launch count). While enabled, every kernel
+ * libmea launches is bracketed by a pair of CUDA events recorded on its launching
+ * stream. mea_profile_read synchronises those events and writes
+ *   "name count total_ms\n" per kernel into buf (truncated to cap bytes), then clears
+ * the record. Host-side bookkeeping only; off by default.
+ */
+MEA_API void mea_profile_enable(int on);
+MEA_API mea_status_t mea_profile_read(char* buf, size_t cap);
+
 MEA_API mea_status_t mea_debug_umma_tile(const void* a, const void* b, const void* v, float* s_out,
                                  float* o_out, void* stream);
 

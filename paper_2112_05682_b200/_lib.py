@@ -30,6 +30,8 @@ SIGNATURES = {
     "mea_attention_bwd_workspace_size": (_st, [_i64, _i64, _i64, _i64, _i64, _st, _c.c_int, _c.POINTER(_sz)]),
     "mea_fill_synthetic": (_st, [_vp, _i64, _st, _c.c_uint64, _c.c_uint32, _i64, _vp]),
     "mea_debug_umma_tile": (_st, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "mea_profile_enable": (None, [_c.c_int]),
+    "mea_profile_read": (_st, [_c.c_char_p, _sz]),
 }
 
 _lib = None

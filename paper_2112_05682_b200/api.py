@@ -204,3 +204,19 @@ def mea_debug_umma_tile(a, b, v):
     o = torch.empty((128, 64), dtype=torch.float32, device=a.device)
     _check(_lib.load().mea_debug_umma_tile(_ptr(a), _ptr(b), _ptr(v), _ptr(s), _ptr(o), _stream(a.device)))
     return s, o
+
+
+# ------------------------------------------------------------------------ launch profiling
+def profile_enable(on=True):
+    _lib.load().mea_profile_enable(1 if on else 0)
+
+
+def profile_read():
+    """{kernel name: (launch count, total ms)} since the last read (synchronises)."""
+    buf = ctypes.create_string_buffer(1 << 14)
+    _check(_lib.load().mea_profile_read(buf, len(buf)))
+    res = {}
+    for line in buf.value.decode().splitlines():
+        name, cnt, ms = line.split()
+        res[name] = (int(cnt), float(ms))
+    return res

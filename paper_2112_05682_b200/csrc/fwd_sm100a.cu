@@ -15,12 +15,17 @@
 //
 // CTA = 2 query tiles (256 rows) of one (b, h) sharing every K/V tile:
 //   warp 0      TMA producer: Q0,Q1 once, then a 4-stage K/V ring (mbarrier full/empty)
-//   warp 1      MMA issuer (one thread): S0,S1 = Q K^T; O0,O1 += P V; commits -> mbarriers
+//   warp 1      MMA issuer (one elected lane): S0,S1 = Q K^T; O0,O1 += P V; commits -> mbarriers
 //   warp 2      TMEM allocator
-//   warps 4-7   softmax warpgroup for query tile 0 (one thread = one row = one TMEM lane)
-//   warps 8-11  softmax warpgroup for query tile 1
+//   warps 4-11  softmax for query tile 0: warps 4-7 take score columns 0-63 of each key tile,
+//               warps 8-11 columns 64-127 (a thread = one row-half = one TMEM lane)
+//   warps 12-19 softmax for query tile 1, same split
+// Splitting each row over two threads gives 4 softmax warps per SM sub-partition: enough
+// independent instruction streams to keep the exponential units busy (one warp per SMSP
+// reached only ~0.5 IPC on its dependency chains). The halves exchange their partial row
+// max through shared memory once per tile.
 // MMA issue order per key tile t:  PV0_t, S0_{t+1}, PV1_t, S1_{t+1}  so that softmax of one
-// tile overlaps the tensor-core work of the other ("ping-pong"). Because S0_{t+1} is issued
+// tile overlaps the tensor-core work of the other. Because S0_{t+1} is issued
 // after PV0_t, the commit that signals S0_{t+1} also proves PV0_t finished: O0 is quiescent
 // while softmax 0 works on tile t+1, so the lazy O rescale needs no extra wait.
 //
@@ -40,11 +45,14 @@ namespace {
 
 constexpr int kStages = 4;
 constexpr int kTileBytes = kTileN * kHeadDim * 2;  // 16 KiB: 128 rows x 128 B
-constexpr int kThreads = 384;
+constexpr int kThreads = 640;  // 4 producer/MMA/alloc warps + 4 softmax warpgroups
+constexpr int kSoftmaxRegs = 104;  // 128*64 + 512*104 = 61440 of 65536: leave slack, inc blocks otherwise
+constexpr int kControlRegs = 56;
 __host__ __device__ constexpr uint32_t col_s(int wg) { return wg ? 128u : 0u; }
 __host__ __device__ constexpr uint32_t col_o(int wg) { return wg ? 320u : 256u; }
 __host__ __device__ constexpr uint32_t col_p(int wg) { return wg ? 448u : 384u; }
-constexpr float kLazyThreshold = 8.0f;  // log2 units: rescale when the max grows by > 2^8
+constexpr float kLazyThreshold = 8.0f;
+constexpr uint32_t kBarX0 = 1;  // named barriers 1, 2: the softmax warps of query tile 0, 1  // log2 units: rescale when the max grows by > 2^8
 
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, false, false);  // A=Q K-major, B=K K-major
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 64, false, true);    // A=P (TMEM), B=V MN-major
@@ -60,6 +68,8 @@ struct FwdSmem {
   uint64_t p_full[2];
   uint64_t o_done[2];
   uint32_t tmem_base;
+  float xmax[2][2][2 * kTileM];  // [query tile][tile parity][half * 128 + row]: partial row max
+  float xl[2][2 * kTileM];       // [query tile][half * 128 + row]: partial s* at the end
 };
 constexpr size_t kFwdSmemBytes = sizeof(FwdSmem) + 1024;
 
@@ -89,6 +99,26 @@ __device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t p_tmem, const
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(a, fmaxf(b, c)); }
 
+// 2^x on the FMA pipe for a pair (offloads part of the exponentials from the MUFU unit):
+// x = r + f with r = round(x), f in [-1/2, 1/2]; 2^f by a degree-3 minimax polynomial
+// (max relative error 7.5e-5, below the bf16 rounding of P); 2^r added to the exponent
+// field. x is clamped at -126 so the result stays a normal float (or underflows to ~0).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23: round-to-int
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 q = __ffma2_rn(f, make_float2(0.05517164f, 0.05517164f), make_float2(0.24261114f, 0.24261114f));
+  q = __ffma2_rn(q, f, make_float2(0.69326097f, 0.69326097f));
+  q = __ffma2_rn(q, f, make_float2(0.99992806f, 0.99992806f));
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
+}
+// Which exponential pairs (of the 64 per row and tile) go to the FMA pipe instead of MUFU.
+__device__ __forceinline__ constexpr bool kPolyPair(int i) { return (i & 3) == 3; }
+
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_bf16_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                     const __grid_constant__ CUtensorMap mv, const FwdParams p) {
@@ -113,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.s_full[i], 1);
-      mbar_init(&sm.p_full[i], 128);
+      mbar_init(&sm.p_full[i], 256);  // both halves of every row
       mbar_init(&sm.o_done[i], 1);
     }
     fence_barrier_init();
@@ -133,186 +163,252 @@ __global__ void __launch_bounds__(kThreads, 1)
   // warpgroup 0 (producer / MMA / allocator) needs few registers; the softmax warpgroups
   // hold a 128-score row each.
   if (warp < 4) {
-    setmaxnreg_dec<80>();
+    setmaxnreg_dec<kControlRegs>();
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+    const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+    if (elect_one()) {
       mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
       tma_load_4d(sm.q[0], &mq, &sm.q_full, 0, h, q0, b, stream);
       tma_load_4d(sm.q[1], &mq, &sm.q_full, 0, h, q0 + kTileM, b, stream);
-      for (int t = 0; t < T; ++t) {
-        const int st = t % kStages, n = t / kStages;
-        if (t >= kStages) mbar_wait(&sm.kv_empty[st], (n - 1) & 1);
-        const int krow = (t_begin + t) * kTileN;
+    }
+    __syncwarp();
+    for (int t = 0; t < T; ++t) {
+      const int st = t % kStages, n = t / kStages;
+      if (t >= kStages) mbar_wait(&sm.kv_empty[st], (n - 1) & 1);
+      const int krow = (t_begin + t) * kTileN;
+      if (elect_one()) {
         mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTileBytes);
         tma_load_4d(sm.k[st], &mk, &sm.kv_full[st], 0, h, krow, b, keep);
         tma_load_4d(sm.v[st], &mv, &sm.kv_full[st], 0, h, krow, b, keep);
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      mbar_wait(&sm.q_full, 0);
-      mbar_wait(&sm.kv_full[0], 0);
-      tc_fence_after();
-      issue_qk(tmem + col_s(0), sm.q[0], sm.k[0]);
+    // The whole warp walks the schedule (waits are warp-wide); one elected lane issues.
+    // Descriptors are precomputed: a K step or a ring stage is a plain add to the start
+    // address field (addresses < 256 KiB, so the 14-bit field never carries).
+    const uint64_t dq0 = sdesc_sw128(smem_u32(sm.q[0]), 16, 1024);
+    const uint64_t dq1 = sdesc_sw128(smem_u32(sm.q[1]), 16, 1024);
+    const uint64_t dk0 = sdesc_sw128(smem_u32(sm.k[0]), 16, 1024);
+    const uint64_t dv0 = sdesc_sw128(smem_u32(sm.v[0]), 16, 1024);
+    constexpr uint64_t kStageStep = kTileBytes >> 4;
+    const uint32_t ts0 = tmem + col_s(0), ts1 = tmem + col_s(1);
+    const uint32_t to0 = tmem + col_o(0), to1 = tmem + col_o(1);
+    const uint32_t tp0 = tmem + col_p(0), tp1 = tmem + col_p(1);
+    auto qk = [&](uint32_t d, uint64_t dq, int st) {
+      const uint64_t dk = dk0 + st * kStageStep;
+#pragma unroll
+      for (int kk = 0; kk < kHeadDim / 16; ++kk) umma_ss(d, dq + kk * 2, dk + kk * 2, kIdescQK, kk > 0);
+    };
+    auto pv = [&](uint32_t d, uint32_t tp, int st, bool acc) {
+      const uint64_t dv = dv0 + st * kStageStep;
+#pragma unroll
+      for (int kk = 0; kk < kTileN / 16; ++kk) umma_ts(d, tp + kk * 8, dv + kk * 128, kIdescPV, (acc || kk > 0) ? 1u : 0u);
+    };
+    mbar_wait(&sm.q_full, 0);
+    mbar_wait(&sm.kv_full[0], 0);
+    tc_fence_after();
+    if (elect_one()) {
+      qk(ts0, dq0, 0);
       umma_commit(&sm.s_full[0]);
-      issue_qk(tmem + col_s(1), sm.q[1], sm.k[0]);
+      qk(ts1, dq1, 0);
       umma_commit(&sm.s_full[1]);
-      for (int t = 0; t < T; ++t) {
-        const int st = t % kStages;
-        const int nx = (t + 1) % kStages;
-        const bool more = (t + 1) < T;
-        // query tile 0
-        mbar_wait(&sm.p_full[0], t & 1);
-        tc_fence_after();
-        issue_pv(tmem + col_o(0), tmem + col_p(0), sm.v[st], t > 0);
+    }
+    __syncwarp();
+    for (int t = 0; t < T; ++t) {
+      const int st = t % kStages;
+      const int nx = (t + 1) % kStages;
+      const bool more = (t + 1) < T;
+      // query tile 0: O0 += P0 V_t, then S0 = Q0 K_{t+1}^T
+      mbar_wait(&sm.p_full[0], t & 1);
+      if (more) mbar_wait(&sm.kv_full[nx], ((t + 1) / kStages) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        pv(to0, tp0, st, t > 0);
         if (more) {
-          mbar_wait(&sm.kv_full[nx], ((t + 1) / kStages) & 1);
-          tc_fence_after();
-          issue_qk(tmem + col_s(0), sm.q[0], sm.k[nx]);
+          qk(ts0, dq0, nx);
           umma_commit(&sm.s_full[0]);
         } else {
           umma_commit(&sm.o_done[0]);
         }
-        // query tile 1
-        mbar_wait(&sm.p_full[1], t & 1);
-        tc_fence_after();
-        issue_pv(tmem + col_o(1), tmem + col_p(1), sm.v[st], t > 0);
+      }
+      __syncwarp();
+      // query tile 1
+      mbar_wait(&sm.p_full[1], t & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        pv(to1, tp1, st, t > 0);
         umma_commit(&sm.kv_empty[st]);  // K_t and V_t no longer read
         if (more) {
-          issue_qk(tmem + col_s(1), sm.q[1], sm.k[nx]);
+          qk(ts1, dq1, nx);
           umma_commit(&sm.s_full[1]);
         } else {
           umma_commit(&sm.o_done[1]);
         }
       }
+      __syncwarp();
     }
   }
   } else {
-    setmaxnreg_inc<208>();
+    setmaxnreg_inc<kSoftmaxRegs>();
     // ------------------------------------------------------------ softmax warpgroups
-    const int wg = (warp - 4) >> 2;
+    // Four warpgroups: WG (qt, half) owns query tile qt and the 64 score columns
+    // [64*half, 64*half + 64) of every 128-key tile. One thread = one (row, half): it keeps
+    // the row's reference max m* (identical in both halves) and its half of s*. The two
+    // halves of a row exchange their partial row max through shared memory once per tile.
+    const int sw = warp - 4;
+    const int qt = sw >> 3;
+    const int half = (sw >> 2) & 1;
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = q0 + wg * kTileM + quarter * 32 + lane;
+    const int rloc = quarter * 32 + lane;
+    const int row = q0 + qt * kTileM + rloc;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t colS = col_s(qt) + half * 64, colO = col_o(qt) + half * 32, colP = col_p(qt) + half * 32;
+    const uint32_t xbar = kBarX0 + qt;  // the 8 warps sharing query tile qt
     const float c = p.scale_log2;
     float m_ref = -INFINITY;  // reference max m*, log2 units of the scaled score
-    float l = 0.f;            // s*
+    float l = 0.f;            // this half's part of s*
     for (int t = 0; t < T; ++t) {
-      mbar_wait(&sm.s_full[wg], t & 1);
+      mbar_wait(&sm.s_full[qt], t & 1);
       tc_fence_after();
-      uint32_t sr[128];
-      tmem_ld32(lane_base + col_s(wg) + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld32(lane_base + col_s(wg) + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      tmem_ld32(lane_base + col_s(wg) + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[64]));
-      tmem_ld32(lane_base + col_s(wg) + 96, *reinterpret_cast<uint32_t(*)[32]>(&sr[96]));
+      uint32_t sr[64];
+      tmem_ld32(lane_base + colS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld32(lane_base + colS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
       tmem_ld_wait();
-      const int valid = key_end - (t_begin + t) * kTileN;  // keys of this tile inside the range
-      // row extremum of the raw score (max if c >= 0, min if c < 0): max(s*c) over valid keys
-      float ext;
-      if (c >= 0.f) {
-        float m0 = -INFINITY, m1 = -INFINITY;
-        if (valid >= kTileN) {
+      const int tile_valid = key_end - (t_begin + t) * kTileN;  // keys of this tile in range
+      const int valid = tile_valid - half * 64;                // ... of my half (may be <= 0)
+      float* xm = sm.xmax[qt][t & 1];
+      uint32_t pk[32];  // P in bf16 pairs
+      float ext = 0.f;
+      bool have_ext = false;
+      // Fast path (full tile, m* already set): exponentiate against the current reference max
+      // while the partial max is computed alongside; the exchanged full-row max only has to
+      // confirm that no score exceeds the reference by more than the lazy threshold.
+      bool fast = (t > 0) && (tile_valid >= kTileN) && (c >= 0.f);
+      if (fast) {
+        const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
+        float2 rs = make_float2(0.f, 0.f);
+        float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-          for (int i = 0; i < 128; i += 4) {
-            m0 = fmax3(m0, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
-            m1 = fmax3(m1, __uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3]));
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 128; ++i)
-            if (i < valid) m0 = fmaxf(m0, __uint_as_float(sr[i]));
+        for (int i = 0; i < 32; ++i) {
+          const float2 s2 = make_float2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]));
+          if (i & 1) mx1 = fmax3(mx1, s2.x, s2.y);
+          else mx0 = fmax3(mx0, s2.x, s2.y);
+          const float2 x = __ffma2_rn(s2, c2, nm2);  // s*c - m*
+          const float2 e = kPolyPair(i) ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          rs = __fadd2_rn(rs, e);
+          pk[i] = pack_bf16x2(e.x, e.y);
         }
-        ext = fmaxf(m0, m1);
-      } else {
-        float m0 = INFINITY;
-#pragma unroll
-        for (int i = 0; i < 128; ++i)
-          if (i < valid) m0 = fminf(m0, __uint_as_float(sr[i]));
-        ext = m0;
-      }
-      const float m_cand = ext * c;
-      const bool need = m_cand > m_ref + kLazyThreshold;  // always true on the first tile
-      float alpha = 1.f;
-      if (need) {
-        alpha = ex2_approx(m_ref - m_cand);  // 0 when m_ref = -inf
-        m_ref = m_cand;
-        l *= alpha;
-      }
-      if (t > 0 && __any_sync(0xffffffffu, need)) {
-        // v* <- v* alpha. O is quiescent: S_t's commit covers PV_{t-1}.
-#pragma unroll
-        for (int part = 0; part < 4; ++part) {
-          uint32_t o[16];
-          tmem_ld16(lane_base + col_o(wg) + part * 16, o);
+        const float mx = fmaxf(mx0, mx1);
+        xm[half * 128 + rloc] = mx;
+        named_bar_sync(xbar, 256);
+        const float mfull = fmaxf(mx, xm[(half ^ 1) * 128 + rloc]);
+        const bool need = mfull * c > m_ref + kLazyThreshold;
+        if (__any_sync(0xffffffffu, need)) {  // identical in both halves (same rows, same data)
+          fast = false;
+          have_ext = true;
+          ext = mfull;
+          tmem_ld32(lane_base + colS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+          tmem_ld32(lane_base + colS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
           tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st16(lane_base + col_o(wg) + part * 16, o);
+        } else {
+          l += rs.x + rs.y;
         }
       }
-      // P = 2^(s c - m*) in bf16 pairs; s* += rowsum P
-      const float neg_m = -m_ref;
-      float rs0 = 0.f, rs1 = 0.f;
-      uint32_t pk[64];
-      if (valid >= kTileN) {
+      if (!fast) {
+        if (!have_ext) {
+          // row extremum of the raw score over valid keys: max if c >= 0, min if c < 0
+          float e0;
+          if (c >= 0.f) {
+            e0 = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          const float p0 = ex2_approx(fmaf(__uint_as_float(sr[2 * i]), c, neg_m));
-          const float p1 = ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), c, neg_m));
-          rs0 += p0;
-          rs1 += p1;
-          pk[i] = pack_bf16x2(p0, p1);
+            for (int i = 0; i < 64; ++i)
+              if (i < valid) e0 = fmaxf(e0, __uint_as_float(sr[i]));
+          } else {
+            e0 = INFINITY;
+#pragma unroll
+            for (int i = 0; i < 64; ++i)
+              if (i < valid) e0 = fminf(e0, __uint_as_float(sr[i]));
+          }
+          xm[half * 128 + rloc] = e0;
+          named_bar_sync(xbar, 256);
+          const float e1 = xm[(half ^ 1) * 128 + rloc];
+          ext = (c >= 0.f) ? fmaxf(e0, e1) : fminf(e0, e1);
         }
-      } else {
+        const float m_cand = ext * c;
+        const bool need = m_cand > m_ref + kLazyThreshold;  // always true on the first tile
+        float alpha = 1.f;
+        if (need) {
+          alpha = ex2_approx(m_ref - m_cand);  // 0 when m_ref = -inf
+          m_ref = m_cand;
+          l *= alpha;
+        }
+        if (t > 0 && __any_sync(0xffffffffu, need)) {
+          // v* <- v* alpha (my 32 of the row's 64 O columns). O is quiescent: S_t's commit
+          // covers PV_{t-1}.
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
+          for (int part = 0; part < 2; ++part) {
+            uint32_t o[16];
+            tmem_ld16(lane_base + colO + part * 16, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st16(lane_base + colO + part * 16, o);
+          }
+        }
+        // P = 2^(s c - m*) in bf16 pairs; s* += rowsum P
+        const float neg_m = -m_ref;
+        float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
           const float p0 = (2 * i < valid) ? ex2_approx(fmaf(__uint_as_float(sr[2 * i]), c, neg_m)) : 0.f;
           const float p1 = (2 * i + 1 < valid) ? ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), c, neg_m)) : 0.f;
           rs0 += p0;
           rs1 += p1;
           pk[i] = pack_bf16x2(p0, p1);
         }
+        l += rs0 + rs1;
       }
-      l += rs0 + rs1;
-      tmem_st32(lane_base + col_p(wg) + 0, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-      tmem_st32(lane_base + col_p(wg) + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+      tmem_st32(lane_base + colP, pk);
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&sm.p_full[wg]);
+      mbar_arrive(&sm.p_full[qt]);
     }
     // ------------------------------------------------------------ epilogue: out = v*/s*
-    mbar_wait(&sm.o_done[wg], 0);
+    float* xl = sm.xl[qt];
+    xl[half * 128 + rloc] = l;
+    named_bar_sync(xbar, 256);
+    const float lrow = l + xl[(half ^ 1) * 128 + rloc];  // s* of the whole row
+    mbar_wait(&sm.o_done[qt], 0);
     tc_fence_after();
-    uint32_t o[64];
-    tmem_ld32(lane_base + col_o(wg) + 0, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
-    tmem_ld32(lane_base + col_o(wg) + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
+    uint32_t o[32];
+    tmem_ld32(lane_base + colO, o);
     tmem_ld_wait();
     if (row < p.n_q) {
       const size_t bh = (size_t)b * p.H + h;
       if (p.num_splits > 1) {
         const size_t prow = ((size_t)split * p.B * p.H + bh) * p.n_q + row;
-        float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kHeadDim);
+        float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kHeadDim + half * 32);
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
+        for (int i = 0; i < 8; ++i)
           dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
                                __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
-        reinterpret_cast<float2*>(p.part_ml)[prow] = make_float2(m_ref, l);
+        if (half == 0) reinterpret_cast<float2*>(p.part_ml)[prow] = make_float2(m_ref, lrow);
       } else {
-        const float inv = 1.f / l;
-        const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim;
+        const float inv = 1.f / lrow;
+        const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + half * 32;
         if (p.out_f32) {
           float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
+          for (int i = 0; i < 8; ++i)
             dst[i] = make_float4(__uint_as_float(o[4 * i]) * inv, __uint_as_float(o[4 * i + 1]) * inv,
                                  __uint_as_float(o[4 * i + 2]) * inv, __uint_as_float(o[4 * i + 3]) * inv);
         } else {
           uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < 4; ++i) {
             uint4 w;
             w.x = pack_bf16x2(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv);
             w.y = pack_bf16x2(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv);
@@ -321,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             dst[i] = w;
           }
         }
-        if (p.lse) p.lse[bh * p.n_q + row] = (m_ref + __log2f(l)) * 0.6931471805599453f;
+        if (p.lse && half == 0) p.lse[bh * p.n_q + row] = (m_ref + __log2f(lrow)) * 0.6931471805599453f;
       }
     }
   }

@@ -7,6 +7,9 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
+#include <map>
+#include <cstdio>
 
 #include "internal.h"
 #include "mea.h"
@@ -46,6 +49,35 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 bool valid_dtype(mea_dtype_t t) { return t == MEA_F32 || t == MEA_BF16; }
 
 constexpr int64_t kMaxInt = 2147483647;
+
+// ------------------------------------------------------------------ launch profiling
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+
+// Brackets one launch with events on `st` when profiling is enabled.
+struct ProfScope {
+  cudaEvent_t a = nullptr, b = nullptr;
+  const char* name;
+  cudaStream_t st;
+  ProfScope(const char* n, cudaStream_t s) : name(n), st(s) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    if (!g_prof_on) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_prof.push_back({name, a, b});
+  }
+};
 
 }  // namespace
 
@@ -158,6 +190,7 @@ mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void
     if (d > 128) return fail(MEA_ERR_UNSUPPORTED, "f32 path supports d <= 128");
     if (out_dtype != MEA_F32) return fail(MEA_ERR_UNSUPPORTED, "f32 inputs need f32 output");
     if (k_chunk > 0 && k_chunk < n_k) return fail(MEA_ERR_UNSUPPORTED, "key chunking is a bf16-path schedule");
+    ProfScope ps("fwd_f32", st);
     cudaError_t e = launch_fwd_f32(static_cast<const float*>(q), static_cast<const float*>(k),
                                    static_cast<const float*>(v), static_cast<float*>(out), lse, (int)B, (int)H,
                                    (int)n_q, (int)n_k, (int)d, scale, st);
@@ -202,8 +235,14 @@ mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void
     p.part_o = static_cast<float*>(workspace);
     p.part_ml = p.part_o + rows * kHeadDim;
   }
-  if ((e = launch_fwd_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_bf16 launch");
-  if (pl.splits > 1 && (e = launch_merge_rows(p, st)) != cudaSuccess) return cuda_fail(e, "merge_rows launch");
+  {
+    ProfScope ps("fwd_bf16", st);
+    if ((e = launch_fwd_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_bf16 launch");
+  }
+  if (pl.splits > 1) {
+    ProfScope ps("merge_rows", st);
+    if ((e = launch_merge_rows(p, st)) != cudaSuccess) return cuda_fail(e, "merge_rows launch");
+  }
   return MEA_OK;
 }
 
@@ -245,9 +284,16 @@ mea_status_t mea_single_query_fwd(const void* q, const void* k, const void* v, v
   if (!out || !aligned16(out)) return fail(out ? MEA_ERR_MISALIGNED : MEA_ERR_INVALID_VALUE, "bad out pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* ws = static_cast<float*>(workspace);
-  cudaError_t e = launch_sq_partial(q, k, v, in_dtype == MEA_BF16, (int)B, (int)H, (int)n_k, (int)d, scale, splits, ws, st);
+  cudaError_t e;
+  {
+    ProfScope ps("sq_partial", st);
+    e = launch_sq_partial(q, k, v, in_dtype == MEA_BF16, (int)B, (int)H, (int)n_k, (int)d, scale, splits, ws, st);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "sq_partial launch");
-  e = launch_sq_merge(ws, splits, (int)(B * H), (int)d, 0, out, out_dtype == MEA_F32, nullptr, nullptr, nullptr, st);
+  {
+    ProfScope ps("sq_merge", st);
+    e = launch_sq_merge(ws, splits, (int)(B * H), (int)d, 0, out, out_dtype == MEA_F32, nullptr, nullptr, nullptr, st);
+  }
   return e == cudaSuccess ? MEA_OK : cuda_fail(e, "sq_merge launch");
 }
 
@@ -259,9 +305,16 @@ mea_status_t mea_single_query_partial(const void* q, const void* k, const void* 
   if (!m || !s || !vstar) return fail(MEA_ERR_INVALID_VALUE, "NULL triple pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   float* ws = static_cast<float*>(workspace);
-  cudaError_t e = launch_sq_partial(q, k, v, in_dtype == MEA_BF16, (int)B, (int)H, (int)n_k, (int)d, scale, splits, ws, st);
+  cudaError_t e;
+  {
+    ProfScope ps("sq_partial", st);
+    e = launch_sq_partial(q, k, v, in_dtype == MEA_BF16, (int)B, (int)H, (int)n_k, (int)d, scale, splits, ws, st);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "sq_partial launch");
-  e = launch_sq_merge(ws, splits, (int)(B * H), (int)d, 1, nullptr, 0, m, s, vstar, st);
+  {
+    ProfScope ps("sq_merge_triple", st);
+    e = launch_sq_merge(ws, splits, (int)(B * H), (int)d, 1, nullptr, 0, m, s, vstar, st);
+  }
   return e == cudaSuccess ? MEA_OK : cuda_fail(e, "sq_merge launch");
 }
 
@@ -273,6 +326,7 @@ mea_status_t mea_merge_partials(const float* m, const float* s, const float* vst
   if (B * H > 65535) return fail(MEA_ERR_UNSUPPORTED, "B*H > 65535");
   if (!valid_dtype(out_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
   if (!m || !s || !vstar || !out) return fail(MEA_ERR_INVALID_VALUE, "NULL pointer");
+  ProfScope ps("merge_partials", static_cast<cudaStream_t>(stream));
   cudaError_t e = launch_merge_partials(m, s, vstar, (int)P, (int)(B * H), (int)d, out, out_dtype == MEA_F32,
                                         static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? MEA_OK : cuda_fail(e, "merge_partials launch");
@@ -309,9 +363,48 @@ mea_status_t mea_fill_synthetic(void* dst, int64_t numel, mea_dtype_t dtype, uin
   if (numel < 0 || offset < 0 || !valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad arguments");
   if (numel == 0) return MEA_OK;
   if (!dst) return fail(MEA_ERR_INVALID_VALUE, "NULL dst");
+  ProfScope ps("fill_synthetic", static_cast<cudaStream_t>(stream));
   cudaError_t e = launch_fill_synthetic(dst, numel, dtype == MEA_BF16, seed, tensor_id, offset,
                                         static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? MEA_OK : cuda_fail(e, "fill launch");
+}
+
+void mea_profile_enable(int on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = on != 0;
+}
+
+mea_status_t mea_profile_read(char* buf, size_t cap) {
+  std::vector<ProfRec> recs;
+  {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    recs.swap(g_prof);
+  }
+  std::map<std::string, std::pair<int, double>> agg;
+  cudaError_t err = cudaSuccess;
+  for (auto& r : recs) {
+    float ms = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+    if (e != cudaSuccess) err = e;
+    auto& x = agg[r.name];
+    x.first += 1;
+    x.second += ms;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  std::string out;
+  char line[160];
+  for (auto& kv : agg) {
+    snprintf(line, sizeof line, "%s %d %.6f\n", kv.first.c_str(), kv.second.first, kv.second.second);
+    out += line;
+  }
+  if (buf && cap) {
+    size_t n = out.size() < cap - 1 ? out.size() : cap - 1;
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return err == cudaSuccess ? MEA_OK : cuda_fail(err, "profile events");
 }
 
 mea_status_t mea_debug_umma_tile(const void* a, const void* b, const void* v, float* s_out, float* o_out,
