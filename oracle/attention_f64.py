@@ -238,6 +238,32 @@ def backward(q, k, v, dout, scale):
     return dq, dk, dv
 
 
+def backward_rows(q, k, v, dout, scale, q_rows, k_rows, block=2048):
+    """O6 restricted to some outputs, for checking large configurations: dq for the query
+    rows ``q_rows`` and dk, dv for the key rows ``k_rows``, each exactly as in ``backward``
+    (same formulas; the full softmax statistics lse_i and delta_i = dO_i . O_i of every query
+    row are computed block by block of query rows, since each row's are independent)."""
+    q, k, v = _check(q, k, v)
+    dout = _f64(dout)
+    n_q = q.shape[0]
+    lse = np.empty(n_q)
+    delta = np.empty(n_q)
+    for a in range(0, n_q, block):
+        o, l = naive(q[a:a + block], k, v, scale)
+        lse[a:a + block] = l
+        delta[a:a + block] = delta_rowsum(o, dout[a:a + block])
+    qr = np.asarray(q_rows)
+    p = np.exp(scores(q[qr], k, scale) - lse[qr, None])          # P rows of the sampled queries
+    ds = p * (dout[qr] @ v.T - delta[qr, None])
+    dq = scale * (ds @ k)
+    kr = np.asarray(k_rows)
+    pc = np.exp(scores(q, k[kr], scale) - lse[:, None])          # P columns of the sampled keys
+    dv = pc.T @ dout
+    dsc = pc * (dout @ v[kr].T - delta[:, None])
+    dk = scale * (dsc.T @ q)
+    return dq, dk, dv
+
+
 def delta_rowsum(out, dout):
     """delta_i = dot(dO_i, O_i) (equals sum_j P_ij dP_ij)."""
     return (_f64(out) * _f64(dout)).sum(axis=1)

@@ -46,7 +46,10 @@ namespace {
 constexpr int kStages = 4;
 constexpr int kTileBytes = kTileN * kHeadDim * 2;  // 16 KiB: 128 rows x 128 B
 constexpr int kThreads = 640;  // 4 producer/MMA/alloc warps + 4 softmax warpgroups
-constexpr int kSoftmaxRegs = 104;  // 128*64 + 512*104 = 61440 of 65536: leave slack, inc blocks otherwise
+// setmaxnreg.inc can only redistribute the registers the CTA was launched with (640 x 96:
+// 480 per lane slot of an SM sub-partition, which holds 1 control + 4 softmax warps); a larger
+// total blocks forever (measured). 64 + 4 * 104 = 480.
+constexpr int kSoftmaxRegs = 104;
 constexpr int kControlRegs = 56;
 __host__ __device__ constexpr uint32_t col_s(int wg) { return wg ? 128u : 0u; }
 __host__ __device__ constexpr uint32_t col_o(int wg) { return wg ? 320u : 256u; }

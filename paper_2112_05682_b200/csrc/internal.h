@@ -28,9 +28,8 @@ struct FwdParams {
 struct BwdParams {
   int B, H, n_q, n_k;
   float scale, scale_log2;
-  const float* lse;        // [B,H,n_q]
-  const float* delta;      // [B,H,n_q]
-  float* dq_acc;           // [B,n_q,H,64] f32 (sum of dS K over key tiles, unscaled)
+  const float* lse2;       // [B*H][nq_pad]: lse * log2(e), +inf in the padding
+  const float* delta;      // [B*H][nq_pad]: dO_i . O_i, 0 in the padding
   void* dk;                // [B,n_k,H,64] bf16
   void* dv;                // [B,n_k,H,64] bf16
   int num_k_blocks;        // ceil(n_k / 128)
@@ -59,8 +58,8 @@ cudaError_t launch_merge_partials(const float* m, const float* s, const float* v
                                   void* out, int out_f32, cudaStream_t st);
 
 // backward
-cudaError_t launch_bwd_preprocess(const void* out, const void* dout, float* delta, float* dq_acc, int B, int H,
-                                  int n_q, cudaStream_t s);
+cudaError_t launch_bwd_preprocess(const void* out, const void* dout, const float* lse, float* delta, float* lse2,
+                                  float* dq_acc, int B, int H, int n_q, cudaStream_t s);
 cudaError_t launch_bwd_bf16(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                             const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
                             cudaStream_t s);

@@ -333,16 +333,34 @@ mea_status_t mea_merge_partials(const float* m, const float* s, const float* vst
 }
 
 // ------------------------------------------------------------------ backward
+namespace {
+struct BwdLayout {
+  size_t delta, lse2, dq_acc, lse_tmp, out_tmp, total;
+};
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+BwdLayout bwd_layout(int64_t B, int64_t H, int64_t n_q, int64_t d, bool lse_given) {
+  const size_t nq_pad = (size_t)((n_q + kTileM - 1) / kTileM) * kTileM;
+  const size_t rows_pad = (size_t)B * H * nq_pad;
+  BwdLayout L{};
+  size_t off = 0;
+  L.delta = off;  off = align256(off + rows_pad * sizeof(float));
+  L.lse2 = off;   off = align256(off + rows_pad * sizeof(float));
+  L.dq_acc = off; off = align256(off + (size_t)B * n_q * H * d * sizeof(float));
+  if (!lse_given) {
+    L.lse_tmp = off; off = align256(off + (size_t)B * H * n_q * sizeof(float));
+    L.out_tmp = off; off = align256(off + (size_t)B * n_q * H * d * 2);
+  }
+  L.total = off;
+  return L;
+}
+}  // namespace
+
 mea_status_t mea_attention_bwd_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
                                               mea_dtype_t dtype, int lse_given, size_t* bytes) {
   if (!bytes) return fail(MEA_ERR_INVALID_VALUE, "bytes is NULL");
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
   if (!valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  const size_t rows = (size_t)B * H * n_q;
-  size_t ws = rows * sizeof(float)                       // delta
-              + rows * (size_t)d * sizeof(float);        // dq accumulator
-  if (!lse_given) ws += rows * sizeof(float);            // recomputed lse
-  *bytes = (ws + 255) & ~size_t(255);
+  *bytes = bwd_layout(B, H, n_q, d, lse_given != 0).total;
   return MEA_OK;
 }
 
@@ -352,9 +370,79 @@ mea_status_t mea_attention_bwd(const void* q, const void* k, const void* v, cons
                                size_t workspace_bytes, void* stream) {
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, scale)) return s;
   if (!valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  (void)q; (void)k; (void)v; (void)out; (void)dout; (void)dq; (void)dk; (void)dv; (void)lse;
-  (void)workspace; (void)workspace_bytes; (void)stream;
-  return fail(MEA_ERR_UNSUPPORTED, "backward not built yet");
+  if (n_k == 0) return fail(MEA_ERR_EMPTY_KEYS, "attention over an empty key list");
+  if (dtype != MEA_BF16 || d != kHeadDim) return fail(MEA_ERR_UNSUPPORTED, "backward: bf16 with d == 64");
+  if (!k || !v || !dk || !dv) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (n_q == 0) {  // no queries: the gradients of k and v are zero
+    if (!aligned16(dk) || !aligned16(dv)) return fail(MEA_ERR_MISALIGNED, "dk, dv must be 16-byte aligned");
+    const size_t nb = (size_t)B * n_k * H * d * 2;
+    if ((e = cudaMemsetAsync(dk, 0, nb, st)) != cudaSuccess || (e = cudaMemsetAsync(dv, 0, nb, st)) != cudaSuccess)
+      return cuda_fail(e, "memset");
+    return MEA_OK;
+  }
+  if (!q || !out || !dout || !dq) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(dout) || !aligned16(dq) ||
+      !aligned16(dk) || !aligned16(dv))
+    return fail(MEA_ERR_MISALIGNED, "tensors must be 16-byte aligned");
+  const BwdLayout L = bwd_layout(B, H, n_q, d, lse != nullptr);
+  if (!workspace || workspace_bytes < L.total) return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "backward workspace");
+  if (!aligned16(workspace)) return fail(MEA_ERR_MISALIGNED, "workspace must be 16-byte aligned");
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  float* delta = reinterpret_cast<float*>(ws + L.delta);
+  float* lse2 = reinterpret_cast<float*>(ws + L.lse2);
+  float* dq_acc = reinterpret_cast<float*>(ws + L.dq_acc);
+
+  CUtensorMap mq, mk, mv, mdo, mdq;
+  const char* why = "";
+  if ((e = make_bnhd_map(&mq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_q, H, d, 64, kTileM,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+      (e = make_bnhd_map(&mdo, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_q, H, d, 64, kTileM,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+      (e = make_bnhd_map(&mk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+      (e = make_bnhd_map(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+      (e = make_bnhd_map(&mdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, n_q, H, d, 32, kTileM,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess)
+    return cuda_fail(e, why);
+
+  if (!lse) {
+    // B0: the statistics pass — rerun the forward for lse (its output goes to scratch).
+    float* lse_tmp = reinterpret_cast<float*>(ws + L.lse_tmp);
+    mea_status_t r = mea_attention_fwd(q, k, v, ws + L.out_tmp, B, H, n_q, n_k, d, MEA_BF16, MEA_BF16, scale, lse_tmp,
+                                       0, 0, nullptr, 0, stream);
+    if (r != MEA_OK) return r;
+    lse = lse_tmp;
+  }
+  {
+    ProfScope ps("bwd_preprocess", st);
+    if ((e = launch_bwd_preprocess(out, dout, lse, delta, lse2, dq_acc, (int)B, (int)H, (int)n_q, st)) != cudaSuccess)
+      return cuda_fail(e, "bwd_preprocess launch");
+  }
+  BwdParams p{};
+  p.B = (int)B;
+  p.H = (int)H;
+  p.n_q = (int)n_q;
+  p.n_k = (int)n_k;
+  p.scale = scale;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.lse2 = lse2;
+  p.delta = delta;
+  p.dk = dk;
+  p.dv = dv;
+  p.num_k_blocks = (int)((n_k + kTileN - 1) / kTileN);
+  {
+    ProfScope ps("bwd_bf16", st);
+    if ((e = launch_bwd_bf16(p, mq, mk, mv, mdo, mdq, st)) != cudaSuccess) return cuda_fail(e, "bwd_bf16 launch");
+  }
+  {
+    ProfScope ps("dq_convert", st);
+    if ((e = launch_dq_convert(dq_acc, dq, B * n_q * H * d, scale, st)) != cudaSuccess)
+      return cuda_fail(e, "dq_convert launch");
+  }
+  return MEA_OK;
 }
 
 // ------------------------------------------------------------------ generator / debug

@@ -40,11 +40,25 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifdef MEA_DEBUG_HANG
+// Diagnostic build only: a wait that never completes is counted (by barrier smem offset)
+// and abandoned, so a deadlock shows up as counts instead of a hung GPU.
+__device__ unsigned int g_mea_hang[1024];
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  for (uint32_t spin = 0; !mbar_try_wait(bar, parity); ++spin) {
+    if (spin > (1u << 22)) {
+      atomicAdd(&g_mea_hang[(smem_u32(bar) >> 3) & 1023], 1u);
+      return;
+    }
+  }
+}
+#else
 // Wait until the phase with the given parity has completed.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+#endif
 
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
@@ -82,6 +96,10 @@ __device__ __forceinline__ void bulk_wait_group_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_group0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_group_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
 
 // L2 cache-policy hints (createpolicy.fractional).
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -198,14 +216,25 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// Broadcast lane 0's value (lets ptxas keep warp-invariant MMA operands in uniform registers).
+__device__ __forceinline__ uint64_t shfl0_u64(uint64_t v) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, 0);
+  const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), 0);
+  return ((uint64_t)hi << 32) | lo;
+}
+
 // Register budget hand-off between warpgroups.
 template <int kRegs>
 __device__ __forceinline__ void setmaxnreg_inc() {
+#ifndef MEA_NO_SETMAXNREG
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+#endif
 }
 template <int kRegs>
 __device__ __forceinline__ void setmaxnreg_dec() {
+#ifndef MEA_NO_SETMAXNREG
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
+#endif
 }
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {

@@ -1,0 +1,87 @@
+"""GPU parity of mea_attention_bwd (dq, dk, dv) against the float64 oracle (O6).
+
+bf16 gradients: max abs error <= 5e-2 and relative norm <= 2e-2 (BASELINE.json north_star,
+SURVEY 8(c)). Shapes span several 128-tiles with ragged tails in both n_q and n_k; dO is
+N(0,1) and all-ones (the paper's "sum of the results" loss); lse given and
+recomputed (NULL). configs[3] runs at full size and is checked on sampled rows.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import gen
+from tests import helpers as Hh
+
+pytestmark = pytest.mark.gpu
+
+
+def _bwd(q, k, v, do, scale=None, with_lse=True):
+    from paper_2112_05682_b200 import api
+    qd, kd, vd, dod = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v, do))
+    out, lse = api.mea_attention_fwd(qd, kd, vd, scale=scale, want_lse=True)
+    dq, dk, dv = api.mea_attention_bwd(qd, kd, vd, out, dod, lse=lse if with_lse else None, scale=scale)
+    torch.cuda.synchronize()
+    return [t.double().cpu().numpy() for t in (dq, dk, dv)]
+
+
+@pytest.mark.parametrize("B,n_q,n_k,H", [(1, 128, 128, 1), (1, 17, 129, 2), (2, 300, 257, 2), (1, 1000, 700, 1),
+                                         (1, 129, 1, 1), (1, 256, 1030, 3)])
+def test_bf16_backward_matches_oracle(B, n_q, n_k, H):
+    d = 64
+    q, k, v, do = Hh.host_inputs(B, n_q, n_k, H, d, seed=21, with_dout=True)
+    refs = O.mha_backward(q, k, v, do, 1 / math.sqrt(d))
+    for got, ref, nm in zip(_bwd(q, k, v, do), refs, ("dq", "dk", "dv")):
+        Hh.assert_close_bf16(got, ref, abs_tol=Hh.TOL_BF16_GRAD, rel_tol=Hh.REL_NORM_GRAD, what=nm)
+
+
+def test_bf16_backward_ones_dout_and_recomputed_lse():
+    """dO = 1: the gradient of sum(attention) that the paper differentiates."""
+    q, k, v = Hh.host_inputs(1, 384, 300, 2, 64, seed=22)
+    do = np.ones_like(q)
+    refs = O.mha_backward(q, k, v, do, 0.125)
+    for with_lse in (True, False):
+        for got, ref, nm in zip(_bwd(q, k, v, do, with_lse=with_lse), refs, ("dq", "dk", "dv")):
+            # with dO = 1 and delta = 1, dS and hence dq, dk are ~0: compare absolutely
+            err = np.abs(got - ref).max()
+            assert err <= Hh.TOL_BF16_GRAD, (nm, err)
+        np.testing.assert_allclose(_bwd(q, k, v, do, with_lse=with_lse)[2], refs[2], atol=Hh.TOL_BF16_GRAD)
+
+
+def test_bf16_backward_scale_and_zero_queries():
+    from paper_2112_05682_b200 import api
+    q, k, v, do = Hh.host_inputs(1, 200, 333, 1, 64, seed=23, with_dout=True)
+    refs = O.mha_backward(q, k, v, do, 0.3)
+    for got, ref, nm in zip(_bwd(q, k, v, do, scale=0.3), refs, ("dq", "dk", "dv")):
+        Hh.assert_close_bf16(got, ref, abs_tol=Hh.TOL_BF16_GRAD, rel_tol=Hh.REL_NORM_GRAD, what=nm)
+    kd = Hh.to_dev(k, torch.bfloat16)
+    q0 = torch.zeros(1, 0, 1, 64, dtype=torch.bfloat16, device="cuda")
+    dk = torch.full_like(kd, 7.0)
+    dv = torch.full_like(kd, 7.0)
+    api.mea_attention_bwd(q0, kd, kd, q0, q0, dk=dk, dv=dv)
+    torch.cuda.synchronize()
+    assert not dk.any() and not dv.any()
+
+
+def test_config4_backward_sampled_rows():
+    """configs[3]: B=1 H=16 n=16384 d=64 bf16 backward — oracle on sampled rows of 2 heads."""
+    from paper_2112_05682_b200 import api
+    B, n, H, d = 1, 16384, 16, 64
+    shape = (B, n, H, d)
+    ts = [torch.empty(shape, dtype=torch.bfloat16, device="cuda") for _ in range(4)]
+    for t, tid in zip(ts, (gen.TENSOR_Q, gen.TENSOR_K, gen.TENSOR_V, gen.TENSOR_DO)):
+        api.mea_fill_synthetic(t, 0, tid)
+    q, k, v, do = ts
+    out, lse = api.mea_attention_fwd(q, k, v, want_lse=True)
+    dq, dk, dv = api.mea_attention_bwd(q, k, v, out, do, lse=lse)
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 127, 128, 4097, 16383])
+    for h in (0, 11):
+        hq, hk, hv, hdo = (gen.rows_of(shape, 0, tid, 0, np.arange(n), h)
+                           for tid in (gen.TENSOR_Q, gen.TENSOR_K, gen.TENSOR_V, gen.TENSOR_DO))
+        rq, rk, rv = O.backward_rows(hq, hk, hv, hdo, 1 / 8, rows, rows)
+        Hh.assert_close_bf16(dq[0, rows, h].double().cpu().numpy(), rq, Hh.TOL_BF16_GRAD, Hh.REL_NORM_GRAD, "dq")
+        Hh.assert_close_bf16(dk[0, rows, h].double().cpu().numpy(), rk, Hh.TOL_BF16_GRAD, Hh.REL_NORM_GRAD, "dk")
+        Hh.assert_close_bf16(dv[0, rows, h].double().cpu().numpy(), rv, Hh.TOL_BF16_GRAD, Hh.REL_NORM_GRAD, "dv")

@@ -241,3 +241,14 @@ def test_generator_row_sampling_matches_full_tensor():
     full = gen.normal_tensor(shape, 7, gen.TENSOR_K, "bf16")
     rows = np.array([0, 5, 36])
     np.testing.assert_array_equal(gen.rows_of(shape, 7, gen.TENSOR_K, 1, rows, 2), full[1, rows, 2])
+
+
+def test_backward_rows_equals_full_backward(rng):
+    n_q, n_k, d = 37, 29, 8
+    q, k, v, do = _rand(rng, n_q, d), _rand(rng, n_k, d), _rand(rng, n_k, d), _rand(rng, n_q, d)
+    dq, dk, dv = O.backward(q, k, v, do, 0.4)
+    qr, kr = np.array([0, 5, 36]), np.array([1, 28])
+    sq, sk, sv = O.backward_rows(q, k, v, do, 0.4, qr, kr, block=10)
+    np.testing.assert_allclose(sq, dq[qr], atol=1e-12)
+    np.testing.assert_allclose(sk, dk[kr], atol=1e-12)
+    np.testing.assert_allclose(sv, dv[kr], atol=1e-12)
