@@ -18,7 +18,7 @@ schedule (q_chunk 1024 / k_chunk 4096), the single-query split-K path at configs
 and the end-to-end number through the public API with host buffers (e2e).
 
 Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events on the
-launching stream with a 512 MiB L2 flush (write) before each step outside the events;
+launching stream with a 512 MiB L2 flush (read) before each step outside the events;
 barrier + synchronize around the timed loop; the max over ranks is reported.
 """
 import argparse
@@ -44,7 +44,7 @@ SQ_NK = 1 << 20                   # configs[1]
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["mea", "reference"], default="mea")
     ap.add_argument("--workload", choices=["cfg3", "cfg5"], default="cfg3")
@@ -81,7 +81,7 @@ class Clocks:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -218,7 +218,13 @@ def main():
     if run_bwd:
         nb = api.mea_attention_bwd_workspace_size(Bl, Hl, n, n, D, api.MEA_BF16, True)
         bwd_ws = torch.empty(nb, dtype=torch.uint8, device=dev)
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    # L2 flush by READING 512 MiB (> 126 MB L2): a write-based flush would leave ~126 MB of
+    # dirty lines whose write-back steals HBM bandwidth from the next timed kernel.
+    flush = torch.ones(128 << 20, dtype=torch.float32, device=dev)
+    flush_sink = torch.empty((), dtype=torch.float32, device=dev)
+
+    def flush_l2():
+        torch.sum(flush, dim=0, out=flush_sink)
 
     def step():
         api.mea_attention_fwd(q, k, v, out=out, lse=lse)
@@ -231,7 +237,7 @@ def main():
         barrier()
         evs = []
         for _ in range(steps):
-            flush.fill_(1)
+            flush_l2()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             fn()
@@ -325,6 +331,25 @@ def main():
             "frac_hbm_total": sq_bytes / ((part_ms + merge_ms) * 1e-3) / 1e9 / pk["hbm_gbs"],
             "peak_gbs": pk["hbm_gbs"], "scratch_bytes": sq_ws.numel()}
         del sq_k, sq_v
+    # ---------------- key-range sharded single query across ranks (NCCL all-gather + merge)
+    if world > 1 and a.workload == "cfg3":
+        from paper_2112_05682_b200 import dist as mdist
+        Bq, Hq = 1, 16          # a decode-shaped batch of 16 heads, 2^20 keys per rank (weak)
+        n_local = SQ_NK
+        sq_q = torch.empty((Bq, Hq, D), dtype=torch.bfloat16, device=dev)
+        sq_k = torch.empty((Bq, n_local, Hq, D), dtype=torch.bfloat16, device=dev)
+        sq_v = torch.empty_like(sq_k)
+        api.mea_fill_synthetic(sq_q, a.seed, gen.TENSOR_Q)
+        api.mea_fill_synthetic(sq_k, a.seed, gen.TENSOR_K, offset=rank * sq_k.numel())
+        api.mea_fill_synthetic(sq_v, a.seed, gen.TENSOR_V, offset=rank * sq_v.numel())
+        run = lambda: mdist.sharded_single_query(sq_q, sq_k, sq_v)
+        t = timed(run, max(5, a.steps // 3), 2)
+        sh_ms = max_over_ranks(statistics.mean(t))
+        gb = world * 2 * n_local * Hq * D * 2 / 1e9
+        extras["single_query_key_sharded"] = {
+            "keys_total": n_local * world, "heads": Hq, "ms": sh_ms, "gbs_total": gb / (sh_ms * 1e-3),
+            "collective": "one all_gather of (m*, s*, v*) per (b,h), NCCL"}
+        del sq_k, sq_v
     # ---------------- scratch bytes vs the paper's accounting (standard attention: n^2*4 B/head)
     scratch = {"fwd_workspace_bytes": 0, "fwd_lse_residual_bytes": lse.numel() * 4,
                "bwd_workspace_bytes": bwd_ws.numel() if bwd_ws is not None else None,
@@ -376,7 +401,7 @@ def main():
             "dtype": "bf16", "data": "synthetic (counter-based Irwin-Hall(12), N(0,1)-like, PAPER.md:231)",
             "config": {"workload": wl, "B_per_gpu": Bl, "H": Hl, "n": n, "d": D, "global_batch": Bl * world,
                        "seq_len": n, "parallelism": f"dp{world} (batch x head sharding, no collective)",
-                       "l2": "flushed before every timed step (512 MiB write, outside the events)"},
+                       "l2": "flushed before every timed step (512 MiB read, outside the events)"},
             "clocks": clk, "gpu_launches": gpu_launches, "roofline": roofline, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "scratch": scratch, **extras,
             "paper_context": {"tpu_v3_fwd_ms_n16384_h1": 11.3, "tpu_v3_diff_ms_n16384_h1": 21.0,

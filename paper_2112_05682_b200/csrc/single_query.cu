@@ -22,7 +22,7 @@
 namespace mea {
 namespace {
 
-constexpr int kSqThreads = 256;
+constexpr int kSqThreads = 512;  // one CTA per SM: 16 warps x 256 B x 2 steps in flight
 constexpr int kSqWarps = kSqThreads / 32;
 constexpr int kKeysPerWarpStep = 16;  // 4 groups x 4 keys
 constexpr int kUnroll = 2;            // warp steps in flight
@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_
                                                                      const __nv_bfloat16* __restrict__ v, int H,
                                                                      int n_k, float scale_log2, int splits,
                                                                      float* __restrict__ part) {
+  asm volatile("griddepcontrol.launch_dependents;");
   const int split = blockIdx.x, bh = blockIdx.y;
   const int b = bh / H, h = bh % H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -237,51 +238,76 @@ __global__ void __launch_bounds__(128) sq_partial_f32_kernel(const float* __rest
 
 // Merge `splits` partial states per (b,h) (Figure 1 lines 33-40):
 //   M = max m_s;  out = sum_s 2^(m_s - M) v*_s / sum_s 2^(m_s - M) s*_s.
-// block (128 dims, 4 groups of splits). mode 0: out (dtype); mode 1: triple with m in
-// natural-log units (m_nat = m * ln 2) for the cross-GPU merge.
-__global__ void __launch_bounds__(512) sq_merge_kernel(const float* __restrict__ part, int splits, int d, int mode,
-                                                       void* out, int out_f32, float* m_out, float* s_out,
-                                                       float* v_out) {
+// One CTA of 8 warps per (b,h): the max by a block reduction, then warp w folds splits
+// w, w+8, ... (lanes own dims lane + 32 i, 4 independent loads in flight per lane), then
+// the 8 warp results are combined. mode 0: out (dtype); mode 1: the merged triple with m in
+// natural-log units (m_nat = m ln 2) for the cross-GPU merge.
+constexpr int kMergeWarps = 8;
+__global__ void __launch_bounds__(kMergeWarps * 32) sq_merge_kernel(const float* __restrict__ part, int splits,
+                                                                    int d, int mode, void* out, int out_f32,
+                                                                    float* m_out, float* s_out, float* v_out) {
+  // PDL: everything above this point may overlap the tail of the partial kernel.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int bh = blockIdx.x;
-  const int f = threadIdx.x, grp = threadIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float* base = part + (size_t)bh * splits * (d + 2);
-  __shared__ float sm_M[4], sm_l[4], sm_a[4][128];
+  __shared__ float sm_red[kMergeWarps], sm_l[kMergeWarps], sm_a[kMergeWarps][128];
   float M = -INFINITY;
-  for (int s = grp; s < splits; s += 4) M = fmaxf(M, base[(size_t)s * (d + 2)]);
-  float l = 0.f, a = 0.f;
-  if (M != -INFINITY)
-    for (int s = grp; s < splits; s += 4) {
-      const float* ps = base + (size_t)s * (d + 2);
-      const float w = exp2f(ps[0] - M);
-      l += w * ps[1];
-      if (f < d) a += w * ps[2 + f];
-    }
-  if (f == 0) {
-    sm_M[grp] = M;
-    sm_l[grp] = l;
-  }
-  sm_a[grp][f] = a;
+  for (int s = threadIdx.x; s < splits; s += blockDim.x) M = fmaxf(M, base[(size_t)s * (d + 2)]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  if (lane == 0) sm_red[warp] = M;
   __syncthreads();
-  if (grp != 0 || f >= d) return;
-  float MM = -INFINITY;
-  for (int g2 = 0; g2 < 4; ++g2) MM = fmaxf(MM, sm_M[g2]);
-  float L = 0.f, A = 0.f;
-  if (MM != -INFINITY)
-    for (int g2 = 0; g2 < 4; ++g2) {
-      const float w = exp2f(sm_M[g2] - MM);
-      L += w * sm_l[g2];
-      A += w * sm_a[g2][f];
+  M = sm_red[0];
+#pragma unroll
+  for (int w = 1; w < kMergeWarps; ++w) M = fmaxf(M, sm_red[w]);
+  float l = 0.f, a[4] = {0.f, 0.f, 0.f, 0.f};
+  if (M != -INFINITY) {
+    // 16 splits per warp per round, all loads issued before any use (latency-bound otherwise)
+    for (int s0 = warp; s0 < splits; s0 += 16 * kMergeWarps) {
+      float mw[16], lw[16], vw[16][4];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int s = s0 + u * kMergeWarps;
+        const bool ok = s < splits;
+        const float* ps = base + (size_t)(ok ? s : 0) * (d + 2);
+        mw[u] = ok ? ps[0] : -INFINITY;
+        lw[u] = ok ? ps[1] : 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) vw[u][i] = (ok && lane + 32 * i < d) ? ps[2 + lane + 32 * i] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float w = exp2f(mw[u] - M);
+        l = fmaf(w, lw[u], l);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = fmaf(w, vw[u][i], a[i]);
+      }
     }
-  if (mode == 0) {
-    const float r = A / L;
-    if (out_f32) static_cast<float*>(out)[(size_t)bh * d + f] = r;
-    else static_cast<__nv_bfloat16*>(out)[(size_t)bh * d + f] = __float2bfloat16_rn(r);
-  } else {
-    if (f == 0) {
-      m_out[bh] = MM * 0.6931471805599453f;
-      s_out[bh] = L;
+  }
+  if (lane == 0) sm_l[warp] = l;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (lane + 32 * i < d) sm_a[warp][lane + 32 * i] = a[i];
+  __syncthreads();
+  for (int f = threadIdx.x; f < d; f += blockDim.x) {
+    float L = 0.f, A = 0.f;
+#pragma unroll
+    for (int w = 0; w < kMergeWarps; ++w) {
+      L += sm_l[w];
+      A += sm_a[w][f];
     }
-    v_out[(size_t)bh * d + f] = A;
+    if (mode == 0) {
+      const float r = A / L;
+      if (out_f32) static_cast<float*>(out)[(size_t)bh * d + f] = r;
+      else static_cast<__nv_bfloat16*>(out)[(size_t)bh * d + f] = __float2bfloat16_rn(r);
+    } else {
+      if (f == 0) {
+        m_out[bh] = M * 0.6931471805599453f;
+        s_out[bh] = L;
+      }
+      v_out[(size_t)bh * d + f] = A;
+    }
   }
 }
 
@@ -306,10 +332,10 @@ __global__ void merge_partials_kernel(const float* __restrict__ m, const float* 
 
 }  // namespace
 
-// Splits: enough CTAs to keep ~2 resident per SM streaming (HBM needs ~35 KB in flight per
-// SM), but at least ~1024 keys per split so the merge stays small.
+// Splits: one 512-thread CTA per SM streaming (HBM needs ~35 KB in flight per SM; a CTA has
+// 256 KB in flight), at least ~1024 keys per split, so the merge stays small.
 int sq_num_splits(int64_t BH, int64_t n_k) {
-  const int64_t target_ctas = 148 * 2;
+  const int64_t target_ctas = 148;
   int64_t splits = (target_ctas + BH - 1) / BH;
   const int64_t max_by_keys = (n_k + 1023) / 1024;
   if (splits > max_by_keys) splits = max_by_keys;
@@ -335,8 +361,18 @@ cudaError_t launch_sq_partial(const void* q, const void* k, const void* v, int b
 
 cudaError_t launch_sq_merge(const float* ws, int splits, int BH, int d, int mode, void* out, int out_f32, float* m,
                             float* sum, float* vstar, cudaStream_t s) {
-  sq_merge_kernel<<<BH, dim3(128, 4), 0, s>>>(ws, splits, d, mode, out, out_f32, m, sum, vstar);
-  return cudaGetLastError();
+  // Programmatic dependent launch: the merge grid is scheduled while the partial kernel
+  // drains and waits (griddepcontrol.wait) for its results, hiding the launch gap.
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(BH);
+  cfg.blockDim = dim3(kMergeWarps * 32);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, sq_merge_kernel, ws, splits, d, mode, out, out_f32, m, sum, vstar);
 }
 
 cudaError_t launch_merge_partials(const float* m, const float* s, const float* vstar, int P, int BH, int d, void* out,
