@@ -63,13 +63,15 @@ struct BwdSmem {
   float lse2[kBStages][kTile];
   float delta[kBStages][kTile];
   uint64_t kv_full, qdo_full[kBStages], qdo_empty[kBStages];
-  uint64_t s_full, p_full, p_free, dq_full, dq_empty, dkv_done;
+  uint64_t s_full, s_loaded, p_full, p_free, dq_full, dq_empty, dkv_done;
   uint32_t tmem_base;
 };
 constexpr size_t kBwdSmemBytes = sizeof(BwdSmem) + 1024;
 
+// 1024-byte alignment (128B-swizzle atoms) by pointer arithmetic on the __shared__ array, so
+// the compiler keeps the shared address space (LDS/STS instead of generic LD/ST).
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+  return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
 
 // 1-D bulk copy global -> shared, completion on an mbarrier.
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       mbar_init(&sm.qdo_empty[i], 1);
     }
     mbar_init(&sm.s_full, 1);
+    mbar_init(&sm.s_loaded, 512);
     mbar_init(&sm.p_full, 512);
     mbar_init(&sm.p_free, 1);
     mbar_init(&sm.dq_full, 1);
@@ -184,6 +187,15 @@ __global__ void __launch_bounds__(kBThreads, 1)
             scores((i + 1) % kBStages);
             umma_commit(&sm.s_full);
           }
+        }
+        __syncwarp();
+#ifdef MEA_BWD_HOLD_GRAD
+        // hold the gradient MMAs until the softmax warps have read ST/dPT of tile i+1: TMEM
+        // loads issued while the tensor core streams accumulators stall for hundreds of cycles
+        if (more) mbar_wait(&sm.s_loaded, (i + 1) & 1);
+#endif
+        tc_fence_after();
+        if (elect_one()) {
           // dV += PT dO : K = 128 queries in steps of 16 (PT: 8 columns per step; dO: 16 rows)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) umma_ts(tm + kColDV, tm + kColP + kk * 8, o + kk * 128, kIdDV, (i > 0 || kk > 0));
@@ -220,14 +232,34 @@ __global__ void __launch_bounds__(kBThreads, 1)
     // dST row j, queries [32g, 32g+32) -> half g/2, 16-byte chunks (32g%64)/8 .. +3, swizzled
     uint8_t* ds_row = sm.ds[g >> 1] + j * 128;
     const int chunk0 = ((g & 1) * 32) / 8;
+#ifdef MEA_EXP_TIMING
+    unsigned long long* tdbg = reinterpret_cast<unsigned long long*>(p.dv);
+    const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && quarter == 0 && lane == 0;
+#define TPROBE(k) if (probe && i >= 8 && i < 24) tdbg[(g * 16 + (i - 8)) * 8 + (k)] = clock64();
+#else
+#define TPROBE(k)
+#endif
     for (int i = 0; i < NQ; ++i) {
       const int st = i % kBStages;
+      TPROBE(0)
       mbar_wait(&sm.s_full, i & 1);
+      TPROBE(1)
       tc_fence_after();
       uint32_t sr[32], dr[32];
       tmem_ld32(lane_base + kColST + g * 32, sr);
       tmem_ld32(lane_base + kColDPT + g * 32, dr);
       tmem_ld_wait();
+#ifdef MEA_BWD_HOLD_GRAD
+      {
+        // consume the loaded registers so the arrive really follows the TMEM data
+        uint32_t x = 0;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) x ^= sr[u] ^ dr[u];
+        asm volatile("" ::"r"(x));
+      }
+      tc_fence_before();
+      if (i > 0) mbar_arrive(&sm.s_loaded);
+#endif
       const float* l2 = sm.lse2[st] + g * 32;
       const float* dl = sm.delta[st] + g * 32;
       uint32_t pk[16], dk[16];
@@ -244,7 +276,9 @@ __global__ void __launch_bounds__(kBThreads, 1)
         pk[u] = pack_bf16x2(pr.x, pr.y);
         dk[u] = pack_bf16x2(ds.x, ds.y);
       }
+      TPROBE(2)
       if (i > 0) mbar_wait(&sm.p_free, (i - 1) & 1);  // tile i-1's MMAs no longer read P / dS
+      TPROBE(3)
       tmem_st16(lane_base + kColP + g * 16, pk);
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
@@ -255,6 +289,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm.p_full);
+      TPROBE(4)
     }
     // ------------------------------------------------------------------ dV, dK epilogue
     if (g < 2) {
@@ -265,7 +300,11 @@ __global__ void __launch_bounds__(kBThreads, 1)
       tmem_ld32(lane_base + col, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
       tmem_ld32(lane_base + col + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
       tmem_ld_wait();
+#ifdef MEA_EXP_TIMING
+      if (false) {
+#else
       if (key_ok) {
+#endif
         const float sc = (g == 0) ? 1.f : p.scale;
         __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g == 0 ? p.dv : p.dk) +
                              (((size_t)b * p.n_k + k0 + j) * p.H + h) * kHeadDim;

@@ -15,7 +15,8 @@
 //
 // CTA = 2 query tiles (256 rows) of one (b, h) sharing every K/V tile:
 //   warp 0      TMA producer: Q0,Q1 once, then a 4-stage K/V ring (mbarrier full/empty)
-//   warp 1      MMA issuer (one elected lane): S0,S1 = Q K^T; O0,O1 += P V; commits -> mbarriers
+//   warps 1, 3  MMA issuers for query tile 0 / 1 (one elected lane each): S = Q K^T,
+//               O += P V; commits -> mbarriers
 //   warp 2      TMEM allocator
 //   warps 4-11  softmax for query tile 0: warps 4-7 take score columns 0-63 of each key tile,
 //               warps 8-11 columns 64-127 (a thread = one row-half = one TMEM lane)
@@ -55,7 +56,6 @@ __host__ __device__ constexpr uint32_t col_s(int wg) { return wg ? 128u : 0u; }
 __host__ __device__ constexpr uint32_t col_o(int wg) { return wg ? 320u : 256u; }
 __host__ __device__ constexpr uint32_t col_p(int wg) { return wg ? 448u : 384u; }
 constexpr float kLazyThreshold = 8.0f;
-constexpr uint32_t kBarX0 = 1;  // named barriers 1, 2: the softmax warps of query tile 0, 1  // log2 units: rescale when the max grows by > 2^8
 
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, false, false);  // A=Q K-major, B=K K-major
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 64, false, true);    // A=P (TMEM), B=V MN-major
@@ -68,16 +68,18 @@ struct FwdSmem {
   uint64_t kv_full[kStages];
   uint64_t kv_empty[kStages];
   uint64_t s_full[2];
+  uint64_t s_loaded[2];  // the softmax warps of a query tile have read S_t (S_{t+1} may be written)
+  uint64_t pv_done[2];   // PV_t finished: P buffer free again, O quiescent
   uint64_t p_full[2];
   uint64_t o_done[2];
   uint32_t tmem_base;
-  float xmax[2][2][2 * kTileM];  // [query tile][tile parity][half * 128 + row]: partial row max
-  float xl[2][2 * kTileM];       // [query tile][half * 128 + row]: partial s* at the end
 };
 constexpr size_t kFwdSmemBytes = sizeof(FwdSmem) + 1024;
 
+// 1024-byte alignment (128B-swizzle atoms) by pointer arithmetic on the __shared__ array, so
+// the compiler keeps the shared address space (LDS/STS instead of generic LD/ST).
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+  return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
 
 // S[tmem d_col] = Qtile . Ktile^T  (M=128 queries, N=128 keys, K=64 in 4 steps of 16)
@@ -102,25 +104,9 @@ __device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t p_tmem, const
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(a, fmaxf(b, c)); }
 
-// 2^x on the FMA pipe for a pair (offloads part of the exponentials from the MUFU unit):
-// x = r + f with r = round(x), f in [-1/2, 1/2]; 2^f by a degree-3 minimax polynomial
-// (max relative error 7.5e-5, below the bf16 rounding of P); 2^r added to the exponent
-// field. x is clamped at -126 so the result stays a normal float (or underflows to ~0).
-__device__ __forceinline__ float2 exp2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
-  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23: round-to-int
-  const float2 t = __fadd2_rn(x, magic);
-  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
-  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
-  float2 q = __ffma2_rn(f, make_float2(0.05517164f, 0.05517164f), make_float2(0.24261114f, 0.24261114f));
-  q = __ffma2_rn(q, f, make_float2(0.69326097f, 0.69326097f));
-  q = __ffma2_rn(q, f, make_float2(0.99992806f, 0.99992806f));
-  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
-                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
-}
-// Which exponential pairs (of the 64 per row and tile) go to the FMA pipe instead of MUFU.
-__device__ __forceinline__ constexpr bool kPolyPair(int i) { return (i & 3) == 3; }
+// (An FMA-pipe polynomial exp2 for a fraction of the elements was measured as a net loss on
+// B200 at d = 64: the softmax is issue-bound, and the polynomial costs ~6 extra instructions per
+// element against one MUFU op. All exponentials go to MUFU ex2.)
 
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_bf16_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
@@ -142,11 +128,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&sm.q_full, 1);
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&sm.kv_full[i], 1);
-      mbar_init(&sm.kv_empty[i], 1);
+      mbar_init(&sm.kv_empty[i], 2);  // one commit per query tile
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.s_full[i], 1);
       mbar_init(&sm.p_full[i], 256);  // both halves of every row
+      mbar_init(&sm.s_loaded[i], 256);
+      mbar_init(&sm.pv_done[i], 1);
       mbar_init(&sm.o_done[i], 1);
     }
     fence_barrier_init();
@@ -187,108 +175,114 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    // The whole warp walks the schedule (waits are warp-wide); one elected lane issues.
-    // Descriptors are precomputed: a K step or a ring stage is a plain add to the start
-    // address field (addresses < 256 KiB, so the 14-bit field never carries).
-    const uint64_t dq0 = sdesc_sw128(smem_u32(sm.q[0]), 16, 1024);
-    const uint64_t dq1 = sdesc_sw128(smem_u32(sm.q[1]), 16, 1024);
-    const uint64_t dk0 = sdesc_sw128(smem_u32(sm.k[0]), 16, 1024);
-    const uint64_t dv0 = sdesc_sw128(smem_u32(sm.v[0]), 16, 1024);
+  } else if (warp == 1 || warp == 3) {
+    // ------------------------------------------------------------ MMA issuers
+    // One issuer warp per query tile (warp 1: tile 0, warp 3: tile 1), so the two tiles'
+    // softmax pipelines are not forced into lockstep by a single program order. The whole
+    // warp walks the schedule (waits are warp-wide); one elected lane issues. Descriptors are
+    // precomputed: a K step or a ring stage is a plain add to the start-address field.
+    const int qt = __shfl_sync(0xffffffffu, warp >> 1, 0);
+    const uint64_t dq = shfl0_u64(sdesc_sw128(smem_u32(sm.q[qt]), 16, 1024));
+    const uint64_t dk0 = shfl0_u64(sdesc_sw128(smem_u32(sm.k[0]), 16, 1024));
+    const uint64_t dv0 = shfl0_u64(sdesc_sw128(smem_u32(sm.v[0]), 16, 1024));
     constexpr uint64_t kStageStep = kTileBytes >> 4;
-    const uint32_t ts0 = tmem + col_s(0), ts1 = tmem + col_s(1);
-    const uint32_t to0 = tmem + col_o(0), to1 = tmem + col_o(1);
-    const uint32_t tp0 = tmem + col_p(0), tp1 = tmem + col_p(1);
-    auto qk = [&](uint32_t d, uint64_t dq, int st) {
+    const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint32_t ts = tmem_u + col_s(qt), to = tmem_u + col_o(qt), tp = tmem_u + col_p(qt);
+    auto qk = [&](int st) {
       const uint64_t dk = dk0 + st * kStageStep;
 #pragma unroll
-      for (int kk = 0; kk < kHeadDim / 16; ++kk) umma_ss(d, dq + kk * 2, dk + kk * 2, kIdescQK, kk > 0);
+      for (int kk = 0; kk < kHeadDim / 16; ++kk) umma_ss(ts, dq + kk * 2, dk + kk * 2, kIdescQK, kk > 0);
     };
-    auto pv = [&](uint32_t d, uint32_t tp, int st, bool acc) {
+    auto pv = [&](int st, bool acc) {
       const uint64_t dv = dv0 + st * kStageStep;
 #pragma unroll
-      for (int kk = 0; kk < kTileN / 16; ++kk) umma_ts(d, tp + kk * 8, dv + kk * 128, kIdescPV, (acc || kk > 0) ? 1u : 0u);
+      for (int kk = 0; kk < kTileN / 16; ++kk) umma_ts(to, tp + kk * 8, dv + kk * 128, kIdescPV, (acc || kk > 0) ? 1u : 0u);
     };
     mbar_wait(&sm.q_full, 0);
     mbar_wait(&sm.kv_full[0], 0);
+#ifdef MEA_FWD_STAGGER
+    if (qt == 1) mbar_wait(&sm.s_loaded[0], 0);  // start tile 1 half a step behind tile 0
+#endif
     tc_fence_after();
     if (elect_one()) {
-      qk(ts0, dq0, 0);
-      umma_commit(&sm.s_full[0]);
-      qk(ts1, dq1, 0);
-      umma_commit(&sm.s_full[1]);
+      qk(0);
+      umma_commit(&sm.s_full[qt]);
     }
     __syncwarp();
     for (int t = 0; t < T; ++t) {
       const int st = t % kStages;
       const int nx = (t + 1) % kStages;
       const bool more = (t + 1) < T;
-      // query tile 0: O0 += P0 V_t, then S0 = Q0 K_{t+1}^T
-      mbar_wait(&sm.p_full[0], t & 1);
-      if (more) mbar_wait(&sm.kv_full[nx], ((t + 1) / kStages) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        pv(to0, tp0, st, t > 0);
-        if (more) {
-          qk(ts0, dq0, nx);
-          umma_commit(&sm.s_full[0]);
-        } else {
-          umma_commit(&sm.o_done[0]);
+      // S_{t+1} = Q K_{t+1}^T as soon as the softmax warps have read S_t out of TMEM, so the
+      // next scores are computed while the current softmax runs.
+      if (more) {
+        mbar_wait(&sm.kv_full[nx], ((t + 1) / kStages) & 1);
+        mbar_wait(&sm.s_loaded[qt], t & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          qk(nx);
+          umma_commit(&sm.s_full[qt]);
         }
+        __syncwarp();
       }
-      __syncwarp();
-      // query tile 1
-      mbar_wait(&sm.p_full[1], t & 1);
+      // O += P_t V_t once P_t is in TMEM
+      mbar_wait(&sm.p_full[qt], t & 1);
       tc_fence_after();
       if (elect_one()) {
-        pv(to1, tp1, st, t > 0);
-        umma_commit(&sm.kv_empty[st]);  // K_t and V_t no longer read
-        if (more) {
-          qk(ts1, dq1, nx);
-          umma_commit(&sm.s_full[1]);
-        } else {
-          umma_commit(&sm.o_done[1]);
-        }
+        pv(st, t > 0);
+        umma_commit(&sm.pv_done[qt]);
+        umma_commit(&sm.kv_empty[st]);  // this tile is done with K_t, V_t (2 arrivals free it)
+        if (!more) umma_commit(&sm.o_done[qt]);
       }
       __syncwarp();
     }
   }
   } else {
     setmaxnreg_inc<kSoftmaxRegs>();
-    // ------------------------------------------------------------ softmax warpgroups
-    // Four warpgroups: WG (qt, half) owns query tile qt and the 64 score columns
-    // [64*half, 64*half + 64) of every 128-key tile. One thread = one (row, half): it keeps
-    // the row's reference max m* (identical in both halves) and its half of s*. The two
-    // halves of a row exchange their partial row max through shared memory once per tile.
+    // ------------------------------------------------------------ softmax warps
+    // 16 warps; warp (qt, sub, quarter) owns query tile qt, rows quarter*32 + sub*16 + [0,16).
+    // With the 16x32bx2 TMEM shape, lanes 0-15 hold score columns [0,64) of those rows and
+    // lanes 16-31 columns [64,128) of the same rows: the two halves of a row are lanes t and
+    // t^16 of one warp, so the row max and row sum combine with a single xor-shuffle. Every
+    // thread keeps the row's reference max m* (identical in both halves) and its half of s*.
     const int sw = warp - 4;
     const int qt = sw >> 3;
-    const int half = (sw >> 2) & 1;
+    const int sub = (sw >> 2) & 1;
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int rloc = quarter * 32 + lane;
+    const int half = lane >> 4;
+    const int rloc = quarter * 32 + sub * 16 + (lane & 15);
     const int row = q0 + qt * kTileM + rloc;
-    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-    const uint32_t colS = col_s(qt) + half * 64, colO = col_o(qt) + half * 32, colP = col_p(qt) + half * 32;
-    const uint32_t xbar = kBarX0 + qt;  // the 8 warps sharing query tile qt
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32 + sub * 16) << 16);
+    const uint32_t colS = col_s(qt), colO = col_o(qt), colP = col_p(qt);
     const float c = p.scale_log2;
     float m_ref = -INFINITY;  // reference max m*, log2 units of the scaled score
     float l = 0.f;            // this half's part of s*
+#ifdef MEA_EXP_TIMING
+    unsigned long long* tdbg = reinterpret_cast<unsigned long long*>(p.lse);
+    const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && quarter == 0 && sub == 0 && (lane & 15) == 0;
+#define TPROBE(k) if (probe && t >= 8 && t < 24) tdbg[((qt * 2 + half) * 16 + (t - 8)) * 8 + (k)] = clock64();
+#else
+#define TPROBE(k)
+#endif
     for (int t = 0; t < T; ++t) {
+      TPROBE(0)
       mbar_wait(&sm.s_full[qt], t & 1);
+      TPROBE(1)
       tc_fence_after();
       uint32_t sr[64];
-      tmem_ld32(lane_base + colS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld32(lane_base + colS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tmem_ld32_split<64>(lane_base + colS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld32_split<64>(lane_base + colS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
       tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&sm.s_loaded[qt]);  // S_t is in registers: the MMA may overwrite it with S_{t+1}
       const int tile_valid = key_end - (t_begin + t) * kTileN;  // keys of this tile in range
       const int valid = tile_valid - half * 64;                // ... of my half (may be <= 0)
-      float* xm = sm.xmax[qt][t & 1];
       uint32_t pk[32];  // P in bf16 pairs
       float ext = 0.f;
       bool have_ext = false;
       // Fast path (full tile, m* already set): exponentiate against the current reference max
-      // while the partial max is computed alongside; the exchanged full-row max only has to
-      // confirm that no score exceeds the reference by more than the lazy threshold.
+      // while the row max is computed alongside; the max only has to confirm that no score
+      // exceeds the reference by more than the lazy threshold (else: redo below, rare).
       bool fast = (t > 0) && (tile_valid >= kTileN) && (c >= 0.f);
       if (fast) {
         const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
@@ -300,22 +294,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (i & 1) mx1 = fmax3(mx1, s2.x, s2.y);
           else mx0 = fmax3(mx0, s2.x, s2.y);
           const float2 x = __ffma2_rn(s2, c2, nm2);  // s*c - m*
-          const float2 e = kPolyPair(i) ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          const float2 e = make_float2(ex2_approx(x.x), ex2_approx(x.y));
           rs = __fadd2_rn(rs, e);
           pk[i] = pack_bf16x2(e.x, e.y);
         }
-        const float mx = fmaxf(mx0, mx1);
-        xm[half * 128 + rloc] = mx;
-        named_bar_sync(xbar, 256);
-        const float mfull = fmaxf(mx, xm[(half ^ 1) * 128 + rloc]);
-        const bool need = mfull * c > m_ref + kLazyThreshold;
-        if (__any_sync(0xffffffffu, need)) {  // identical in both halves (same rows, same data)
-          fast = false;
+        float mx = fmaxf(mx0, mx1);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));  // full-row max
+        const bool need = mx * c > m_ref + kLazyThreshold;
+        if (__any_sync(0xffffffffu, need)) {  // warp-uniform: covers both halves of these rows
+          fast = false;  // redo from the raw scores (still in registers)
           have_ext = true;
-          ext = mfull;
-          tmem_ld32(lane_base + colS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-          tmem_ld32(lane_base + colS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-          tmem_ld_wait();
+          ext = mx;
         } else {
           l += rs.x + rs.y;
         }
@@ -329,16 +318,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 64; ++i)
               if (i < valid) e0 = fmaxf(e0, __uint_as_float(sr[i]));
+            ext = fmaxf(e0, __shfl_xor_sync(0xffffffffu, e0, 16));
           } else {
             e0 = INFINITY;
 #pragma unroll
             for (int i = 0; i < 64; ++i)
               if (i < valid) e0 = fminf(e0, __uint_as_float(sr[i]));
+            ext = fminf(e0, __shfl_xor_sync(0xffffffffu, e0, 16));
           }
-          xm[half * 128 + rloc] = e0;
-          named_bar_sync(xbar, 256);
-          const float e1 = xm[(half ^ 1) * 128 + rloc];
-          ext = (c >= 0.f) ? fmaxf(e0, e1) : fminf(e0, e1);
         }
         const float m_cand = ext * c;
         const bool need = m_cand > m_ref + kLazyThreshold;  // always true on the first tile
@@ -349,16 +336,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           l *= alpha;
         }
         if (t > 0 && __any_sync(0xffffffffu, need)) {
-          // v* <- v* alpha (my 32 of the row's 64 O columns). O is quiescent: S_t's commit
-          // covers PV_{t-1}.
+          // v* <- v* alpha (lanes 0-15: O columns [0,32), lanes 16-31: [32,64)), once PV_{t-1}
+          // has finished.
+          mbar_wait(&sm.pv_done[qt], (t - 1) & 1);
+          tc_fence_after();
 #pragma unroll
           for (int part = 0; part < 2; ++part) {
             uint32_t o[16];
-            tmem_ld16(lane_base + colO + part * 16, o);
+            tmem_ld16_split<32>(lane_base + colO + part * 16, o);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16(lane_base + colO + part * 16, o);
+            tmem_st16_split<32>(lane_base + colO + part * 16, o);
           }
         }
         // P = 2^(s c - m*) in bf16 pairs; s* += rowsum P
@@ -374,20 +363,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         l += rs0 + rs1;
       }
-      tmem_st32(lane_base + colP, pk);
+      TPROBE(4)
+      if (t > 0) mbar_wait(&sm.pv_done[qt], (t - 1) & 1);  // PV_{t-1} has consumed P_{t-1}
+      tc_fence_after();
+      tmem_st32_split<32>(lane_base + colP, pk);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm.p_full[qt]);
+      TPROBE(5)
     }
     // ------------------------------------------------------------ epilogue: out = v*/s*
-    float* xl = sm.xl[qt];
-    xl[half * 128 + rloc] = l;
-    named_bar_sync(xbar, 256);
-    const float lrow = l + xl[(half ^ 1) * 128 + rloc];  // s* of the whole row
+    const float lrow = l + __shfl_xor_sync(0xffffffffu, l, 16);  // s* of the whole row
     mbar_wait(&sm.o_done[qt], 0);
     tc_fence_after();
     uint32_t o[32];
-    tmem_ld32(lane_base + colO, o);
+    tmem_ld32_split<32>(lane_base + colO, o);
     tmem_ld_wait();
     if (row < p.n_q) {
       const size_t bh = (size_t)b * p.H + h;
@@ -420,7 +410,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             dst[i] = w;
           }
         }
+#ifndef MEA_EXP_TIMING
         if (p.lse && half == 0) p.lse[bh * p.n_q + row] = (m_ref + __log2f(lrow)) * 0.6931471805599453f;
+#endif
       }
     }
   }

@@ -1,0 +1,22 @@
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch, numpy as np
+from paper_2112_05682_b200 import _lib, api
+lib = ctypes.CDLL(sys.argv[1])
+for name, (res, args) in _lib.SIGNATURES.items():
+    f = getattr(lib, name); f.restype = res; f.argtypes = args
+_lib._lib = lib
+q = torch.empty((1, 16384, 16, 64), dtype=torch.bfloat16, device="cuda")
+k, v, do = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+for t, tid in ((q, 1), (k, 2), (v, 3), (do, 4)): api.mea_fill_synthetic(t, 0, tid)
+out, lse = api.mea_attention_fwd(q, k, v, want_lse=True)
+dv = torch.zeros_like(q)
+for _ in range(2): api.mea_attention_bwd(q, k, v, out, do, lse=lse, dv=dv)
+torch.cuda.synchronize()
+ts = dv.view(torch.int64).flatten()[:4*16*8].cpu().numpy().reshape(4, 16, 8).astype(np.int64)
+base = ts[0, 0, 0]
+names = ["wait_S", "compute", "wait_pfree", "store+arrive"]
+for g in range(4):
+    for i in range(3):
+        r = ts[g, i, :5] - base
+        print(f"g{g} i={i+8}", " ".join(f"{x:7d}" for x in r), "| dt:", " ".join(f"{n}={x}" for n, x in zip(names, np.diff(r))))

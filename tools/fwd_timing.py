@@ -12,9 +12,10 @@ for t, tid in ((q, 1), (k, 2), (v, 3)): api.mea_fill_synthetic(t, 0, tid)
 lse = torch.zeros((1, 16, 16384), dtype=torch.float32, device="cuda")
 for _ in range(3): out = api.mea_attention_fwd(q, k, v, lse=lse)
 torch.cuda.synchronize()
-ts = lse.view(torch.int64)[0, 0, :2*16*8].cpu().numpy().reshape(2, 16, 8).astype(np.int64)
+ts = lse.view(torch.int64)[0, 0, :4*16*8].cpu().numpy().reshape(4, 16, 8).astype(np.int64)
 base = ts[0, 0, 0]
-for wg in range(2):
-    for i in range(6):
-        r = ts[wg, i] - base
-        print(wg, i + 8, " ".join(f"{x:8d}" for x in r[:7]), " | dt:", " ".join(f"{x:6d}" for x in np.diff(r[:7])))
+names = ["wait_S", "compute", "xchg", "tail", "store+arrive"]
+for w in range(4):
+    for i in range(4):
+        r = ts[w, i, :6] - base
+        print(f"qt{w//2} half{w%2} t={i+8}", " ".join(f"{x:7d}" for x in r), "| dt:", " ".join(f"{n}={x}" for n, x in zip(names, np.diff(r))))
