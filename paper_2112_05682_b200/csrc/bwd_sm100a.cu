@@ -17,9 +17,10 @@
 //   dK += dST Q        (SS MMA, A = dST K-major, B = Q MN-major)       TMEM [384,448)
 //   dQ  = dS K         (SS MMA, A = dS MN-major, B = K MN-major)       TMEM [448,512)
 //   dQ drain warps: TMEM -> registers -> swizzled smem -> TMA reduce-add (f32) into dq_acc.
-// MMA issue order per query tile i:  ST_{i+1}, dPT_{i+1}, dV_i, dK_i, dQ_i, so the softmax of
-// tile i+1 runs while the tensor core computes the gradients of tile i. The softmax stores of
-// tile i+1 wait on "p_free" (all MMAs of tile i done).
+// MMA issue order: ST_{i+1}, dPT_{i+1} as soon as the softmax warps have read ST_i, dPT_i
+// ("s_loaded"), then dV_i, dK_i, dQ_i once P_i and dS_i are stored ("p_full"). The scores of
+// the next tile are computed under softmax i and the gradients of tile i under softmax i+1;
+// the softmax stores of tile i+1 wait on "p_free" (all MMAs of tile i done).
 //
 // Warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4-19 softmax (4 warpgroups,
 // warpgroup g owns query columns [32g, 32g+32) of each tile; thread = key row), 20-23 dQ drain.
@@ -177,24 +178,21 @@ __global__ void __launch_bounds__(kBThreads, 1)
       for (int i = 0; i < NQ; ++i) {
         const int st = i % kBStages;
         const bool more = i + 1 < NQ;
-        mbar_wait(&sm.p_full, i & 1);
-        if (more) mbar_wait(&sm.qdo_full[(i + 1) % kBStages], ((i + 1) / kBStages) & 1);
-        tc_fence_after();
-        const uint64_t q = dQ0 + st * kStep, o = dO0 + st * kStep;
-        if (elect_one()) {
-          // the next tile's scores first, so its softmax overlaps this tile's gradient MMAs
-          if (more) {
+        // the next tile's scores as soon as the softmax warps have read ST_i / dPT_i, so they
+        // are computed while softmax i runs
+        if (more) {
+          mbar_wait(&sm.qdo_full[(i + 1) % kBStages], ((i + 1) / kBStages) & 1);
+          mbar_wait(&sm.s_loaded, i & 1);
+          tc_fence_after();
+          if (elect_one()) {
             scores((i + 1) % kBStages);
             umma_commit(&sm.s_full);
           }
+          __syncwarp();
         }
-        __syncwarp();
-#ifdef MEA_BWD_HOLD_GRAD
-        // hold the gradient MMAs until the softmax warps have read ST/dPT of tile i+1: TMEM
-        // loads issued while the tensor core streams accumulators stall for hundreds of cycles
-        if (more) mbar_wait(&sm.s_loaded, (i + 1) & 1);
-#endif
+        mbar_wait(&sm.p_full, i & 1);
         tc_fence_after();
+        const uint64_t q = dQ0 + st * kStep, o = dO0 + st * kStep;
         if (elect_one()) {
           // dV += PT dO : K = 128 queries in steps of 16 (PT: 8 columns per step; dO: 16 rows)
 #pragma unroll
@@ -249,17 +247,8 @@ __global__ void __launch_bounds__(kBThreads, 1)
       tmem_ld32(lane_base + kColST + g * 32, sr);
       tmem_ld32(lane_base + kColDPT + g * 32, dr);
       tmem_ld_wait();
-#ifdef MEA_BWD_HOLD_GRAD
-      {
-        // consume the loaded registers so the arrive really follows the TMEM data
-        uint32_t x = 0;
-#pragma unroll
-        for (int u = 0; u < 32; ++u) x ^= sr[u] ^ dr[u];
-        asm volatile("" ::"r"(x));
-      }
       tc_fence_before();
-      if (i > 0) mbar_arrive(&sm.s_loaded);
-#endif
+      mbar_arrive(&sm.s_loaded);  // ST_i / dPT_i are in registers: the next scores may overwrite
       const float* l2 = sm.lse2[st] + g * 32;
       const float* dl = sm.delta[st] + g * 32;
       uint32_t pk[16], dk[16];

@@ -56,6 +56,7 @@ __host__ __device__ constexpr uint32_t col_s(int wg) { return wg ? 128u : 0u; }
 __host__ __device__ constexpr uint32_t col_o(int wg) { return wg ? 320u : 256u; }
 __host__ __device__ constexpr uint32_t col_p(int wg) { return wg ? 448u : 384u; }
 constexpr float kLazyThreshold = 8.0f;
+constexpr float kSafeSum = 18446744073709551616.0f;  // 2^64: bound on a tile's half-row sum of terms
 
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, false, false);  // A=Q K-major, B=K K-major
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 64, false, true);    // A=P (TMEM), B=V MN-major
@@ -287,26 +288,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (fast) {
         const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
         float2 rs = make_float2(0.f, 0.f);
-        float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const float2 s2 = make_float2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]));
-          if (i & 1) mx1 = fmax3(mx1, s2.x, s2.y);
-          else mx0 = fmax3(mx0, s2.x, s2.y);
           const float2 x = __ffma2_rn(s2, c2, nm2);  // s*c - m*
           const float2 e = make_float2(ex2_approx(x.x), ex2_approx(x.y));
           rs = __fadd2_rn(rs, e);
           pk[i] = pack_bf16x2(e.x, e.y);
         }
-        float mx = fmaxf(mx0, mx1);
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));  // full-row max
-        const bool need = mx * c > m_ref + kLazyThreshold;
+        // No row max here: the max only guards overflow, and every term is
+        // bounded by the row sum, so a finite row sum below 2^kSafeLog2 certifies that all
+        // 2^(s c - m*) terms (and hence P in bf16 and the fp32 sums) are safe. Otherwise redo
+        // the tile with the exact max (rare: the max must grow by > 2^kSafeLog2).
+        const float rsum = rs.x + rs.y;
+        const bool need = !(rsum <= kSafeSum);  // also catches inf / NaN
         if (__any_sync(0xffffffffu, need)) {  // warp-uniform: covers both halves of these rows
           fast = false;  // redo from the raw scores (still in registers)
-          have_ext = true;
-          ext = mx;
         } else {
-          l += rs.x + rs.y;
+          l += rsum;
         }
       }
       if (!fast) {
