@@ -111,22 +111,25 @@ class Clocks:
 
 
 # ----------------------------------------------------------------------------- reference arm
-def oracle_sample(rows, n=N, d=D, seed=0):
-    """Float64 oracle (oracle/) on a bounded sample of the workload: one head, the first
-    `rows` query rows against all n keys; forward (naive, O1) + backward (O6). Returns
-    (seconds, algorithmic flops of the sample)."""
+def oracle_sample(rows, n=N, d=D, seed=0, heads=1):
+    """Float64 oracle (oracle/) on a bounded sample of the workload: `heads` heads, the first
+    `rows` query rows of each against all n keys; forward (naive, O1) + backward (O6).
+    Returns (seconds, algorithmic flops of the sample)."""
     import numpy as np
     import oracle as O
     from synth import gen
     shape = (1, n, H, d)
-    q = gen.rows_of(shape, seed, gen.TENSOR_Q, 0, np.arange(rows), 0)
-    k = gen.rows_of(shape, seed, gen.TENSOR_K, 0, np.arange(n), 0)
-    v = gen.rows_of(shape, seed, gen.TENSOR_V, 0, np.arange(n), 0)
-    do = gen.rows_of(shape, seed, gen.TENSOR_DO, 0, np.arange(rows), 0)
-    t0 = time.perf_counter()
-    O.naive(q, k, v, 1 / math.sqrt(d))
-    O.backward(q, k, v, do, 1 / math.sqrt(d))
-    return time.perf_counter() - t0, 14 * rows * n * d
+    secs = 0.0
+    for h in range(heads):
+        q = gen.rows_of(shape, seed, gen.TENSOR_Q, 0, np.arange(rows), h)
+        k = gen.rows_of(shape, seed, gen.TENSOR_K, 0, np.arange(n), h)
+        v = gen.rows_of(shape, seed, gen.TENSOR_V, 0, np.arange(n), h)
+        do = gen.rows_of(shape, seed, gen.TENSOR_DO, 0, np.arange(rows), h)
+        t0 = time.perf_counter()
+        O.naive(q, k, v, 1 / math.sqrt(d))
+        O.backward(q, k, v, do, 1 / math.sqrt(d))
+        secs += time.perf_counter() - t0
+    return secs, 14 * rows * n * d * heads
 
 
 def cpu_cores():
@@ -384,10 +387,11 @@ def main():
     # ---------------- cpu baseline: the oracle on the host cores (rank 0, N == 1 only)
     cpu = None
     if world == 1 and not a.no_cpu_baseline:
-        rows = 2048
-        secs, fl = oracle_sample(rows, n=min(n, N), seed=a.seed)
+        rows, heads = 4096, 8    # ~10 s of host work on a 16-core box
+        secs, fl = oracle_sample(rows, n=min(n, N), seed=a.seed, heads=heads)
         cpu = {"value": fl / secs / 1e12, "unit": "TFLOP/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": f"float64 oracle fwd (O1) + bwd (O6): 1 head, {rows} query rows x {min(n, N)} keys, d=64",
+               "sample": f"float64 oracle fwd (O1) + bwd (O6): {heads} of {H} heads x {rows} query rows x "
+                         f"{min(n, N)} keys, d=64 (threads: numpy/OpenBLAS default)",
                "seconds": secs}
 
     if rank == 0:

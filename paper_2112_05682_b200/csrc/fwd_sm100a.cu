@@ -25,10 +25,10 @@
 // independent instruction streams to keep the exponential units busy (one warp per SMSP
 // reached only ~0.5 IPC on its dependency chains). The halves exchange their partial row
 // max through shared memory once per tile.
-// MMA issue order per key tile t:  PV0_t, S0_{t+1}, PV1_t, S1_{t+1}  so that softmax of one
-// tile overlaps the tensor-core work of the other. Because S0_{t+1} is issued
-// after PV0_t, the commit that signals S0_{t+1} also proves PV0_t finished: O0 is quiescent
-// while softmax 0 works on tile t+1, so the lazy O rescale needs no extra wait.
+// Per query tile, the issuer writes S_{t+1} = Q K_{t+1}^T as soon as the softmax warps have read
+// S_t out of TMEM ("s_loaded"), so scores are computed while the softmax runs; O += P_t V_t
+// follows once P_t is stored ("p_full"). The softmax waits "pv_done" of tile t-1 before it
+// overwrites P or rescales O (rare).
 //
 // TMEM columns (512 allocated): S0 [0,128) S1 [128,256) O0 [256,320) O1 [320,384)
 //                                P0 [384,448) P1 [448,512)  (P = bf16 pairs, 2 per column)
@@ -201,9 +201,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     mbar_wait(&sm.q_full, 0);
     mbar_wait(&sm.kv_full[0], 0);
-#ifdef MEA_FWD_STAGGER
-    if (qt == 1) mbar_wait(&sm.s_loaded[0], 0);  // start tile 1 half a step behind tile 0
-#endif
     tc_fence_after();
     if (elect_one()) {
       qk(0);

@@ -32,6 +32,7 @@ struct BwdParams {
   const float* delta;      // [B*H][nq_pad]: dO_i . O_i, 0 in the padding
   void* dk;                // [B,n_k,H,64] bf16
   void* dv;                // [B,n_k,H,64] bf16
+  float* dq_acc;           // [B,n_q,H,64] f32 accumulator (the TMA reduce target)
   int num_k_blocks;        // ceil(n_k / 128)
 };
 

@@ -432,6 +432,7 @@ mea_status_t mea_attention_bwd(const void* q, const void* k, const void* v, cons
   p.delta = delta;
   p.dk = dk;
   p.dv = dv;
+  p.dq_acc = dq_acc;
   p.num_k_blocks = (int)((n_k + kTileN - 1) / kTileN);
   {
     ProfScope ps("bwd_bf16", st);
