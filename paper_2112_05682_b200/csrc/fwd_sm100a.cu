@@ -105,9 +105,28 @@ __device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t p_tmem, const
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(a, fmaxf(b, c)); }
 
-// (An FMA-pipe polynomial exp2 for a fraction of the elements was measured as a net loss on
-// B200 at d = 64: the softmax is issue-bound, and the polynomial costs ~6 extra instructions per
-// element against one MUFU op. All exponentials go to MUFU ex2.)
+// 2^x on the FMA/ALU pipes for a pair: x = r + f, r = round(x), f in [-1/2, 1/2]; 2^f by a
+// degree-3 minimax polynomial (max relative error 7.5e-5, below the bf16 rounding of P); 2^r
+// added to the exponent field with one IMAD. x is clamped at -126. Used for the pairs selected
+// by kPolyEvery (0 = all exponentials on MUFU). Measured at configs[2]: every 16th pair 1.24 ms,
+// every 8th 1.24, every 4th 1.27, none 1.28 (MUFU alone is 16 exp/clk/SM, the polynomial 13).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));  // 1.5 * 2^23: round-to-int
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 q = __ffma2_rn(f, make_float2(0.05517164f, 0.05517164f), make_float2(0.24261114f, 0.24261114f));
+  q = __ffma2_rn(q, f, make_float2(0.69326097f, 0.69326097f));
+  q = __ffma2_rn(q, f, make_float2(0.99992806f, 0.99992806f));
+  return make_float2(__uint_as_float(__float_as_uint(t.x) * 8388608u + __float_as_uint(q.x)),
+                     __uint_as_float(__float_as_uint(t.y) * 8388608u + __float_as_uint(q.y)));
+}
+#ifndef MEA_POLY_EVERY
+#define MEA_POLY_EVERY 16
+#endif
+constexpr int kPolyEvery = MEA_POLY_EVERY;  // every kPolyEvery-th exponential pair on the FMA pipe
+__device__ __forceinline__ constexpr bool poly_pair(int i) { return kPolyEvery > 0 && (i % kPolyEvery) == kPolyEvery - 1; }
 
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_bf16_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
@@ -289,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 32; ++i) {
           const float2 s2 = make_float2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]));
           const float2 x = __ffma2_rn(s2, c2, nm2);  // s*c - m*
-          const float2 e = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          const float2 e = poly_pair(i) ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
           rs = __fadd2_rn(rs, e);
           pk[i] = pack_bf16x2(e.x, e.y);
         }
