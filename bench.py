@@ -277,11 +277,12 @@ def main():
     dom_ms = kernels[dom]["avg_ms"]
     achieved = dom_flops / (dom_ms * 1e-3) / 1e12 if dom_flops else None
     traffic = None
-    try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        traffic = tr.get(dom)
-    except Exception:
-        pass
+    if a.workload == "cfg3":   # profiles/traffic.json holds ncu captures at configs[2]/[3] shapes
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+            traffic = tr.get(dom)
+        except Exception:
+            pass
     roofline = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": pk["tflops"], "unit": "TFLOP/s",
                 "frac": (achieved / pk["tflops"]) if achieved else None, "traffic": traffic,
                 "peak_source": pk["source"] + " bf16 dense burst",

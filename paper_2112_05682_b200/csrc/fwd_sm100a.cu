@@ -287,25 +287,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       TPROBE(1)
       tc_fence_after();
       uint32_t sr[64];
-      tmem_ld32_split<64>(lane_base + colS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld32_split<64>(lane_base + colS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&sm.s_loaded[qt]);  // S_t is in registers: the MMA may overwrite it with S_{t+1}
       const int tile_valid = key_end - (t_begin + t) * kTileN;  // keys of this tile in range
       const int valid = tile_valid - half * 64;                // ... of my half (may be <= 0)
       uint32_t pk[32];  // P in bf16 pairs
       float ext = 0.f;
       bool have_ext = false;
-      // Fast path (full tile, m* already set): exponentiate against the current reference max
-      // while the row max is computed alongside; the max only has to confirm that no score
-      // exceeds the reference by more than the lazy threshold (else: redo below, rare).
+      // Fast path (full tile, m* already set): exponentiate against the current reference max.
+      // The second 32 score columns load while the first 32 are exponentiated.
       bool fast = (t > 0) && (tile_valid >= kTileN) && (c >= 0.f);
+      tmem_ld32_split<64>(lane_base + colS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
       if (fast) {
+        tmem_ld_wait();
+        tmem_ld32_split<64>(lane_base + colS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
         const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
         float2 rs = make_float2(0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
+          if (i == 16) {  // second half of the scores has landed; S_t may now be overwritten
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&sm.s_loaded[qt]);
+          }
           const float2 s2 = make_float2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]));
           const float2 x = __ffma2_rn(s2, c2, nm2);  // s*c - m*
           const float2 e = poly_pair(i) ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
@@ -313,9 +315,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[i] = pack_bf16x2(e.x, e.y);
         }
         // No row max here: the max only guards overflow, and every term is
-        // bounded by the row sum, so a finite row sum below 2^kSafeLog2 certifies that all
+        // bounded by the row sum, so a finite row sum below 2^64 certifies that all
         // 2^(s c - m*) terms (and hence P in bf16 and the fp32 sums) are safe. Otherwise redo
-        // the tile with the exact max (rare: the max must grow by > 2^kSafeLog2).
+        // the tile with the exact max (rare: the max must grow by > 2^64).
         const float rsum = rs.x + rs.y;
         const bool need = !(rsum <= kSafeSum);  // also catches inf / NaN
         if (__any_sync(0xffffffffu, need)) {  // warp-uniform: covers both halves of these rows
@@ -323,6 +325,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           l += rsum;
         }
+      } else {
+        tmem_ld32_split<64>(lane_base + colS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&sm.s_loaded[qt]);  // S_t is in registers: the MMA may overwrite it
       }
       if (!fast) {
         if (!have_ext) {

@@ -147,3 +147,25 @@ def test_empty_and_degenerate_calls():
     assert out.shape == (1, 0, 1, 64)
     with pytest.raises(api.EmptyKeysError):
         api.mea_attention_fwd(torch.zeros(1, 3, 1, 64, dtype=torch.bfloat16, device="cuda"), k[:, :0], k[:, :0])
+
+
+def test_config5_length_sampled_rows():
+    """configs[4]'s sequence length n = 2^20 (one (b,h) of it; heads are independent and the
+    bench shards them across GPUs): forward on the GPU, oracle on sampled query rows."""
+    from paper_2112_05682_b200 import api
+    from synth import gen
+    B, n, H, d = 1, 1 << 20, 1, 64
+    shape = (B, n, H, d)
+    q = torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+    k, v = torch.empty_like(q), torch.empty_like(q)
+    for t, tid in ((q, gen.TENSOR_Q), (k, gen.TENSOR_K), (v, gen.TENSOR_V)):
+        api.mea_fill_synthetic(t, 3, tid)
+    out, lse = api.mea_attention_fwd(q, k, v, want_lse=True)
+    torch.cuda.synchronize()
+    rows = np.array([0, 255, 256, 524287, n - 1])
+    kk = gen.normal_tensor(shape, 3, gen.TENSOR_K, "bf16").astype(np.float64)[0, :, 0]
+    vv = gen.normal_tensor(shape, 3, gen.TENSOR_V, "bf16").astype(np.float64)[0, :, 0]
+    qr = gen.rows_of(shape, 3, gen.TENSOR_Q, 0, rows, 0)
+    ref, ref_lse = O.naive(qr, kk, vv, 1 / 8)
+    Hh.assert_close_bf16(out[0, rows, 0].double().cpu().numpy(), ref)
+    assert np.abs(lse[0, 0, rows].double().cpu().numpy() - ref_lse).max() < 1e-3
