@@ -148,6 +148,25 @@ MEA_API mea_status_t mea_attention_bwd(const void* q, const void* k, const void*
                                float scale, const float* lse, void* workspace,
                                size_t workspace_bytes, void* stream);
 
+/*
+ * Deterministic backward: same contract and results as mea_attention_bwd (within tolerance), but
+ * dK/dV and dQ come from two kernels with no cross-CTA reduction, so the result is bitwise
+ * reproducible run to run and the workspace is only delta and lse (B*H*n_q*8 bytes, + lse and a
+ * forward-output scratch if lse is NULL) instead of the fp32 dQ accumulator. Costs two extra
+ * recomputed GEMMs per tile (slower than mea_attention_bwd).
+ */
+MEA_API mea_status_t mea_attention_bwd_deterministic(const void* q, const void* k, const void* v,
+                                                     const void* out, const void* dout, void* dq, void* dk,
+                                                     void* dv, int64_t B, int64_t H, int64_t n_q,
+                                                     int64_t n_k, int64_t d, mea_dtype_t dtype, float scale,
+                                                     const float* lse, void* workspace,
+                                                     size_t workspace_bytes, void* stream);
+
+MEA_API mea_status_t mea_attention_bwd_deterministic_workspace_size(int64_t B, int64_t H, int64_t n_q,
+                                                                    int64_t n_k, int64_t d,
+                                                                    mea_dtype_t dtype, int lse_given,
+                                                                    size_t* bytes);
+
 MEA_API mea_status_t mea_attention_bwd_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k,
                                               int64_t d, mea_dtype_t dtype, int lse_given,
                                               size_t* bytes);

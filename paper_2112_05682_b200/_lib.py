@@ -28,6 +28,10 @@ SIGNATURES = {
     "mea_attention_bwd": (_st, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _st, _f, _vp,
                                 _vp, _sz, _vp]),
     "mea_attention_bwd_workspace_size": (_st, [_i64, _i64, _i64, _i64, _i64, _st, _c.c_int, _c.POINTER(_sz)]),
+    "mea_attention_bwd_deterministic": (_st, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64,
+                                              _st, _f, _vp, _vp, _sz, _vp]),
+    "mea_attention_bwd_deterministic_workspace_size": (_st, [_i64, _i64, _i64, _i64, _i64, _st, _c.c_int,
+                                                             _c.POINTER(_sz)]),
     "mea_fill_synthetic": (_st, [_vp, _i64, _st, _c.c_uint64, _c.c_uint32, _i64, _vp]),
     "mea_debug_umma_tile": (_st, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "mea_profile_enable": (None, [_c.c_int]),

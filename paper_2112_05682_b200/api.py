@@ -171,8 +171,14 @@ def mea_attention_bwd_workspace_size(B, H, n_q, n_k, d, dtype, lse_given=True):
     return n.value
 
 
-def mea_attention_bwd(q, k, v, out, dout, lse=None, scale=None, dq=None, dk=None, dv=None, workspace=None):
-    """(dq, dk, dv) of out = attention(q, k, v) given dout (recompute-per-tile backward)."""
+def mea_attention_bwd_deterministic_workspace_size(B, H, n_q, n_k, d, dtype, lse_given=True):
+    n = ctypes.c_size_t(0)
+    _check(_lib.load().mea_attention_bwd_deterministic_workspace_size(B, H, n_q, n_k, d, dtype,
+                                                                      int(bool(lse_given)), ctypes.byref(n)))
+    return n.value
+
+
+def _bwd(fn, ws_fn, q, k, v, out, dout, lse, scale, dq, dk, dv, workspace):
     _cuda_contig(q, k, v, out, dout, lse, dq, dk, dv)
     B, n_q, H, d = q.shape
     n_k = k.shape[1]
@@ -182,11 +188,24 @@ def mea_attention_bwd(q, k, v, out, dout, lse=None, scale=None, dq=None, dk=None
     dk = torch.empty_like(k) if dk is None else dk
     dv = torch.empty_like(v) if dv is None else dv
     if workspace is None:
-        workspace = _workspace(mea_attention_bwd_workspace_size(B, H, n_q, n_k, d, dt, lse is not None), q.device)
-    _check(_lib.load().mea_attention_bwd(
-        _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv), B, H, n_q, n_k, d, dt,
-        scale, _ptr(lse), _ptr(workspace), workspace.numel() if workspace is not None else 0, _stream(q.device)))
+        workspace = _workspace(ws_fn(B, H, n_q, n_k, d, dt, lse is not None), q.device)
+    _check(fn(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv), B, H, n_q, n_k, d, dt,
+              scale, _ptr(lse), _ptr(workspace), workspace.numel() if workspace is not None else 0,
+              _stream(q.device)))
     return dq, dk, dv
+
+
+def mea_attention_bwd(q, k, v, out, dout, lse=None, scale=None, dq=None, dk=None, dv=None, workspace=None):
+    """(dq, dk, dv) of out = attention(q, k, v) given dout (recompute-per-tile backward)."""
+    return _bwd(_lib.load().mea_attention_bwd, mea_attention_bwd_workspace_size, q, k, v, out, dout, lse, scale,
+                dq, dk, dv, workspace)
+
+
+def mea_attention_bwd_deterministic(q, k, v, out, dout, lse=None, scale=None, dq=None, dk=None, dv=None,
+                                    workspace=None):
+    """Same as mea_attention_bwd, bitwise reproducible (no cross-CTA reduction), ~2 MiB workspace."""
+    return _bwd(_lib.load().mea_attention_bwd_deterministic, mea_attention_bwd_deterministic_workspace_size, q, k,
+                v, out, dout, lse, scale, dq, dk, dv, workspace)
 
 
 # ------------------------------------------------------------------------ generator / debug

@@ -1,0 +1,294 @@
+// bwd_det_sm100a.cu — dK and dV for the deterministic backward (mea_attention_bwd_deterministic),
+// recomputing every tile of scores from the saved per-row log-sum-exp instead of storing them
+// (the paper's checkpointed differentiation: "recomputed during
+// backpropagation"). The max carries no gradient (stop_gradient): with lse fixed
+// the derivative is the plain softmax VJP:
+//   P = exp(scale q k^T - lse),  dV = P^T dO,  dP = dO V^T,  delta_i = dO_i . O_i,
+//   dS = P o (dP - delta),  dK = scale dS^T Q     (dQ = scale dS K: bwd_dq_sm100a.cu).
+//
+// One CTA owns one tile of 128 keys of one (b, h) and loops over all query tiles of 128:
+//   ST  = K Q^T      (SS MMA, M=128 keys, N=128 queries)        TMEM [0,128)
+//   dPT = V dO^T     (SS MMA)                                   TMEM [128,256)
+//   softmax warps: PT = 2^(ST*c - lse2), dST = PT o (dPT - delta)  (c = scale log2 e,
+//                  lse2 = lse log2 e, both per query column) -> bf16 pairs into TMEM
+//   dV += PT dO      (TS MMA: A = PT from TMEM [256,320), B = dO MN-major)  TMEM [384,448)
+//   dK += dST Q      (TS MMA: A = dST from TMEM [320,384), B = Q MN-major)  TMEM [448,512)
+// Every MMA reads at most one 16 KiB operand tile from shared memory per 256 cycles. With dQ in
+// its own kernel (bwd_dq_sm100a.cu: 2 extra recomputed GEMMs) there is no cross-CTA dQ
+// reduction: the result is bitwise reproducible and the workspace is only delta and lse
+// (~2 MiB at configs[3] instead of the fused path's 66 MiB). Measured at configs[3]: 1.80 ms
+// here + 1.73 ms for dQ, against 3.09 ms for the fused (SMEM-bandwidth-bound) kernel.
+// Schedule: ST_{i+1}, dPT_{i+1} issue once the softmax warps have read tile i out of TMEM
+// ("s_loaded"); dV_i, dK_i once PT_i, dST_i are stored ("p_full"); the softmax stores of tile
+// i+1 wait on "p_free" (dV_i, dK_i done).
+// Warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4-19 softmax (4 warpgroups,
+// warpgroup g owns query columns [32g, 32g+32) of each tile; thread = key row).
+#include <cuda_bf16.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace mea {
+namespace {
+
+constexpr int kBStages = 3;  // Q/dO ring
+constexpr int kTile = 128;
+constexpr int kTileBytes = kTile * kHeadDim * 2;  // 16 KiB bf16 tile
+constexpr int kBThreads = 640;
+// setmaxnreg budgets. Measured on B200: setmaxnreg.inc only redistributes the registers the
+// CTA was launched with (640 threads x 96 = 480 per lane slot of each SM sub-partition, which
+// holds one control and four softmax warps); a larger total blocks forever. 64 + 4*104 = 480.
+constexpr int kBCtrlRegs = 64, kBSoftRegs = 104;
+constexpr uint32_t kColST = 0, kColDPT = 128, kColP = 256, kColDS = 320, kColDV = 384, kColDK = 448;
+
+constexpr uint32_t kIdSS = idesc_bf16_f32(128, 128, false, false);  // ST, dPT
+constexpr uint32_t kIdTS = idesc_bf16_f32(128, 64, false, true);    // dV, dK: A from TMEM, B MN-major
+
+struct BwdSmem {
+  uint8_t k[kTileBytes];
+  uint8_t v[kTileBytes];
+  uint8_t q[kBStages][kTileBytes];
+  uint8_t dout[kBStages][kTileBytes];
+  float lse2[kBStages][kTile];
+  float delta[kBStages][kTile];
+  uint64_t kv_full, qdo_full[kBStages], qdo_empty[kBStages];
+  uint64_t s_full, s_loaded, p_full, p_free, dkv_done;
+  uint32_t tmem_base;
+};
+constexpr size_t kBwdSmemBytes = sizeof(BwdSmem) + 1024;
+
+// 1024-byte alignment (128B-swizzle atoms) by pointer arithmetic on the __shared__ array, so
+// the compiler keeps the shared address space (LDS/STS instead of generic LD/ST).
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
+}
+
+// 1-D bulk copy global -> shared, completion on an mbarrier.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kBThreads, 1)
+    bwd_dkdv_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+                    const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
+                    const BwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  BwdSmem& sm = *reinterpret_cast<BwdSmem*>(align1024(smem_raw));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int k0 = kblk * kTile;
+  const int NQ = (p.n_q + kTile - 1) / kTile;
+  const int nq_pad = NQ * kTile;
+  const size_t bh = (size_t)b * p.H + h;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.kv_full, 1);
+    for (int i = 0; i < kBStages; ++i) {
+      mbar_init(&sm.qdo_full[i], 1);
+      mbar_init(&sm.qdo_empty[i], 1);
+    }
+    mbar_init(&sm.s_full, 1);
+    mbar_init(&sm.s_loaded, 512);
+    mbar_init(&sm.p_full, 512);
+    mbar_init(&sm.p_free, 1);
+    mbar_init(&sm.dkv_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mq);
+    tma_prefetch_desc(&mk);
+    tma_prefetch_desc(&mv);
+    tma_prefetch_desc(&mdo);
+  }
+  if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp < 4) {
+    setmaxnreg_dec<kBCtrlRegs>();
+    if (warp == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      const uint64_t keep = policy_evict_last();
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&sm.kv_full, 2 * kTileBytes);
+        tma_load_4d(sm.k, &mk, &sm.kv_full, 0, h, k0, b, keep);
+        tma_load_4d(sm.v, &mv, &sm.kv_full, 0, h, k0, b, keep);
+      }
+      __syncwarp();
+      for (int i = 0; i < NQ; ++i) {
+        const int st = i % kBStages, n = i / kBStages;
+        if (i >= kBStages) mbar_wait(&sm.qdo_empty[st], (n - 1) & 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&sm.qdo_full[st], 2 * kTileBytes + 2 * kTile * 4);
+          tma_load_4d(sm.q[st], &mq, &sm.qdo_full[st], 0, h, i * kTile, b, keep);
+          tma_load_4d(sm.dout[st], &mdo, &sm.qdo_full[st], 0, h, i * kTile, b, keep);
+          bulk_load(sm.lse2[st], p.lse2 + bh * nq_pad + i * kTile, kTile * 4, &sm.qdo_full[st]);
+          bulk_load(sm.delta[st], p.delta + bh * nq_pad + i * kTile, kTile * 4, &sm.qdo_full[st]);
+        }
+        __syncwarp();
+      }
+    } else if (warp == 1) {
+      // ---------------------------------------------------------------- MMA issuer
+      const uint64_t dK = shfl0_u64(sdesc_sw128(smem_u32(sm.k), 16, 1024));
+      const uint64_t dV = shfl0_u64(sdesc_sw128(smem_u32(sm.v), 16, 1024));
+      const uint64_t dQ0 = shfl0_u64(sdesc_sw128(smem_u32(sm.q[0]), 16, 1024));
+      const uint64_t dO0 = shfl0_u64(sdesc_sw128(smem_u32(sm.dout[0]), 16, 1024));
+      constexpr uint64_t kStep = kTileBytes >> 4;
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      auto scores = [&](int st) {  // ST = K Q^T ; dPT = V dO^T
+        const uint64_t q = dQ0 + st * kStep, o = dO0 + st * kStep;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) umma_ss(tm + kColST, dK + kk * 2, q + kk * 2, kIdSS, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) umma_ss(tm + kColDPT, dV + kk * 2, o + kk * 2, kIdSS, kk > 0);
+      };
+      mbar_wait(&sm.kv_full, 0);
+      mbar_wait(&sm.qdo_full[0], 0);
+      tc_fence_after();
+      if (elect_one()) {
+        scores(0);
+        umma_commit(&sm.s_full);
+      }
+      __syncwarp();
+      for (int i = 0; i < NQ; ++i) {
+        const int st = i % kBStages;
+        const bool more = i + 1 < NQ;
+        if (more) {
+          mbar_wait(&sm.qdo_full[(i + 1) % kBStages], ((i + 1) / kBStages) & 1);
+          mbar_wait(&sm.s_loaded, i & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            scores((i + 1) % kBStages);
+            umma_commit(&sm.s_full);
+          }
+          __syncwarp();
+        }
+        mbar_wait(&sm.p_full, i & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t q = dQ0 + st * kStep, o = dO0 + st * kStep;
+          // dV += PT dO ; dK += dST Q : K = 128 queries in steps of 16 (A: 8 TMEM columns per
+          // step; B: 16 rows of 128 B, MN-major)
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) umma_ts(tm + kColDV, tm + kColP + kk * 8, o + kk * 128, kIdTS, (i > 0 || kk > 0));
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) umma_ts(tm + kColDK, tm + kColDS + kk * 8, q + kk * 128, kIdTS, (i > 0 || kk > 0));
+          umma_commit(&sm.p_free);
+          umma_commit(&sm.qdo_empty[st]);
+          if (!more) umma_commit(&sm.dkv_done);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    setmaxnreg_inc<kBSoftRegs>();
+    // ------------------------------------------------------------------ softmax warpgroups
+    const int g = (warp - 4) >> 2;           // query columns [32g, 32g+32)
+    const int quarter = warp & 3;
+    const int j = quarter * 32 + lane;       // key row within the tile (TMEM lane)
+    const bool key_ok = k0 + j < p.n_k;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const float c = p.scale_log2;
+    const float2 c2 = make_float2(c, c);
+#ifdef MEA_EXP_TIMING
+    unsigned long long* tdbg = reinterpret_cast<unsigned long long*>(p.dv);
+    const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && quarter == 0 && lane == 0;
+#define TPROBE(k) if (probe && i >= 8 && i < 24) tdbg[(g * 16 + (i - 8)) * 8 + (k)] = clock64();
+#else
+#define TPROBE(k)
+#endif
+    for (int i = 0; i < NQ; ++i) {
+      const int st = i % kBStages;
+      TPROBE(0)
+      mbar_wait(&sm.s_full, i & 1);
+      TPROBE(1)
+      tc_fence_after();
+      uint32_t sr[32], dr[32];
+      tmem_ld32(lane_base + kColST + g * 32, sr);
+      tmem_ld32(lane_base + kColDPT + g * 32, dr);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&sm.s_loaded);  // ST_i / dPT_i are in registers: the next scores may overwrite
+      const float* l2 = sm.lse2[st] + g * 32;
+      const float* dl = sm.delta[st] + g * 32;
+      uint32_t pk[16], dk[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
+        const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
+        const float2 lq = *reinterpret_cast<const float2*>(l2 + 2 * u);
+        const float2 de = *reinterpret_cast<const float2*>(dl + 2 * u);
+        const float2 x = __ffma2_rn(s2, c2, make_float2(-lq.x, -lq.y));  // s c - lse2
+        float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));        // P (lse2 = +inf pads -> 0)
+        if (!key_ok) pr = make_float2(0.f, 0.f);
+        const float2 ds = __fmul2_rn(pr, __fadd2_rn(d2, make_float2(-de.x, -de.y)));  // P (dP - delta)
+        pk[u] = pack_bf16x2(pr.x, pr.y);
+        dk[u] = pack_bf16x2(ds.x, ds.y);
+      }
+      TPROBE(2)
+      if (i > 0) mbar_wait(&sm.p_free, (i - 1) & 1);  // dV_{i-1}, dK_{i-1} no longer read PT / dST
+      TPROBE(3)
+      tc_fence_after();
+      tmem_st16(lane_base + kColP + g * 16, pk);
+      tmem_st16(lane_base + kColDS + g * 16, dk);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&sm.p_full);
+      TPROBE(4)
+    }
+    // ------------------------------------------------------------------ dV, dK epilogue
+    if (g < 2) {
+      mbar_wait(&sm.dkv_done, 0);
+      tc_fence_after();
+      uint32_t r[64];
+      const uint32_t col = (g == 0) ? kColDV : kColDK;
+      tmem_ld32(lane_base + col, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+      tmem_ld32(lane_base + col + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+      tmem_ld_wait();
+#ifdef MEA_EXP_TIMING
+      if (false) {
+#else
+      if (key_ok) {
+#endif
+        const float sc = (g == 0) ? 1.f : p.scale;
+        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g == 0 ? p.dv : p.dk) +
+                             (((size_t)b * p.n_k + k0 + j) * p.H + h) * kHeadDim;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(r[8 * u + 0]) * sc, __uint_as_float(r[8 * u + 1]) * sc);
+          w.y = pack_bf16x2(__uint_as_float(r[8 * u + 2]) * sc, __uint_as_float(r[8 * u + 3]) * sc);
+          w.z = pack_bf16x2(__uint_as_float(r[8 * u + 4]) * sc, __uint_as_float(r[8 * u + 5]) * sc);
+          w.w = pack_bf16x2(__uint_as_float(r[8 * u + 6]) * sc, __uint_as_float(r[8 * u + 7]) * sc);
+          reinterpret_cast<uint4*>(dst)[u] = w;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_bwd_dkdv(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                            const CUtensorMap& mdo, cudaStream_t s) {
+  static cudaError_t attr =
+      cudaFuncSetAttribute(bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmemBytes);
+  if (attr != cudaSuccess) return attr;
+  dim3 grid(p.num_k_blocks, p.H, p.B);
+  bwd_dkdv_kernel<<<grid, kBThreads, kBwdSmemBytes, s>>>(mq, mk, mv, mdo, p);
+  return cudaGetLastError();
+}
+
+}  // namespace mea

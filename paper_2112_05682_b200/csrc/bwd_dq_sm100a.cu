@@ -1,0 +1,266 @@
+// bwd_dq_sm100a.cu — dQ of exact attention on tcgen05 tensor cores (second backward kernel).
+//
+// dQ = scale * dS K with dS = P o (dP - delta), P = exp(scale q k^T - lse), dP = dO V^T
+// (the softmax VJP; the paper differentiates with jax.grad through jax.checkpoint,
+// PAPER.md:254-261, and recomputes every tile of scores). One CTA owns 128 query
+// rows of one (b, h) and loops over all key tiles of 128, so dQ accumulates in TMEM and is
+// written once, in bf16: deterministic, no fp32 accumulator, no atomics.
+//   S  = Q K^T    (SS MMA, M=128 queries, N=128 keys)     TMEM [0,128)
+//   dP = dO V^T   (SS MMA)                                TMEM [128,256)
+//   softmax warps: P = 2^(S c - lse2_row), dS = P o (dP - delta_row) -> bf16 -> TMEM
+//                  [320,384) / [384,448) alternately (double buffer)
+//   dQ += dS K    (TS MMA: A = dS from TMEM, B = K MN-major, N=64)  TMEM [256,320)
+// Per query row lse and delta are scalars (no per-element loads). Padded key rows (K, V zero-
+// filled by TMA) give dS * 0 = 0 in dQ, so ragged key tiles need no mask.
+// Schedule: S_{t+1}, dP_{t+1} are issued once the softmax warps have read S_t, dP_t out of TMEM
+// ("s_loaded"); dQ_t once dS_t is stored ("p_full"); with two dS buffers the softmax only waits
+// for dQ_{t-2} ("ds_free") before overwriting one.
+// Warps: 0 TMA producer (Q, dO once; 4-stage K/V ring), 1 MMA issuer, 2 TMEM allocator,
+// 4-19 softmax: warp (colhalf, sub, quarter) owns rows quarter*32 + sub*16 + [0,16) and key
+// columns colhalf*64 + [0,64), lanes 0-15 / 16-31 taking the two 32-column halves (16x32bx2).
+#include <cuda_bf16.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace mea {
+namespace {
+
+constexpr int kQStages = 4;
+constexpr int kTile = 128;
+constexpr int kTileBytes = kTile * kHeadDim * 2;
+constexpr int kQThreads = 640;
+constexpr int kQCtrlRegs = 64, kQSoftRegs = 104;  // 64 + 4*104 = 480 = launch budget per lane slot
+constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256;
+__device__ __forceinline__ uint32_t col_ds(int buf) { return buf ? 384u : 320u; }  // dS double buffer
+
+constexpr uint32_t kIdSS = idesc_bf16_f32(128, 128, false, false);  // S, dP
+constexpr uint32_t kIdDQ = idesc_bf16_f32(128, 64, false, true);    // A = dS (TMEM), B = K MN-major
+
+struct DqSmem {
+  uint8_t q[kTileBytes];
+  uint8_t dout[kTileBytes];
+  uint8_t k[kQStages][kTileBytes];
+  uint8_t v[kQStages][kTileBytes];
+  uint64_t q_full, kv_full[kQStages], kv_empty[kQStages];
+  uint64_t s_full, s_loaded, p_full, ds_free[2], o_done;
+  uint32_t tmem_base;
+};
+constexpr size_t kDqSmemBytes = sizeof(DqSmem) + 1024;
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
+}
+
+__global__ void __launch_bounds__(kQThreads, 1)
+    bwd_dq_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+                  const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
+                  const BwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  DqSmem& sm = *reinterpret_cast<DqSmem*>(align1024(smem_raw));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int q0 = qblk * kTile;
+  const int T = (p.n_k + kTile - 1) / kTile;
+  const int nq_pad = (p.n_q + kTile - 1) / kTile * kTile;
+  const size_t bh = (size_t)b * p.H + h;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.q_full, 1);
+    for (int i = 0; i < kQStages; ++i) {
+      mbar_init(&sm.kv_full[i], 1);
+      mbar_init(&sm.kv_empty[i], 1);
+    }
+    mbar_init(&sm.s_full, 1);
+    mbar_init(&sm.s_loaded, 512);
+    mbar_init(&sm.p_full, 512);
+    mbar_init(&sm.ds_free[0], 1);
+    mbar_init(&sm.ds_free[1], 1);
+    mbar_init(&sm.o_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mq);
+    tma_prefetch_desc(&mk);
+    tma_prefetch_desc(&mv);
+    tma_prefetch_desc(&mdo);
+  }
+  if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp < 4) {
+    setmaxnreg_dec<kQCtrlRegs>();
+    if (warp == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
+        tma_load_4d(sm.q, &mq, &sm.q_full, 0, h, q0, b, once);
+        tma_load_4d(sm.dout, &mdo, &sm.q_full, 0, h, q0, b, once);
+      }
+      __syncwarp();
+      for (int t = 0; t < T; ++t) {
+        const int st = t % kQStages, n = t / kQStages;
+        if (t >= kQStages) mbar_wait(&sm.kv_empty[st], (n - 1) & 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTileBytes);
+          tma_load_4d(sm.k[st], &mk, &sm.kv_full[st], 0, h, t * kTile, b, keep);
+          tma_load_4d(sm.v[st], &mv, &sm.kv_full[st], 0, h, t * kTile, b, keep);
+        }
+        __syncwarp();
+      }
+    } else if (warp == 1) {
+      // ---------------------------------------------------------------- MMA issuer
+      const uint64_t dQd = shfl0_u64(sdesc_sw128(smem_u32(sm.q), 16, 1024));
+      const uint64_t dOd = shfl0_u64(sdesc_sw128(smem_u32(sm.dout), 16, 1024));
+      const uint64_t dK0 = shfl0_u64(sdesc_sw128(smem_u32(sm.k[0]), 16, 1024));
+      const uint64_t dV0 = shfl0_u64(sdesc_sw128(smem_u32(sm.v[0]), 16, 1024));
+      constexpr uint64_t kStep = kTileBytes >> 4;
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      auto scores = [&](int st) {  // S = Q K^T ; dP = dO V^T
+        const uint64_t kd = dK0 + st * kStep, vd = dV0 + st * kStep;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) umma_ss(tm + kColS, dQd + kk * 2, kd + kk * 2, kIdSS, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) umma_ss(tm + kColDP, dOd + kk * 2, vd + kk * 2, kIdSS, kk > 0);
+      };
+      mbar_wait(&sm.q_full, 0);
+      mbar_wait(&sm.kv_full[0], 0);
+      tc_fence_after();
+      if (elect_one()) {
+        scores(0);
+        umma_commit(&sm.s_full);
+      }
+      __syncwarp();
+      for (int t = 0; t < T; ++t) {
+        const int st = t % kQStages, nx = (t + 1) % kQStages;
+        const bool more = t + 1 < T;
+        if (more) {
+          mbar_wait(&sm.kv_full[nx], ((t + 1) / kQStages) & 1);
+          mbar_wait(&sm.s_loaded, t & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            scores(nx);
+            umma_commit(&sm.s_full);
+          }
+          __syncwarp();
+        }
+        mbar_wait(&sm.p_full, t & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          // dQ += dS K : K = 128 keys in steps of 16 (dS: 8 TMEM columns; K rows: 2048 B)
+          const uint64_t kd = dK0 + st * kStep;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) umma_ts(tm + kColDQ, tm + col_ds(t & 1) + kk * 8, kd + kk * 128, kIdDQ, (t > 0 || kk > 0));
+          umma_commit(&sm.ds_free[t & 1]);
+          umma_commit(&sm.kv_empty[st]);
+          if (!more) umma_commit(&sm.o_done);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    setmaxnreg_inc<kQSoftRegs>();
+    // ------------------------------------------------------------------ softmax warps
+    const int sw = warp - 4;
+    const int colhalf = sw >> 3;
+    const int sub = (sw >> 2) & 1;
+    const int quarter = warp & 3;
+    const int rloc = quarter * 32 + sub * 16 + (lane & 15);
+    const int row = q0 + rloc;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32 + sub * 16) << 16);
+    const float c = p.scale_log2;
+    const float2 c2 = make_float2(c, c);
+    const float lse2 = p.lse2[bh * nq_pad + q0 + rloc];   // +inf on padded rows -> P = 0
+    const float delta = p.delta[bh * nq_pad + q0 + rloc];
+    const float2 nl2 = make_float2(-lse2, -lse2), nd2 = make_float2(-delta, -delta);
+#ifdef MEA_EXP_TIMING
+    unsigned long long* tdbg = reinterpret_cast<unsigned long long*>(p.dq);
+    const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && quarter == 0 && sub == 0 && lane == 0;
+#define TPROBE(k) if (probe && t >= 8 && t < 24) tdbg[(colhalf * 16 + (t - 8)) * 8 + (k)] = clock64();
+#else
+#define TPROBE(k)
+#endif
+    for (int t = 0; t < T; ++t) {
+      TPROBE(0)
+      mbar_wait(&sm.s_full, t & 1);
+      TPROBE(1)
+      tc_fence_after();
+      uint32_t sr[32], dr[32];
+      tmem_ld32_split<32>(lane_base + kColS + colhalf * 64, sr);
+      tmem_ld32_split<32>(lane_base + kColDP + colhalf * 64, dr);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&sm.s_loaded);  // S_t, dP_t are in registers: the next scores may overwrite them
+      TPROBE(2)
+      uint32_t pk[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
+        const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
+        const float2 x = __ffma2_rn(s2, c2, nl2);                              // s c - lse2
+        const float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));       // P
+        const float2 ds = __fmul2_rn(pr, __fadd2_rn(d2, nd2));                 // P (dP - delta)
+        pk[u] = pack_bf16x2(ds.x, ds.y);
+      }
+      TPROBE(3)
+      if (t > 1) mbar_wait(&sm.ds_free[t & 1], ((t >> 1) - 1) & 1);  // dQ_{t-2} has consumed this buffer
+      TPROBE(4)
+      tc_fence_after();
+      tmem_st16_split<16>(lane_base + col_ds(t & 1) + colhalf * 32, pk);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&sm.p_full);
+      TPROBE(5)
+    }
+    // ------------------------------------------------------------------ epilogue: dq = scale dQ
+    mbar_wait(&sm.o_done, 0);
+    tc_fence_after();
+    uint32_t o[16];
+    tmem_ld16_split<16>(lane_base + kColDQ + colhalf * 32, o);
+    tmem_ld_wait();
+#ifdef MEA_EXP_TIMING
+    if (false) {
+#else
+    if (row < p.n_q) {
+#endif
+      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.dq) +
+                           (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + colhalf * 32 + (lane >> 4) * 16;
+      uint4 w0, w1;
+      const float sc = p.scale;
+      w0.x = pack_bf16x2(__uint_as_float(o[0]) * sc, __uint_as_float(o[1]) * sc);
+      w0.y = pack_bf16x2(__uint_as_float(o[2]) * sc, __uint_as_float(o[3]) * sc);
+      w0.z = pack_bf16x2(__uint_as_float(o[4]) * sc, __uint_as_float(o[5]) * sc);
+      w0.w = pack_bf16x2(__uint_as_float(o[6]) * sc, __uint_as_float(o[7]) * sc);
+      w1.x = pack_bf16x2(__uint_as_float(o[8]) * sc, __uint_as_float(o[9]) * sc);
+      w1.y = pack_bf16x2(__uint_as_float(o[10]) * sc, __uint_as_float(o[11]) * sc);
+      w1.z = pack_bf16x2(__uint_as_float(o[12]) * sc, __uint_as_float(o[13]) * sc);
+      w1.w = pack_bf16x2(__uint_as_float(o[14]) * sc, __uint_as_float(o[15]) * sc);
+      reinterpret_cast<uint4*>(dst)[0] = w0;
+      reinterpret_cast<uint4*>(dst)[1] = w1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_bwd_dq(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                          const CUtensorMap& mdo, cudaStream_t s) {
+  static cudaError_t attr =
+      cudaFuncSetAttribute(bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDqSmemBytes);
+  if (attr != cudaSuccess) return attr;
+  dim3 grid((p.n_q + kTile - 1) / kTile, p.H, p.B);
+  bwd_dq_kernel<<<grid, kQThreads, kDqSmemBytes, s>>>(mq, mk, mv, mdo, p);
+  return cudaGetLastError();
+}
+
+}  // namespace mea

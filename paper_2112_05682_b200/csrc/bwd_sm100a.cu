@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
 }
 
 // delta_i = dO_i . O_i, lse2 = lse log2 e, both padded to a multiple of 128 rows
-// per (b,h) (pads: delta 0, lse2 +inf so padded query rows get P = 0); dq_acc = 0.
+// per (b,h) (pads: delta 0, lse2 +inf so padded query rows get P = 0); dq_acc = 0 when given.
 // 8 threads per row, 16-byte loads.
 __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ dout,
                                       const float* __restrict__ lse, float* __restrict__ delta,
@@ -380,9 +380,11 @@ __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ out, con
       acc = fmaf(__uint_as_float(ow[u] << 16), __uint_as_float(dw[u] << 16), acc);
       acc = fmaf(__uint_as_float(ow[u] & 0xFFFF0000u), __uint_as_float(dw[u] & 0xFFFF0000u), acc);
     }
-    float4* z = reinterpret_cast<float4*>(dq_acc + off);
-    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (dq_acc) {
+      float4* z = reinterpret_cast<float4*>(dq_acc + off);
+      z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
   acc += __shfl_xor_sync(0xffffffffu, acc, 1);
   acc += __shfl_xor_sync(0xffffffffu, acc, 2);

@@ -32,7 +32,8 @@ struct BwdParams {
   const float* delta;      // [B*H][nq_pad]: dO_i . O_i, 0 in the padding
   void* dk;                // [B,n_k,H,64] bf16
   void* dv;                // [B,n_k,H,64] bf16
-  float* dq_acc;           // [B,n_q,H,64] f32 accumulator (the TMA reduce target)
+  void* dq;                // [B,n_q,H,64] bf16 (deterministic path writes it directly)
+  float* dq_acc;           // [B,n_q,H,64] f32 reduction target (fused path)
   int num_k_blocks;        // ceil(n_k / 128)
 };
 
@@ -59,12 +60,16 @@ cudaError_t launch_merge_partials(const float* m, const float* s, const float* v
                                   void* out, int out_f32, cudaStream_t st);
 
 // backward
+// dq_acc nullable: zeroed when given (fused path)
 cudaError_t launch_bwd_preprocess(const void* out, const void* dout, const float* lse, float* delta, float* lse2,
                                   float* dq_acc, int B, int H, int n_q, cudaStream_t s);
-cudaError_t launch_bwd_bf16(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
-                            const CUtensorMap& mv, const CUtensorMap& mdo, const CUtensorMap& mdq,
-                            cudaStream_t s);
+cudaError_t launch_bwd_bf16(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                            const CUtensorMap& mdo, const CUtensorMap& mdq, cudaStream_t s);
 cudaError_t launch_dq_convert(const float* dq_acc, void* dq, int64_t numel, float scale, cudaStream_t s);
+cudaError_t launch_bwd_dkdv(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                            const CUtensorMap& mdo, cudaStream_t s);
+cudaError_t launch_bwd_dq(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                          const CUtensorMap& mdo, cudaStream_t s);
 
 // generator
 cudaError_t launch_fill_synthetic(void* dst, int64_t numel, int bf16, uint64_t seed, uint32_t tid,

@@ -338,14 +338,16 @@ struct BwdLayout {
   size_t delta, lse2, dq_acc, lse_tmp, out_tmp, total;
 };
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-BwdLayout bwd_layout(int64_t B, int64_t H, int64_t n_q, int64_t d, bool lse_given) {
+BwdLayout bwd_layout(int64_t B, int64_t H, int64_t n_q, int64_t d, bool lse_given, bool fused) {
   const size_t nq_pad = (size_t)((n_q + kTileM - 1) / kTileM) * kTileM;
   const size_t rows_pad = (size_t)B * H * nq_pad;
   BwdLayout L{};
   size_t off = 0;
   L.delta = off;  off = align256(off + rows_pad * sizeof(float));
   L.lse2 = off;   off = align256(off + rows_pad * sizeof(float));
-  L.dq_acc = off; off = align256(off + (size_t)B * n_q * H * d * sizeof(float));
+  if (fused) {  // the fused kernel's dQ reduction target
+    L.dq_acc = off; off = align256(off + (size_t)B * n_q * H * d * sizeof(float));
+  }
   if (!lse_given) {
     L.lse_tmp = off; off = align256(off + (size_t)B * H * n_q * sizeof(float));
     L.out_tmp = off; off = align256(off + (size_t)B * n_q * H * d * 2);
@@ -360,14 +362,16 @@ mea_status_t mea_attention_bwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
   if (!bytes) return fail(MEA_ERR_INVALID_VALUE, "bytes is NULL");
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
   if (!valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  *bytes = bwd_layout(B, H, n_q, d, lse_given != 0).total;
+  *bytes = bwd_layout(B, H, n_q, d, lse_given != 0, true).total;
   return MEA_OK;
 }
 
-mea_status_t mea_attention_bwd(const void* q, const void* k, const void* v, const void* out, const void* dout, void* dq,
-                               void* dk, void* dv, int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
-                               mea_dtype_t dtype, float scale, const float* lse, void* workspace,
-                               size_t workspace_bytes, void* stream) {
+}  // extern "C"
+
+static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const void* out, const void* dout, void* dq,
+                             void* dk, void* dv, int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                             mea_dtype_t dtype, float scale, const float* lse, void* workspace,
+                             size_t workspace_bytes, void* stream, bool fused) {
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, scale)) return s;
   if (!valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
   if (n_k == 0) return fail(MEA_ERR_EMPTY_KEYS, "attention over an empty key list");
@@ -386,13 +390,13 @@ mea_status_t mea_attention_bwd(const void* q, const void* k, const void* v, cons
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(dout) || !aligned16(dq) ||
       !aligned16(dk) || !aligned16(dv))
     return fail(MEA_ERR_MISALIGNED, "tensors must be 16-byte aligned");
-  const BwdLayout L = bwd_layout(B, H, n_q, d, lse != nullptr);
+  const BwdLayout L = bwd_layout(B, H, n_q, d, lse != nullptr, fused);
   if (!workspace || workspace_bytes < L.total) return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "backward workspace");
   if (!aligned16(workspace)) return fail(MEA_ERR_MISALIGNED, "workspace must be 16-byte aligned");
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   float* delta = reinterpret_cast<float*>(ws + L.delta);
   float* lse2 = reinterpret_cast<float*>(ws + L.lse2);
-  float* dq_acc = reinterpret_cast<float*>(ws + L.dq_acc);
+  float* dq_acc = fused ? reinterpret_cast<float*>(ws + L.dq_acc) : nullptr;
 
   CUtensorMap mq, mk, mv, mdo, mdq;
   const char* why = "";
@@ -404,8 +408,8 @@ mea_status_t mea_attention_bwd(const void* q, const void* k, const void* v, cons
                          CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
       (e = make_bnhd_map(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
                          CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
-      (e = make_bnhd_map(&mdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, n_q, H, d, 32, kTileM,
-                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess)
+      (fused && (e = make_bnhd_map(&mdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, n_q, H, d, 32, kTileM,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess))
     return cuda_fail(e, why);
 
   if (!lse) {
@@ -433,17 +437,55 @@ mea_status_t mea_attention_bwd(const void* q, const void* k, const void* v, cons
   p.dk = dk;
   p.dv = dv;
   p.dq_acc = dq_acc;
+  p.dq = dq;
+  p.dq_acc = dq_acc;
   p.num_k_blocks = (int)((n_k + kTileN - 1) / kTileN);
-  {
-    ProfScope ps("bwd_bf16", st);
-    if ((e = launch_bwd_bf16(p, mq, mk, mv, mdo, mdq, st)) != cudaSuccess) return cuda_fail(e, "bwd_bf16 launch");
-  }
-  {
+  if (fused) {
+    {
+      ProfScope ps("bwd_bf16", st);
+      if ((e = launch_bwd_bf16(p, mq, mk, mv, mdo, mdq, st)) != cudaSuccess) return cuda_fail(e, "bwd_bf16 launch");
+    }
     ProfScope ps("dq_convert", st);
     if ((e = launch_dq_convert(dq_acc, dq, B * n_q * H * d, scale, st)) != cudaSuccess)
       return cuda_fail(e, "dq_convert launch");
+  } else {
+    {
+      ProfScope ps("bwd_dkdv", st);
+      if ((e = launch_bwd_dkdv(p, mq, mk, mv, mdo, st)) != cudaSuccess) return cuda_fail(e, "bwd_dkdv launch");
+    }
+    ProfScope ps("bwd_dq", st);
+    if ((e = launch_bwd_dq(p, mq, mk, mv, mdo, st)) != cudaSuccess) return cuda_fail(e, "bwd_dq launch");
   }
   return MEA_OK;
+}
+
+extern "C" {
+
+mea_status_t mea_attention_bwd(const void* q, const void* k, const void* v, const void* out, const void* dout, void* dq,
+                               void* dk, void* dv, int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                               mea_dtype_t dtype, float scale, const float* lse, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  return bwd_impl(q, k, v, out, dout, dq, dk, dv, B, H, n_q, n_k, d, dtype, scale, lse, workspace, workspace_bytes,
+                  stream, true);
+}
+
+mea_status_t mea_attention_bwd_deterministic_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k,
+                                                            int64_t d, mea_dtype_t dtype, int lse_given,
+                                                            size_t* bytes) {
+  if (!bytes) return fail(MEA_ERR_INVALID_VALUE, "bytes is NULL");
+  if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
+  if (!valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  *bytes = bwd_layout(B, H, n_q, d, lse_given != 0, false).total;
+  return MEA_OK;
+}
+
+mea_status_t mea_attention_bwd_deterministic(const void* q, const void* k, const void* v, const void* out,
+                                             const void* dout, void* dq, void* dk, void* dv, int64_t B, int64_t H,
+                                             int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t dtype, float scale,
+                                             const float* lse, void* workspace, size_t workspace_bytes,
+                                             void* stream) {
+  return bwd_impl(q, k, v, out, dout, dq, dk, dv, B, H, n_q, n_k, d, dtype, scale, lse, workspace, workspace_bytes,
+                  stream, false);
 }
 
 // ------------------------------------------------------------------ generator / debug

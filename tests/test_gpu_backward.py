@@ -18,23 +18,37 @@ from tests import helpers as Hh
 pytestmark = pytest.mark.gpu
 
 
-def _bwd(q, k, v, do, scale=None, with_lse=True):
+def _bwd(q, k, v, do, scale=None, with_lse=True, deterministic=False):
     from paper_2112_05682_b200 import api
     qd, kd, vd, dod = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v, do))
     out, lse = api.mea_attention_fwd(qd, kd, vd, scale=scale, want_lse=True)
-    dq, dk, dv = api.mea_attention_bwd(qd, kd, vd, out, dod, lse=lse if with_lse else None, scale=scale)
+    fn = api.mea_attention_bwd_deterministic if deterministic else api.mea_attention_bwd
+    dq, dk, dv = fn(qd, kd, vd, out, dod, lse=lse if with_lse else None, scale=scale)
     torch.cuda.synchronize()
     return [t.double().cpu().numpy() for t in (dq, dk, dv)]
 
 
+@pytest.mark.parametrize("deterministic", [False, True])
 @pytest.mark.parametrize("B,n_q,n_k,H", [(1, 128, 128, 1), (1, 17, 129, 2), (2, 300, 257, 2), (1, 1000, 700, 1),
                                          (1, 129, 1, 1), (1, 256, 1030, 3)])
-def test_bf16_backward_matches_oracle(B, n_q, n_k, H):
+def test_bf16_backward_matches_oracle(B, n_q, n_k, H, deterministic):
     d = 64
     q, k, v, do = Hh.host_inputs(B, n_q, n_k, H, d, seed=21, with_dout=True)
     refs = O.mha_backward(q, k, v, do, 1 / math.sqrt(d))
-    for got, ref, nm in zip(_bwd(q, k, v, do), refs, ("dq", "dk", "dv")):
+    for got, ref, nm in zip(_bwd(q, k, v, do, deterministic=deterministic), refs, ("dq", "dk", "dv")):
         Hh.assert_close_bf16(got, ref, abs_tol=Hh.TOL_BF16_GRAD, rel_tol=Hh.REL_NORM_GRAD, what=nm)
+
+
+def test_deterministic_backward_is_bitwise_reproducible():
+    q, k, v, do = Hh.host_inputs(1, 1000, 1500, 2, 64, seed=24, with_dout=True)
+    a = _bwd(q, k, v, do, deterministic=True, with_lse=False)
+    b = _bwd(q, k, v, do, deterministic=True, with_lse=False)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    from paper_2112_05682_b200 import api
+    small = api.mea_attention_bwd_deterministic_workspace_size(1, 16, 16384, 16384, 64, api.MEA_BF16)
+    fused = api.mea_attention_bwd_workspace_size(1, 16, 16384, 16384, 64, api.MEA_BF16)
+    assert small == 2 * 16 * 16384 * 4 and fused > 32 * small
 
 
 def test_bf16_backward_ones_dout_and_recomputed_lse():
