@@ -80,7 +80,11 @@ MEA_API const char* mea_last_error_detail(void);
  *     (v*, s*, m*), zero workspace. k_chunk in (0, n_k) selects the paper's key-chunk
  *     summaries: each chunk's (m*, s*, v*) goes to the workspace
  *     and a merge pass combines them (bf16 path; rounded up to a multiple of 128
- *     keys). q_chunk is a scheduling hint only (results do not depend on it).
+ *     keys). With a key split, q_chunk > 0 processes the query rows in chunks of
+ *     q_chunk rows (rounded up to 256), one after another, as Figure 1's outer map over
+ *     query chunks does, so only one chunk's summaries are alive:
+ *     workspace = splits * B * H * min(n_q, q_chunk') * (d + 2) * 4 bytes. Without a key
+ *     split q_chunk has no effect. Results do not depend on q_chunk.
  *   in_dtype MEA_BF16 requires d == 64 and out_dtype in {BF16, F32};
  *   in_dtype MEA_F32 requires d <= 128, out_dtype F32 and k_chunk == 0.
  */
@@ -90,7 +94,7 @@ MEA_API mea_status_t mea_attention_fwd(const void* q, const void* k, const void*
                                float* lse, int64_t q_chunk, int64_t k_chunk,
                                void* workspace, size_t workspace_bytes, void* stream);
 
-/* Workspace bytes mea_attention_fwd needs for these arguments (0 when k_chunk == 0). */
+/* Workspace bytes mea_attention_fwd needs for these arguments (0 unless 0 < k_chunk < n_k). */
 MEA_API mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k,
                                               int64_t d, mea_dtype_t in_dtype, int64_t q_chunk,
                                               int64_t k_chunk, size_t* bytes);

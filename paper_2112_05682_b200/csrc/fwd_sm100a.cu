@@ -137,7 +137,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int qblk = blockIdx.x % p.num_q_blocks;
   const int split = blockIdx.x / p.num_q_blocks;
   const int h = blockIdx.y, b = blockIdx.z;
-  const int q0 = qblk * kRowsPerCta;
+  const int q0 = p.q_begin + qblk * kRowsPerCta;
+  const int q_end = min(p.n_q, p.q_begin + p.q_count);
   const int n_tiles = (p.n_k + kTileN - 1) / kTileN;
   const int t_begin = split * p.tiles_per_split;
   const int t_end = min(n_tiles, t_begin + p.tiles_per_split);
@@ -401,10 +402,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t o[32];
     tmem_ld32_split<32>(lane_base + colO, o);
     tmem_ld_wait();
-    if (row < p.n_q) {
+    if (row < q_end) {
       const size_t bh = (size_t)b * p.H + h;
       if (p.num_splits > 1) {
-        const size_t prow = ((size_t)split * p.B * p.H + bh) * p.n_q + row;
+        const size_t prow = ((size_t)split * p.B * p.H + bh) * p.q_count + (row - p.q_begin);
         float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kHeadDim + half * 32);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Figure 1 lines 33-40 over the key-split partials of each query row:
 // M = max_c m_c; out = sum_c 2^(m_c - M) v*_c / sum_c 2^(m_c - M) s*_c. One warp per row.
 __global__ void merge_rows_kernel(const FwdParams p) {
-  const int64_t rows = (int64_t)p.B * p.H * p.n_q;
+  const int64_t rows = (int64_t)p.B * p.H * p.q_count;  // rows of this query window
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -466,7 +467,8 @@ __global__ void merge_rows_kernel(const FwdParams p) {
     a0 += w * o.x;
     a1 += w * o.y;
   }
-  const int64_t bh = r / p.n_q, row = r % p.n_q;
+  const int64_t bh = r / p.q_count, row = p.q_begin + r % p.q_count;
+  if (row >= p.n_q) return;
   const int64_t b = bh / p.H, h = bh % p.H;
   const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + 2 * lane;
   const float inv = 1.f / den;
@@ -475,7 +477,7 @@ __global__ void merge_rows_kernel(const FwdParams p) {
   } else {
     reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(p.out) + off)[0] = pack_bf16x2(a0 * inv, a1 * inv);
   }
-  if (p.lse && lane == 0) p.lse[r] = (M + __log2f(den)) * 0.6931471805599453f;
+  if (p.lse && lane == 0) p.lse[bh * p.n_q + row] = (M + __log2f(den)) * 0.6931471805599453f;
 }
 
 // ---------------------------------------------------------------------------- debug probe
@@ -564,7 +566,7 @@ cudaError_t launch_fwd_bf16(const FwdParams& p, const CUtensorMap& mq, const CUt
 }
 
 cudaError_t launch_merge_rows(const FwdParams& p, cudaStream_t s) {
-  const int64_t rows = (int64_t)p.B * p.H * p.n_q;
+  const int64_t rows = (int64_t)p.B * p.H * p.q_count;
   const int warps = 8;
   merge_rows_kernel<<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, s>>>(p);
   return cudaGetLastError();

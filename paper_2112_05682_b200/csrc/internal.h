@@ -18,11 +18,12 @@ struct FwdParams {
   void* out;               // [B,n_q,H,64], bf16 or f32 (unused in split mode)
   int out_f32;
   float* lse;              // [B,H,n_q] natural log, nullable
-  int num_q_blocks;        // ceil(n_q / 256)
+  int q_begin, q_count;    // query-row window of this launch (paper's query chunk)
+  int num_q_blocks;        // ceil(q_count / 256)
   int num_splits;          // key splits (1 = online over all keys)
   int tiles_per_split;     // key tiles of 128 per split
-  float* part_o;           // [splits][B*H][n_q][64] unnormalised v*   (split mode)
-  float* part_ml;          // [splits][B*H][n_q][2]  (m* in log2 units, s*) (split mode)
+  float* part_o;           // [splits][B*H][q_count][64] unnormalised v*   (split mode)
+  float* part_ml;          // [splits][B*H][q_count][2]  (m* in log2 units, s*) (split mode)
 };
 
 struct BwdParams {

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -113,20 +114,28 @@ namespace {
 
 struct FwdPlan {
   int splits = 1, tiles_per_split = 0;
+  int64_t q_window = 0;  // query rows per launch (split mode): the paper's query chunk
   size_t ws = 0;
 };
 
-FwdPlan plan_fwd(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t k_chunk) {
+// Key split (k_chunk < n_k): Figure 1's summaries of key chunks of k_chunk keys (rounded up to
+// whole 128-key tiles), merged per row afterwards. With q_chunk > 0 the query
+// rows are processed in windows of q_chunk rows (rounded up to the 256-row CTA), one after the
+// other, as Figure 1's outer map over query chunks does, so the summaries of
+// only one query chunk are alive at a time: workspace = splits * B * H * q_window * (d + 2) f32.
+FwdPlan plan_fwd(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t q_chunk, int64_t k_chunk) {
   FwdPlan pl;
   const int64_t n_tiles = (n_k + kTileN - 1) / kTileN;
   pl.tiles_per_split = (int)n_tiles;
+  pl.q_window = n_q;
   if (k_chunk > 0 && k_chunk < n_k) {
     const int64_t tps = (k_chunk + kTileN - 1) / kTileN;
     const int64_t splits = (n_tiles + tps - 1) / tps;
     if (splits > 1) {
       pl.splits = (int)splits;
       pl.tiles_per_split = (int)tps;
-      pl.ws = (size_t)splits * B * H * n_q * (kHeadDim + 2) * sizeof(float);
+      if (q_chunk > 0) pl.q_window = std::min(n_q, (q_chunk + kRowsPerCta - 1) / kRowsPerCta * kRowsPerCta);
+      pl.ws = (size_t)splits * B * H * pl.q_window * (kHeadDim + 2) * sizeof(float);
     }
   }
   return pl;
@@ -167,7 +176,7 @@ mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
   if (q_chunk < 0 || k_chunk < 0) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
   if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  *bytes = (in_dtype == MEA_BF16) ? plan_fwd(B, H, n_q, n_k, k_chunk).ws : 0;
+  *bytes = (in_dtype == MEA_BF16) ? plan_fwd(B, H, n_q, n_k, q_chunk, k_chunk).ws : 0;
   return MEA_OK;
 }
 
@@ -198,7 +207,7 @@ mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void
   }
 
   if (d != kHeadDim) return fail(MEA_ERR_UNSUPPORTED, "bf16 tensor-core path supports d == 64");
-  const FwdPlan pl = plan_fwd(B, H, n_q, n_k, k_chunk);
+  const FwdPlan pl = plan_fwd(B, H, n_q, n_k, q_chunk, k_chunk);
   if (pl.ws > 0) {
     if (workspace_bytes < pl.ws || !workspace) return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "key-chunk summaries need workspace");
     if (!aligned16(workspace)) return fail(MEA_ERR_MISALIGNED, "workspace must be 16-byte aligned");
@@ -227,21 +236,26 @@ mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void
   p.out = out;
   p.out_f32 = out_dtype == MEA_F32;
   p.lse = lse;
-  p.num_q_blocks = (int)nqb;
   p.num_splits = pl.splits;
   p.tiles_per_split = pl.tiles_per_split;
   if (pl.splits > 1) {
-    const size_t rows = (size_t)pl.splits * B * H * n_q;
+    const size_t rows = (size_t)pl.splits * B * H * pl.q_window;
     p.part_o = static_cast<float*>(workspace);
     p.part_ml = p.part_o + rows * kHeadDim;
   }
-  {
-    ProfScope ps("fwd_bf16", st);
-    if ((e = launch_fwd_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_bf16 launch");
-  }
-  if (pl.splits > 1) {
-    ProfScope ps("merge_rows", st);
-    if ((e = launch_merge_rows(p, st)) != cudaSuccess) return cuda_fail(e, "merge_rows launch");
+  // one window (all rows) unless the key-split schedule runs query chunk by query chunk
+  for (int64_t w0 = 0; w0 < n_q; w0 += pl.q_window) {
+    p.q_begin = (int)w0;
+    p.q_count = (int)std::min<int64_t>(pl.q_window, n_q - w0);
+    p.num_q_blocks = (p.q_count + kRowsPerCta - 1) / kRowsPerCta;
+    {
+      ProfScope ps("fwd_bf16", st);
+      if ((e = launch_fwd_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_bf16 launch");
+    }
+    if (pl.splits > 1) {
+      ProfScope ps("merge_rows", st);
+      if ((e = launch_merge_rows(p, st)) != cudaSuccess) return cuda_fail(e, "merge_rows launch");
+    }
   }
   return MEA_OK;
 }

@@ -53,7 +53,13 @@ def test_host_only_calls(lib):
     assert lib.mea_attention_fwd_workspace_size(1, 16, 16384, 16384, 64, 1, 0, 0, ctypes.byref(n)) == 0
     assert n.value == 0
     assert lib.mea_attention_fwd_workspace_size(1, 16, 16384, 16384, 64, 1, 1024, 4096, ctypes.byref(n)) == 0
-    assert n.value == 4 * 16 * 16384 * 66 * 4
+    assert n.value == 4 * 16 * 1024 * 66 * 4     # one query chunk of summaries alive
+    assert lib.mea_attention_fwd_workspace_size(1, 16, 16384, 16384, 64, 1, 0, 4096, ctypes.byref(n)) == 0
+    assert n.value == 4 * 16 * 16384 * 66 * 4    # q_chunk 0: all rows in one launch
+    assert lib.mea_attention_fwd_workspace_size(1, 16, 16384, 16384, 64, 1, 300, 4096, ctypes.byref(n)) == 0
+    assert n.value == 4 * 16 * 512 * 66 * 4      # q_chunk rounded up to the 256-row CTA
+    assert lib.mea_attention_fwd_workspace_size(1, 16, 16384, 16384, 64, 1, 1024, 16384, ctypes.byref(n)) == 0
+    assert n.value == 0                          # k_chunk >= n_k: no key split, q_chunk has no effect
     # single-query workspace is independent of n_k once the split count saturates
     a, b = ctypes.c_size_t(), ctypes.c_size_t()
     lib.mea_single_query_workspace_size(1, 1, 1 << 20, 64, 1, ctypes.byref(a))

@@ -56,6 +56,20 @@ def test_bf16_key_chunk_schedule_matches_default():
         assert np.abs(lb - ref_lse).max() < 1e-3
 
 
+def test_bf16_query_chunk_windows():
+    """Key split run query chunk by query chunk (Figure 1's outer map): every
+    window size, incl. ragged last windows and windows smaller than one CTA, gives the same rows."""
+    from paper_2112_05682_b200 import api
+    q, k, v = Hh.host_inputs(2, 1100, 700, 2, 64, seed=8)
+    ref, ref_lse = O.mha_forward(q, k, v, 0.125)
+    for qc in (1, 256, 300, 600, 1100, 5000):
+        ws = api.mea_attention_fwd_workspace_size(2, 2, 1100, 700, 64, api.MEA_BF16, qc, 256)
+        assert ws == 3 * 2 * 2 * min(1100, -(-qc // 256) * 256) * 66 * 4
+        b, lb = _run(q, k, v, scale=0.125, k_chunk=256, q_chunk=qc)
+        Hh.assert_close_bf16(b, ref)
+        assert np.abs(lb - ref_lse).max() < 1e-3
+
+
 def test_bf16_stress_monotone_and_huge_scores():
     """S1: scores grow along the keys (rescale on every tile); S2: scores near +-1000."""
     n, d = 700, 64
