@@ -32,7 +32,14 @@
 namespace mea {
 namespace {
 
-constexpr int kBStages = 2;                 // Q/dO ring
+#ifndef MEA_BSTAGES
+#define MEA_BSTAGES 3
+#endif
+#ifndef MEA_DQBUFS
+#define MEA_DQBUFS 1
+#endif
+constexpr int kBStages = MEA_BSTAGES;       // Q/dO ring
+constexpr int kDqBufs = MEA_DQBUFS;         // dQ staging buffers
 constexpr int kTile = 128;
 constexpr int kTileBytes = kTile * kHeadDim * 2;  // 16 KiB bf16 tile
 constexpr int kBThreads = 768;
@@ -60,7 +67,7 @@ struct BwdSmem {
   uint8_t q[kBStages][kTileBytes];
   uint8_t dout[kBStages][kTileBytes];
   uint8_t ds[2][kTileBytes];          // [query half][128 keys][64 queries] bf16, SW128
-  float dq_stage[2][2][kTile * 32];   // [buffer][column half][128 rows x 32 f32], SW128
+  float dq_stage[kDqBufs][2][kTile * 32];  // [buffer][column half][128 rows x 32 f32], SW128
   float lse2[kBStages][kTile];
   float delta[kBStages][kTile];
   uint64_t kv_full, qdo_full[kBStages], qdo_empty[kBStages];
@@ -315,10 +322,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const int rq = quarter * 32 + lane;  // query row within the tile (TMEM lane)
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     for (int i = 0; i < NQ; ++i) {
-      const int buf = i & 1;
+      const int buf = i % kDqBufs;
       mbar_wait(&sm.dq_full, i & 1);
-      // the TMA reduce that last read this staging buffer (tile i-2) must be done reading
-      if (warp == 20 && lane == 0) bulk_wait_group_read<1>();
+      // the TMA reduce that last read this staging buffer (tile i - kDqBufs) must be done reading
+      if (warp == 20 && lane == 0) bulk_wait_group_read<kDqBufs - 1>();
       named_bar_sync(kBarDq, 128);
       tc_fence_after();
 #pragma unroll
