@@ -44,7 +44,10 @@
 namespace mea {
 namespace {
 
-constexpr int kStages = 4;
+#ifndef MEA_FSTAGES
+#define MEA_FSTAGES 4
+#endif
+constexpr int kStages = MEA_FSTAGES;  // K/V ring depth
 constexpr int kTileBytes = kTileN * kHeadDim * 2;  // 16 KiB: 128 rows x 128 B
 constexpr int kThreads = 640;  // 4 producer/MMA/alloc warps + 4 softmax warpgroups
 // setmaxnreg.inc can only redistribute the registers the CTA was launched with (640 x 96:
@@ -103,13 +106,11 @@ __device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t p_tmem, const
   }
 }
 
-__device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(a, fmaxf(b, c)); }
-
 // 2^x on the FMA/ALU pipes for a pair: x = r + f, r = round(x), f in [-1/2, 1/2]; 2^f by a
 // degree-3 minimax polynomial (max relative error 7.5e-5, below the bf16 rounding of P); 2^r
 // added to the exponent field with one IMAD. x is clamped at -126. Used for the pairs selected
-// by kPolyEvery (0 = all exponentials on MUFU). Measured at configs[2]: every 16th pair 1.24 ms,
-// every 8th 1.24, every 4th 1.27, none 1.28 (MUFU alone is 16 exp/clk/SM, the polynomial 13).
+// by MEA_POLY_MASK (0 = all exponentials on MUFU). MUFU alone is 16 exp/clk/SM, the polynomial
+// 13; pairs {9, 25} on the polynomial beat all-MUFU by ~7 %.
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   x.x = fmaxf(x.x, -126.f);
   x.y = fmaxf(x.y, -126.f);
@@ -122,11 +123,14 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   return make_float2(__uint_as_float(__float_as_uint(t.x) * 8388608u + __float_as_uint(q.x)),
                      __uint_as_float(__float_as_uint(t.y) * 8388608u + __float_as_uint(q.y)));
 }
-#ifndef MEA_POLY_EVERY
-#define MEA_POLY_EVERY 16
+// Which of the 32 exponential pairs of a half row go to the FMA pipe (bit i = pair i). Measured
+// at configs[2] with interleaved timing (tools/fwd_experiments.py): pairs {9, 25} 6 % faster than
+// {15, 31}; {7, 23} and every 8th pair no better than {15, 31}; every 24th slower. The placement
+// matters because it decides what the scheduler can overlap with the MUFU queue.
+#ifndef MEA_POLY_MASK
+#define MEA_POLY_MASK 0x02000200u
 #endif
-constexpr int kPolyEvery = MEA_POLY_EVERY;  // every kPolyEvery-th exponential pair on the FMA pipe
-__device__ __forceinline__ constexpr bool poly_pair(int i) { return kPolyEvery > 0 && (i % kPolyEvery) == kPolyEvery - 1; }
+__device__ __forceinline__ constexpr bool poly_pair(int i) { return ((MEA_POLY_MASK) >> i) & 1u; }
 
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_bf16_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,

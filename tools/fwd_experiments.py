@@ -1,4 +1,9 @@
-"""Time forward-kernel variants (built with -D flags into separate .so files) at cfg3."""
+"""Time forward-kernel variants (separate .so builds, tools/build_variant.sh) at configs[2]
+(B=1, H=16, n=16384, d=64 bf16). Calls are interleaved variant by variant (A B C A B C ...) so
+every variant sees the same clock / power state; outputs are compared with the first variant's.
+
+    ITERS=60 python tools/fwd_experiments.py exp_so/exp_a.so exp_so/exp_b.so [...]
+"""
 import ctypes, os, sys, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -6,22 +11,38 @@ from paper_2112_05682_b200 import _lib, api
 
 libs = sys.argv[1:]
 dev = torch.device("cuda", 0)
-for H in (16, 1):
-    q = torch.empty((1, 16384, H, 64), dtype=torch.bfloat16, device=dev)
-    k, v = torch.empty_like(q), torch.empty_like(q)
-    for t, tid in ((q, 1), (k, 2), (v, 3)):
-        api.mea_fill_synthetic(t, 0, tid)
-    out = torch.empty_like(q)
+H = 16
+q = torch.empty((1, 16384, H, 64), dtype=torch.bfloat16, device=dev)
+k, v = torch.empty_like(q), torch.empty_like(q)
+for t, tid in ((q, 1), (k, 2), (v, 3)):
+    api.mea_fill_synthetic(t, 0, tid)
+outs = {p: torch.empty_like(q) for p in libs}
+fns = {}
+for path in libs:
+    lib = ctypes.CDLL(path)
+    for name, (r, args) in _lib.SIGNATURES.items():
+        f = getattr(lib, name); f.restype = r; f.argtypes = args
+    fns[path] = lib
+
+
+def call(path):
+    _lib._lib = fns[path]
+    api.mea_attention_fwd(q, k, v, out=outs[path])
+
+
+res = {p: [] for p in libs}
+ITERS = int(os.environ.get("ITERS", "40"))
+for i in range(ITERS + 2):
     for path in libs:
-        lib = ctypes.CDLL(path)
-        for name, (res, args) in _lib.SIGNATURES.items():
-            f = getattr(lib, name); f.restype = res; f.argtypes = args
-        _lib._lib = lib
-        ts = []
-        for i in range(12):
-            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-            e0.record(); api.mea_attention_fwd(q, k, v, out=out); e1.record()
-            torch.cuda.synchronize()
-            if i >= 2: ts.append(e0.elapsed_time(e1))
-        ms = statistics.median(ts)
-        print(f"H={H:2d} {os.path.basename(path):30s} {ms:8.3f} ms  {4*16384*16384*64*H/ms/1e9:8.1f} TFLOP/s")
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record(); call(path); e1.record()
+        torch.cuda.synchronize()
+        if i >= 2: res[path].append(e0.elapsed_time(e1))
+ref = outs[libs[0]].float()
+for path in libs[1:]:
+    print(f"{os.path.basename(path)}: max|diff| vs first {(outs[path].float() - ref).abs().max().item():.3e}")
+base = statistics.median(res[libs[0]])
+for path, ts in res.items():
+    ms = statistics.median(ts)
+    print(f"{os.path.basename(path):24s} fwd {ms:.3f} ms (min {min(ts):.3f}, {100 * (ms / base - 1):+.1f}%)  "
+          f"{4*16384*16384*64*H/ms/1e9:.1f} TFLOP/s")
