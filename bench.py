@@ -356,6 +356,25 @@ def main():
             "keys_total": n_local * world, "heads": Hq, "ms": sh_ms, "gbs_total": gb / (sh_ms * 1e-3),
             "collective": "one all_gather of (m*, s*, v*) per (b,h), NCCL"}
         del sq_k, sq_v
+        # key-range sharded self-attention (long context beyond one GPU): every rank holds all
+        # query rows and n/world of the keys of configs[2]'s shape; row triples, one all-gather,
+        # merge on every rank (strong scaling in the keys)
+        lo, hi = mdist.shard_range(n, world, rank)
+        q_all = torch.empty_like(q)                 # the same query rows on every rank (batch element 0)
+        api.mea_fill_synthetic(q_all, a.seed, gen.TENSOR_Q)
+        k_loc = torch.empty((Bl, hi - lo, Hl, D), dtype=torch.bfloat16, device=dev)
+        v_loc = torch.empty_like(k_loc)             # this rank's key range of batch element 0
+        api.mea_fill_synthetic(k_loc, a.seed, gen.TENSOR_K, offset=lo * Hl * D)
+        api.mea_fill_synthetic(v_loc, a.seed, gen.TENSOR_V, offset=lo * Hl * D)
+        run = lambda: mdist.sharded_self_attention(q_all, k_loc, v_loc)
+        t = timed(run, max(3, a.steps // 3), 1)
+        sa_ms = max_over_ranks(statistics.mean(t))
+        extras["self_attention_key_sharded"] = {
+            "n": n, "heads": Hl, "keys_per_rank": hi - lo, "ms": sa_ms,
+            "tflops_total": flop_fwd / (sa_ms * 1e-3) / 1e12,
+            "exchange_bytes_per_rank": Bl * n * Hl * (D + 2) * 4,
+            "collective": "one all_gather of the per-row (m*, s*, v*) triples, NCCL; merge on every rank"}
+        del q_all, k_loc, v_loc
     # ---------------- scratch bytes vs the paper's accounting (standard attention: n^2*4 B/head)
     scratch = {"fwd_workspace_bytes": 0, "fwd_lse_residual_bytes": lse.numel() * 4,
                "bwd_workspace_bytes": bwd_ws.numel() if bwd_ws is not None else None,

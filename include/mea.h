@@ -124,9 +124,24 @@ MEA_API mea_status_t mea_single_query_workspace_size(int64_t B, int64_t H, int64
  *   vstar [B*H*d]: v* = sum_j v_j e^{s_j - m}   (all float32).
  * n_k == 0 is allowed here and yields the empty triple (-inf, 0, 0).
  * mea_merge_partials combines P stacked triples m [P,B*H], s [P,B*H], vstar [P,B*H,d]
- * into out [B,H,d] (out_dtype). Empty triples contribute nothing; all-empty rows are
+ * into out [B,H,d] (out_dtype); for self-attention rows pass H := n_q * H (out [B,n_q,H,d]). Empty triples contribute nothing; all-empty rows are
  * MEA_ERR_EMPTY_KEYS only if detectable on the host (P == 0), else they yield NaN.
  */
+/*
+ * Self-attention over one key range, as a stream state per query row (multi-GPU building block:
+ * key-range sharding of long-context self-attention; the merge is
+ * mea_merge_partials with H := n_q * H).
+ *   q [B,n_q,H,d], k,v [B,n_k,H,d] bf16, d == 64 (MEA_ERR_UNSUPPORTED otherwise).
+ *   m [B,n_q,H], s [B,n_q,H], vstar [B,n_q,H,d] float32 outputs, same meaning as for
+ *   mea_single_query_partial (m in natural-log units of the scaled score).
+ *   n_k == 0 yields the empty triple (-inf, 0, 0) for every row; n_q == 0 is a no-op.
+ * No workspace. Errors as mea_attention_fwd.
+ */
+MEA_API mea_status_t mea_attention_partial_fwd(const void* q, const void* k, const void* v, float* m,
+                                       float* s, float* vstar, int64_t B, int64_t H, int64_t n_q,
+                                       int64_t n_k, int64_t d, mea_dtype_t in_dtype, float scale,
+                                       void* stream);
+
 MEA_API mea_status_t mea_single_query_partial(const void* q, const void* k, const void* v, float* m,
                                       float* s, float* vstar, int64_t B, int64_t H, int64_t n_k,
                                       int64_t d, mea_dtype_t in_dtype, float scale,

@@ -107,6 +107,24 @@ def mea_attention_fwd(q, k, v, scale=None, out=None, out_dtype=None, lse=None, w
     return (out, lse) if (want_lse or lse is not None) else out
 
 
+def mea_attention_partial_fwd(q, k, v, scale=None):
+    """Stream state (m*, s*, v*) of every query row over this call's keys (one key range of a
+    sharded self-attention). Returns m [B,n_q,H], s [B,n_q,H] and vstar [B,n_q,H,d], float32,
+    m in natural-log units; merge ranges with mea_merge_partials(..., B, n_q * H)."""
+    _cuda_contig(q, k, v)
+    B, n_q, H, d = q.shape
+    n_k = k.shape[1]
+    if k.shape != (B, n_k, H, d) or v.shape != k.shape:
+        raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    m = torch.empty((B, n_q, H), dtype=torch.float32, device=q.device)
+    s = torch.empty((B, n_q, H), dtype=torch.float32, device=q.device)
+    vs = torch.empty((B, n_q, H, d), dtype=torch.float32, device=q.device)
+    _check(_lib.load().mea_attention_partial_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(m), _ptr(s), _ptr(vs), B, H, n_q,
+                                                 n_k, d, _dtype(q), scale, _stream(q.device)))
+    return m, s, vs
+
+
 # ------------------------------------------------------------------------ single query
 def mea_single_query_workspace_size(B, H, n_k, d, in_dtype):
     n = ctypes.c_size_t(0)

@@ -408,7 +408,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_ld_wait();
     if (row < q_end) {
       const size_t bh = (size_t)b * p.H + h;
-      if (p.num_splits > 1) {
+      if (p.tri_v) {
+        // this call's (m*, s*, v*) per row, for a merge across key ranges
+        const size_t idx = ((size_t)b * p.n_q + row) * p.H + h;
+        float4* dst = reinterpret_cast<float4*>(p.tri_v + idx * kHeadDim + half * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
+                               __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
+        if (half == 0) {
+          p.tri_m[idx] = m_ref * 0.6931471805599453f;
+          p.tri_s[idx] = lrow;
+        }
+      } else if (p.num_splits > 1) {
         const size_t prow = ((size_t)split * p.B * p.H + bh) * p.q_count + (row - p.q_begin);
         float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kHeadDim + half * 32);
 #pragma unroll
@@ -566,6 +578,22 @@ cudaError_t launch_fwd_bf16(const FwdParams& p, const CUtensorMap& mq, const CUt
   if (attr != cudaSuccess) return attr;
   dim3 grid(p.num_q_blocks * p.num_splits, p.H, p.B);
   fwd_bf16_kernel<<<grid, kThreads, kFwdSmemBytes, s>>>(mq, mk, mv, p);
+  return cudaGetLastError();
+}
+
+// The triple of an empty key range: (m*, s*, v*) = (-inf, 0, 0) (PAPER.md:89's initial state).
+__global__ void empty_triples_kernel(float* m, float* s, float* vstar, int64_t rows, int d) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < rows) {
+    m[i] = -INFINITY;
+    s[i] = 0.f;
+  }
+  if (i < rows * d) vstar[i] = 0.f;
+}
+
+cudaError_t launch_empty_triples(float* m, float* s, float* vstar, int64_t rows, int d, cudaStream_t st) {
+  const int64_t n = rows * d;
+  empty_triples_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(m, s, vstar, rows, d);
   return cudaGetLastError();
 }
 

@@ -24,6 +24,9 @@ struct FwdParams {
   int tiles_per_split;     // key tiles of 128 per split
   float* part_o;           // [splits][B*H][q_count][64] unnormalised v*   (split mode)
   float* part_ml;          // [splits][B*H][q_count][2]  (m* in log2 units, s*) (split mode)
+  float* tri_m;            // partial mode (mea_attention_partial_fwd): [B,n_q,H] m* (natural log)
+  float* tri_s;            //   [B,n_q,H] s*
+  float* tri_v;            //   [B,n_q,H,64] v* (unnormalised)
 };
 
 struct BwdParams {
@@ -47,6 +50,7 @@ cudaError_t make_bnhd_map(CUtensorMap* map, const void* base, CUtensorMapDataTyp
 cudaError_t launch_fwd_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                             const CUtensorMap& mv, cudaStream_t s);
 cudaError_t launch_merge_rows(const FwdParams& p, cudaStream_t s);
+cudaError_t launch_empty_triples(float* m, float* s, float* vstar, int64_t rows, int d, cudaStream_t st);
 cudaError_t launch_fwd_f32(const float* q, const float* k, const float* v, float* out, float* lse, int B,
                            int H, int n_q, int n_k, int d, float scale, cudaStream_t s);
 
@@ -57,7 +61,7 @@ cudaError_t launch_sq_partial(const void* q, const void* k, const void* v, int b
 // mode 0: write out (dtype) ; mode 1: write triple (m natural, s, v*)
 cudaError_t launch_sq_merge(const float* ws, int splits, int BH, int d, int mode, void* out, int out_f32,
                             float* m, float* sum, float* vstar, cudaStream_t s);
-cudaError_t launch_merge_partials(const float* m, const float* s, const float* vstar, int P, int BH, int d,
+cudaError_t launch_merge_partials(const float* m, const float* s, const float* vstar, int P, int64_t rows, int d,
                                   void* out, int out_f32, cudaStream_t st);
 
 // backward

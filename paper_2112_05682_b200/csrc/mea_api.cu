@@ -260,6 +260,56 @@ mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void
   return MEA_OK;
 }
 
+// ------------------------------------------------------------------ partial self-attention
+mea_status_t mea_attention_partial_fwd(const void* q, const void* k, const void* v, float* m, float* s, float* vstar,
+                                       int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                                       mea_dtype_t in_dtype, float scale, void* stream) {
+  if (mea_status_t r = check_common(B, H, n_q, n_k, d, scale)) return r;
+  if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  if (in_dtype != MEA_BF16 || d != kHeadDim) return fail(MEA_ERR_UNSUPPORTED, "partial forward: bf16, d == 64");
+  if (n_q == 0) return MEA_OK;
+  if (!m || !s || !vstar || !q) return fail(MEA_ERR_INVALID_VALUE, "NULL pointer");
+  if (!aligned16(q) || !aligned16(vstar) || (reinterpret_cast<uintptr_t>(m) & 3u) ||
+      (reinterpret_cast<uintptr_t>(s) & 3u))
+    return fail(MEA_ERR_MISALIGNED, "q, vstar must be 16-byte aligned; m, s 4-byte");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (n_k == 0) {  // empty key range: the initial stream state
+    ProfScope ps("empty_triples", st);
+    e = launch_empty_triples(m, s, vstar, B * n_q * H, (int)d, st);
+    return e == cudaSuccess ? MEA_OK : cuda_fail(e, "empty_triples launch");
+  }
+  if (!k || !v) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
+  if (!aligned16(k) || !aligned16(v)) return fail(MEA_ERR_MISALIGNED, "k, v must be 16-byte aligned");
+  CUtensorMap mq, mk, mv;
+  const char* why = "";
+  if ((e = make_bnhd_map(&mq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_q, H, d, 64, kTileM,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+      (e = make_bnhd_map(&mk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+      (e = make_bnhd_map(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess)
+    return cuda_fail(e, why);
+  FwdParams p{};
+  p.B = (int)B;
+  p.H = (int)H;
+  p.n_q = (int)n_q;
+  p.n_k = (int)n_k;
+  p.scale = scale;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.num_splits = 1;
+  p.tiles_per_split = (int)((n_k + kTileN - 1) / kTileN);
+  p.q_begin = 0;
+  p.q_count = (int)n_q;
+  p.num_q_blocks = (int)((n_q + kRowsPerCta - 1) / kRowsPerCta);
+  p.tri_m = m;
+  p.tri_s = s;
+  p.tri_v = vstar;
+  ProfScope ps("fwd_bf16", st);
+  if ((e = launch_fwd_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_bf16 launch");
+  return MEA_OK;
+}
+
 // ------------------------------------------------------------------ single query
 mea_status_t mea_single_query_workspace_size(int64_t B, int64_t H, int64_t n_k, int64_t d, mea_dtype_t in_dtype,
                                              size_t* bytes) {
@@ -337,11 +387,12 @@ mea_status_t mea_merge_partials(const float* m, const float* s, const float* vst
   if (P < 0 || B < 1 || H < 1 || d < 1) return fail(MEA_ERR_INVALID_VALUE, "bad sizes");
   if (P == 0) return fail(MEA_ERR_EMPTY_KEYS, "no partials to merge");
   if (d > 128) return fail(MEA_ERR_UNSUPPORTED, "d <= 128");
-  if (B * H > 65535) return fail(MEA_ERR_UNSUPPORTED, "B*H > 65535");
+  if (P > kMaxInt) return fail(MEA_ERR_UNSUPPORTED, "P too large");
   if (!valid_dtype(out_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
   if (!m || !s || !vstar || !out) return fail(MEA_ERR_INVALID_VALUE, "NULL pointer");
+  if ((B * H + 7) / 8 > kMaxInt) return fail(MEA_ERR_UNSUPPORTED, "too many rows");
   ProfScope ps("merge_partials", static_cast<cudaStream_t>(stream));
-  cudaError_t e = launch_merge_partials(m, s, vstar, (int)P, (int)(B * H), (int)d, out, out_dtype == MEA_F32,
+  cudaError_t e = launch_merge_partials(m, s, vstar, (int)P, B * H, (int)d, out, out_dtype == MEA_F32,
                                         static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? MEA_OK : cuda_fail(e, "merge_partials launch");
 }

@@ -311,23 +311,34 @@ __global__ void __launch_bounds__(kMergeWarps * 32) sq_merge_kernel(const float*
   }
 }
 
-// Cross-rank merge: P triples with natural-log m.
+// Cross-rank merge: P triples with natural-log m. One warp per row (a (b,h)
+// of a single query, or a (b, query, h) row of self-attention), lanes over the d features.
 __global__ void merge_partials_kernel(const float* __restrict__ m, const float* __restrict__ s,
-                                      const float* __restrict__ vstar, int P, int BH, int d, void* out, int out_f32) {
-  const int bh = blockIdx.x, f = threadIdx.x;
-  if (f >= d) return;
+                                      const float* __restrict__ vstar, int P, int64_t rows, int d, void* out,
+                                      int out_f32) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
   float M = -INFINITY;
-  for (int r = 0; r < P; ++r) M = fmaxf(M, m[(size_t)r * BH + bh]);
-  float L = 0.f, A = 0.f;
-  for (int r = 0; r < P; ++r) {
-    const float mr = m[(size_t)r * BH + bh];
-    const float w = (mr == -INFINITY) ? 0.f : expf(mr - M);
-    L += w * s[(size_t)r * BH + bh];
-    A += w * vstar[((size_t)r * BH + bh) * d + f];
+  for (int i = 0; i < P; ++i) M = fmaxf(M, m[(size_t)i * rows + r]);
+  float L = 0.f, A[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < P; ++i) {
+    const float mi = m[(size_t)i * rows + r];
+    const float w = (mi == -INFINITY) ? 0.f : expf(mi - M);
+    L += w * s[(size_t)i * rows + r];
+    const float* vi = vstar + ((size_t)i * rows + r) * d;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (lane + 32 * j < d) A[j] += w * vi[lane + 32 * j];
   }
-  const float res = A / L;
-  if (out_f32) static_cast<float*>(out)[(size_t)bh * d + f] = res;
-  else static_cast<__nv_bfloat16*>(out)[(size_t)bh * d + f] = __float2bfloat16_rn(res);
+  const float inv = 1.f / L;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int f = lane + 32 * j;
+    if (f >= d) break;
+    if (out_f32) static_cast<float*>(out)[(size_t)r * d + f] = A[j] * inv;
+    else static_cast<__nv_bfloat16*>(out)[(size_t)r * d + f] = __float2bfloat16_rn(A[j] * inv);
+  }
 }
 
 }  // namespace
@@ -375,9 +386,9 @@ cudaError_t launch_sq_merge(const float* ws, int splits, int BH, int d, int mode
   return cudaLaunchKernelEx(&cfg, sq_merge_kernel, ws, splits, d, mode, out, out_f32, m, sum, vstar);
 }
 
-cudaError_t launch_merge_partials(const float* m, const float* s, const float* vstar, int P, int BH, int d, void* out,
-                                  int out_f32, cudaStream_t st) {
-  merge_partials_kernel<<<BH, 128, 0, st>>>(m, s, vstar, P, BH, d, out, out_f32);
+cudaError_t launch_merge_partials(const float* m, const float* s, const float* vstar, int P, int64_t rows, int d,
+                                  void* out, int out_f32, cudaStream_t st) {
+  merge_partials_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(m, s, vstar, P, rows, d, out, out_f32);
   return cudaGetLastError();
 }
 

@@ -11,6 +11,11 @@ Two ways the hot path shards:
   and every rank merges them with Figure 1's global-max rescale in
   ``mea_merge_partials``.
 
+* Long-context self-attention beyond one GPU: the keys are split into
+  ranges; each rank computes the triple of every query row over its range with
+  ``mea_attention_partial_fwd``, one all-gather exchanges them and every rank merges
+  (``sharded_self_attention``).
+
 The compute steps default to libmea.so; the exchange logic is covered on CPU (gloo,
 world size 2) in tests/test_dist.py by passing the oracle's partial/merge instead.
 """
@@ -68,3 +73,22 @@ def sharded_single_query(q, k_local, v_local, scale=None, out_dtype=torch.bfloat
     m, s, vs = partial_fn(q, k_local, v_local, scale)
     M, S, V = gather_triples(m, s, vs, group)
     return merge_fn(M, S, V, B, H, out_dtype)
+
+
+def sharded_self_attention(q, k_local, v_local, scale=None, out_dtype=torch.bfloat16, group=None,
+                           partial_fn=None, merge_fn=None):
+    """Self-attention with the keys sharded over the ranks of `group`.
+
+    q [B, n_q, H, d] (replicated); k_local, v_local [B, n_k_local, H, d] (this rank's key range,
+    may be empty). Every query row's triple over the local keys is exchanged in
+    one all-gather of B*n_q*H*(d+2) floats per rank and merged with the global-max rescale
+    (PAPER.md:140-147). Returns out [B, n_q, H, d] on every rank.
+    """
+    if partial_fn is None or merge_fn is None:
+        from . import api
+        partial_fn = partial_fn or (lambda q_, k_, v_, sc: api.mea_attention_partial_fwd(q_, k_, v_, scale=sc))
+        merge_fn = merge_fn or (lambda m_, s_, v_, B_, R_, od: api.mea_merge_partials(m_, s_, v_, B_, R_, od))
+    B, n_q, H, d = q.shape
+    m, s, vs = partial_fn(q, k_local, v_local, scale)
+    M, S, V = gather_triples(m.reshape(-1), s.reshape(-1), vs.reshape(-1, d), group)
+    return merge_fn(M, S, V, B, n_q * H, out_dtype).reshape(B, n_q, H, d)

@@ -84,3 +84,51 @@ def test_key_sharded_single_query_gloo_world2(n_k):
             ref = O.naive(q[b, h][None].numpy(), k[b, :, h].numpy(), v[b, :, h].numpy(), scale)[0][0]
             for r in range(world):    # every rank holds the merged result
                 np.testing.assert_allclose(ret[r][b, h], ref, atol=1e-12)
+
+
+def _oracle_partial_rows(q, k, v, scale):
+    """Per query row triple over these keys (O5), laid out like mea_attention_partial_fwd."""
+    import oracle as O
+    B, n_q, H, d = q.shape
+    m = np.empty((B, n_q, H)); s = np.empty((B, n_q, H)); vs = np.empty((B, n_q, H, d))
+    for b in range(B):
+        for h in range(H):
+            mm, ss, vv = O.partial_triple(q[b, :, h].numpy(), k[b, :, h].numpy(), v[b, :, h].numpy(), scale)
+            m[b, :, h], s[b, :, h], vs[b, :, h] = mm, ss, vv
+    return torch.from_numpy(m), torch.from_numpy(s), torch.from_numpy(vs)
+
+
+def _oracle_merge_rows(m, s, v, B, R, out_dtype):
+    import oracle as O
+    return torch.from_numpy(O.merge(m.numpy(), s.numpy(), v.numpy())).reshape(B, R, -1)
+
+
+def _worker_sa(rank, world, port, q, k, v, scale, ret):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = D.shard_range(k.shape[1], world, rank)
+    out = D.sharded_self_attention(q, k[:, lo:hi], v[:, lo:hi], scale=scale, out_dtype=torch.float64,
+                                   partial_fn=_oracle_partial_rows, merge_fn=_oracle_merge_rows)
+    ret[rank] = out.numpy()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_k", [1, 9, 200])
+def test_key_sharded_self_attention_gloo_world2(n_k):
+    """Long-context self-attention by key range: per-rank row triples, one
+    all-gather, merge == the unsharded definition (n_k = 1 leaves rank 1 with no keys)."""
+    import oracle as O
+    B, n_q, H, d, world = 2, 7, 3, 8, 2
+    g = torch.Generator().manual_seed(100 + n_k)
+    q = torch.randn(B, n_q, H, d, generator=g, dtype=torch.float64)
+    k = torch.randn(B, n_k, H, d, generator=g, dtype=torch.float64)
+    v = torch.randn(B, n_k, H, d, generator=g, dtype=torch.float64)
+    scale = 1 / math.sqrt(d)
+    ret = mp.Manager().dict()
+    mp.spawn(_worker_sa, args=(world, _free_port(), q, k, v, scale, ret), nprocs=world, join=True)
+    ref, _ = O.mha_forward(q.numpy(), k.numpy(), v.numpy(), scale)
+    for r in range(world):
+        np.testing.assert_allclose(ret[r], ref, atol=1e-12)
