@@ -38,6 +38,9 @@ namespace {
 #ifndef MEA_DQBUFS
 #define MEA_DQBUFS 1
 #endif
+#ifndef MEA_BPOLY_MASK
+#define MEA_BPOLY_MASK 0u
+#endif
 constexpr int kBStages = MEA_BSTAGES;       // Q/dO ring
 constexpr int kDqBufs = MEA_DQBUFS;         // dQ staging buffers
 constexpr int kTile = 128;
@@ -68,8 +71,11 @@ struct BwdSmem {
   uint8_t dout[kBStages][kTileBytes];
   uint8_t ds[2][kTileBytes];          // [query half][128 keys][64 queries] bf16, SW128
   float dq_stage[kDqBufs][2][kTile * 32];  // [buffer][column half][128 rows x 32 f32], SW128
-  float lse2[kBStages][kTile];
-  float delta[kBStages][kTile];
+  // K-extension of the score MMAs (one extra K = 16 step each): with A = [-1, -1, 0...] per key
+  // and B = [hi, lo, 0...] per query, ST' = K Q^T - lse/scale and dPT' = V dO^T - delta, so the
+  // softmax needs no per-query loads: PT = 2^(c ST'), dST = PT o dPT'.
+  uint8_t aug_c[kAugTileBytes];              // A: -1 in K columns 0, 1 for all 128 rows
+  uint8_t aug[kBStages][2 * kAugTileBytes];  // B: [lse tile][delta tile] of the query tile
   uint64_t kv_full, qdo_full[kBStages], qdo_empty[kBStages];
   uint64_t s_full, s_loaded, p_full, p_free, dq_full, dq_empty, dkv_done;
   uint32_t tmem_base;
@@ -127,6 +133,14 @@ __global__ void __launch_bounds__(kBThreads, 1)
     tma_prefetch_desc(&mdq);
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
+  // A side of the K-extension: row r = [-1, -1, 0 ... 0] (bf16), core matrix (r/8, 0) at
+  // (r/8)*256 + (r%8)*16, core matrix (r/8, 1) at +128 all zero
+  if (threadIdx.x < 256) {
+    const int r = threadIdx.x >> 1, kc = threadIdx.x & 1;
+    *reinterpret_cast<uint4*>(sm.aug_c + (r >> 3) * 256 + kc * 128 + (r & 7) * 16) =
+        make_uint4(kc == 0 ? 0xBF80BF80u : 0u, 0u, 0u, 0u);
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -147,11 +161,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
         const int st = i % kBStages, n = i / kBStages;
         if (i >= kBStages) mbar_wait(&sm.qdo_empty[st], (n - 1) & 1);
         if (elect_one()) {
-          mbar_arrive_expect_tx(&sm.qdo_full[st], 2 * kTileBytes + 2 * kTile * 4);
+          mbar_arrive_expect_tx(&sm.qdo_full[st], 2 * kTileBytes + 2 * kAugTileBytes);
           tma_load_4d(sm.q[st], &mq, &sm.qdo_full[st], 0, h, i * kTile, b, keep);
           tma_load_4d(sm.dout[st], &mdo, &sm.qdo_full[st], 0, h, i * kTile, b, keep);
-          bulk_load(sm.lse2[st], p.lse2 + bh * nq_pad + i * kTile, kTile * 4, &sm.qdo_full[st]);
-          bulk_load(sm.delta[st], p.delta + bh * nq_pad + i * kTile, kTile * 4, &sm.qdo_full[st]);
+          bulk_load(sm.aug[st], p.aug + (bh * NQ + i) * (2 * kAugTileBytes), 2 * kAugTileBytes, &sm.qdo_full[st]);
         }
         __syncwarp();
       }
@@ -167,12 +180,19 @@ __global__ void __launch_bounds__(kBThreads, 1)
       const uint64_t dSm = shfl0_u64(sdesc_sw128(smem_u32(sm.ds[0]), kTileBytes, 1024));
       constexpr uint64_t kStep = kTileBytes >> 4;
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
-      auto scores = [&](int st) {  // ST = K Q^T ; dPT = V dO^T
-        const uint64_t q = dQ0 + st * kStep, o = dO0 + st * kStep;
+      // K-extension operands: no-swizzle K-major, core matrices 8 rows x 16 B, K stride 128 B,
+      // 8-row stride 256 B
+      const uint64_t dC = shfl0_u64(sdesc_noswz(smem_u32(sm.aug_c), 128, 256));
+      const uint64_t dA0 = shfl0_u64(sdesc_noswz(smem_u32(sm.aug[0]), 128, 256));
+      constexpr uint64_t kAugStep = (2 * kAugTileBytes) >> 4, kAugHalf = kAugTileBytes >> 4;
+      auto scores = [&](int st) {  // ST' = K Q^T - lse/scale ; dPT' = V dO^T - delta
+        const uint64_t q = dQ0 + st * kStep, o = dO0 + st * kStep, a = dA0 + st * kAugStep;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) umma_ss(tm + kColST, dK + kk * 2, q + kk * 2, kIdSS, kk > 0);
+        umma_ss(tm + kColST, dC, a, kIdSS, 1u);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) umma_ss(tm + kColDPT, dV + kk * 2, o + kk * 2, kIdSS, kk > 0);
+        umma_ss(tm + kColDPT, dC, a + kAugHalf, kIdSS, 1u);
       };
       mbar_wait(&sm.kv_full, 0);
       mbar_wait(&sm.qdo_full[0], 0);
@@ -182,14 +202,24 @@ __global__ void __launch_bounds__(kBThreads, 1)
         umma_commit(&sm.s_full);
       }
       __syncwarp();
+#ifdef MEA_EXP_TIMING
+      unsigned long long* mdbg = reinterpret_cast<unsigned long long*>(p.dv) + 512;
+      const bool mprobe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0;
+#define MPROBE(k) if (mprobe && i >= 8 && i < 24) mdbg[(i - 8) * 8 + (k)] = clock64();
+#else
+#define MPROBE(k)
+#endif
       for (int i = 0; i < NQ; ++i) {
         const int st = i % kBStages;
         const bool more = i + 1 < NQ;
+        MPROBE(0)
         // the next tile's scores as soon as the softmax warps have read ST_i / dPT_i, so they
         // are computed while softmax i runs
         if (more) {
           mbar_wait(&sm.qdo_full[(i + 1) % kBStages], ((i + 1) / kBStages) & 1);
+          MPROBE(1)
           mbar_wait(&sm.s_loaded, i & 1);
+          MPROBE(2)
           tc_fence_after();
           if (elect_one()) {
             scores((i + 1) % kBStages);
@@ -198,6 +228,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
           __syncwarp();
         }
         mbar_wait(&sm.p_full, i & 1);
+        MPROBE(3)
         tc_fence_after();
         const uint64_t q = dQ0 + st * kStep, o = dO0 + st * kStep;
         if (elect_one()) {
@@ -211,6 +242,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
         }
         __syncwarp();
         if (i > 0) mbar_wait(&sm.dq_empty, (i - 1) & 1);  // dQ of tile i-1 drained from TMEM
+        MPROBE(4)
         tc_fence_after();
         if (elect_one()) {
           // dQ = dS K : K = 128 keys in steps of 16 (16 key rows = 2048 B in both operands)
@@ -256,19 +288,16 @@ __global__ void __launch_bounds__(kBThreads, 1)
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&sm.s_loaded);  // ST_i / dPT_i are in registers: the next scores may overwrite
-      const float* l2 = sm.lse2[st] + g * 32;
-      const float* dl = sm.delta[st] + g * 32;
       uint32_t pk[16], dk[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
         const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
-        const float2 lq = *reinterpret_cast<const float2*>(l2 + 2 * u);
-        const float2 de = *reinterpret_cast<const float2*>(dl + 2 * u);
-        const float2 x = __ffma2_rn(s2, c2, make_float2(-lq.x, -lq.y));  // s c - lse2
-        float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));        // P (lse2 = +inf pads -> 0)
+        const float2 x = __fmul2_rn(s2, c2);  // c (s - lse/scale) = s c - lse log2 e
+        // P (lse2 = +inf pads -> 0); the pairs in MEA_BPOLY_MASK on the FMA pipe unload MUFU
+        float2 pr = (((MEA_BPOLY_MASK) >> u) & 1u) ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
         if (!key_ok) pr = make_float2(0.f, 0.f);
-        const float2 ds = __fmul2_rn(pr, __fadd2_rn(d2, make_float2(-de.x, -de.y)));  // P (dP - delta)
+        const float2 ds = __fmul2_rn(pr, d2);  // P (dP - delta)
         pk[u] = pack_bf16x2(pr.x, pr.y);
         dk[u] = pack_bf16x2(ds.x, ds.y);
       }
@@ -364,11 +393,22 @@ __global__ void __launch_bounds__(kBThreads, 1)
 
 // delta_i = dO_i . O_i, lse2 = lse log2 e, both padded to a multiple of 128 rows
 // per (b,h) (pads: delta 0, lse2 +inf so padded query rows get P = 0); dq_acc = 0 when given.
-// 8 threads per row, 16-byte loads.
+// With aug (fused kernel): the B side of the score MMAs' K-extension, per (b,h, query tile) an
+// 8 KiB block [lse tile][delta tile], each 128 rows x 16 bf16 in no-swizzle K-major core matrices
+// (row r, K column k at (r/8)*256 + (k/8)*128 + (r%8)*16 + (k%8)*2): row = [hi, lo, 0 ...] with
+// hi + lo = lse/scale (resp. delta) to ~2^-16 relative; padded rows: lse/scale = +-inf (so that
+// c ST' = -inf, P = 0) and delta = 0. 8 threads per row, 16-byte loads.
+__device__ __forceinline__ uint32_t bf16_hi_lo(float x) {
+  const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+  const float rest = isinf(x) ? 0.f : x - __bfloat162float(hi);
+  const __nv_bfloat16 lo = __float2bfloat16_rn(rest);
+  return (uint32_t)__bfloat16_as_ushort(hi) | ((uint32_t)__bfloat16_as_ushort(lo) << 16);
+}
+
 __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ dout,
                                       const float* __restrict__ lse, float* __restrict__ delta,
-                                      float* __restrict__ lse2, float* __restrict__ dq_acc, int B, int H, int n_q,
-                                      int nq_pad) {
+                                      float* __restrict__ lse2, float* __restrict__ dq_acc, uint8_t* __restrict__ aug,
+                                      float scale, int B, int H, int n_q, int nq_pad) {
   const int64_t rows = (int64_t)B * H * nq_pad;
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
   const int part = threadIdx.x & 7;
@@ -396,9 +436,21 @@ __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ out, con
   acc += __shfl_xor_sync(0xffffffffu, acc, 1);
   acc += __shfl_xor_sync(0xffffffffu, acc, 2);
   acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  const float l = (q < n_q) ? lse[bh * n_q + q] : INFINITY;
   if (part == 0) {
     delta[r] = acc;
-    lse2[r] = (q < n_q) ? lse[bh * n_q + q] * 1.4426950408889634f : INFINITY;
+    lse2[r] = l * 1.4426950408889634f;
+  }
+  if (aug && part < 4) {  // parts 0,1: lse tile (K core 0, 1); parts 2,3: delta tile
+    const int tile = q / kTile, rr = q % kTile;
+    uint8_t* blk = aug + (bh * (nq_pad / kTile) + tile) * (2 * kAugTileBytes) + (part >> 1) * kAugTileBytes;
+    const int kc = part & 1;
+    uint32_t w0 = 0u;
+    if (kc == 0) {
+      const float x = (part < 2) ? ((q < n_q) ? l / scale : (scale > 0.f ? INFINITY : -INFINITY)) : acc;
+      w0 = bf16_hi_lo(x);
+    }
+    *reinterpret_cast<uint4*>(blk + (rr >> 3) * 256 + kc * 128 + (rr & 7) * 16) = make_uint4(w0, 0u, 0u, 0u);
   }
 }
 
@@ -413,12 +465,12 @@ __global__ void dq_convert_kernel(const float4* __restrict__ acc, uint2* __restr
 }  // namespace
 
 cudaError_t launch_bwd_preprocess(const void* out, const void* dout, const float* lse, float* delta, float* lse2,
-                                  float* dq_acc, int B, int H, int n_q, cudaStream_t s) {
+                                  float* dq_acc, uint8_t* aug, float scale, int B, int H, int n_q, cudaStream_t s) {
   const int nq_pad = (n_q + kTile - 1) / kTile * kTile;
   const int64_t threads = (int64_t)B * H * nq_pad * 8;
   bwd_preprocess_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), lse, delta, lse2, dq_acc, B,
-      H, n_q, nq_pad);
+      static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), lse, delta, lse2, dq_acc, aug,
+      scale, B, H, n_q, nq_pad);
   return cudaGetLastError();
 }
 

@@ -106,23 +106,6 @@ __device__ __forceinline__ void issue_pv(uint32_t d_tmem, uint32_t p_tmem, const
   }
 }
 
-// 2^x on the FMA/ALU pipes for a pair: x = r + f, r = round(x), f in [-1/2, 1/2]; 2^f by a
-// degree-3 minimax polynomial (max relative error 7.5e-5, below the bf16 rounding of P); 2^r
-// added to the exponent field with one IMAD. x is clamped at -126. Used for the pairs selected
-// by MEA_POLY_MASK (0 = all exponentials on MUFU). MUFU alone is 16 exp/clk/SM, the polynomial
-// 13; pairs {9, 25} on the polynomial beat all-MUFU by ~7 %.
-__device__ __forceinline__ float2 exp2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
-  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));  // 1.5 * 2^23: round-to-int
-  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
-  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
-  float2 q = __ffma2_rn(f, make_float2(0.05517164f, 0.05517164f), make_float2(0.24261114f, 0.24261114f));
-  q = __ffma2_rn(q, f, make_float2(0.69326097f, 0.69326097f));
-  q = __ffma2_rn(q, f, make_float2(0.99992806f, 0.99992806f));
-  return make_float2(__uint_as_float(__float_as_uint(t.x) * 8388608u + __float_as_uint(q.x)),
-                     __uint_as_float(__float_as_uint(t.y) * 8388608u + __float_as_uint(q.y)));
-}
 // Which of the 32 exponential pairs of a half row go to the FMA pipe (bit i = pair i). Measured
 // at configs[2] with interleaved timing (tools/fwd_experiments.py): pairs {9, 25} 6 % faster than
 // {15, 31}; {7, 23} and every 8th pair no better than {15, 31}; every 24th slower. The placement

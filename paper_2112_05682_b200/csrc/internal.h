@@ -34,6 +34,8 @@ struct BwdParams {
   float scale, scale_log2;
   const float* lse2;       // [B*H][nq_pad]: lse * log2(e), +inf in the padding
   const float* delta;      // [B*H][nq_pad]: dO_i . O_i, 0 in the padding
+  const uint8_t* aug;      // fused kernel: per (b,h, 128-query tile) 8 KiB = the bf16 K-extension
+                           // tiles [lse/scale hi, lo] and [delta hi, lo] (see bwd_preprocess)
   void* dk;                // [B,n_k,H,64] bf16
   void* dv;                // [B,n_k,H,64] bf16
   void* dq;                // [B,n_q,H,64] bf16 (deterministic path writes it directly)
@@ -67,7 +69,8 @@ cudaError_t launch_merge_partials(const float* m, const float* s, const float* v
 // backward
 // dq_acc nullable: zeroed when given (fused path)
 cudaError_t launch_bwd_preprocess(const void* out, const void* dout, const float* lse, float* delta, float* lse2,
-                                  float* dq_acc, int B, int H, int n_q, cudaStream_t s);
+                                  float* dq_acc, uint8_t* aug, float scale, int B, int H, int n_q, cudaStream_t s);
+constexpr int kAugTileBytes = 4096;   // 128 rows x 16 bf16, no-swizzle K-major core matrices
 cudaError_t launch_bwd_bf16(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                             const CUtensorMap& mdo, const CUtensorMap& mdq, cudaStream_t s);
 cudaError_t launch_dq_convert(const float* dq_acc, void* dq, int64_t numel, float scale, cudaStream_t s);

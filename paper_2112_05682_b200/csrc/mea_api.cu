@@ -400,7 +400,7 @@ mea_status_t mea_merge_partials(const float* m, const float* s, const float* vst
 // ------------------------------------------------------------------ backward
 namespace {
 struct BwdLayout {
-  size_t delta, lse2, dq_acc, lse_tmp, out_tmp, total;
+  size_t delta, lse2, dq_acc, aug, lse_tmp, out_tmp, total;
 };
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 BwdLayout bwd_layout(int64_t B, int64_t H, int64_t n_q, int64_t d, bool lse_given, bool fused) {
@@ -410,8 +410,9 @@ BwdLayout bwd_layout(int64_t B, int64_t H, int64_t n_q, int64_t d, bool lse_give
   size_t off = 0;
   L.delta = off;  off = align256(off + rows_pad * sizeof(float));
   L.lse2 = off;   off = align256(off + rows_pad * sizeof(float));
-  if (fused) {  // the fused kernel's dQ reduction target
+  if (fused) {  // the fused kernel's dQ reduction target and its score K-extension tiles
     L.dq_acc = off; off = align256(off + (size_t)B * n_q * H * d * sizeof(float));
+    L.aug = off;    off = align256(off + rows_pad / kTileM * 2 * kAugTileBytes);
   }
   if (!lse_given) {
     L.lse_tmp = off; off = align256(off + (size_t)B * H * n_q * sizeof(float));
@@ -452,6 +453,9 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
     return MEA_OK;
   }
   if (!q || !out || !dout || !dq) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
+  // The fused kernel folds lse/scale into its score MMA; scale == 0 (all scores 0, P uniform)
+  // takes the two-kernel path, whose workspace is a prefix-sized subset of the fused one.
+  if (fused && scale == 0.f) fused = false;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(dout) || !aligned16(dq) ||
       !aligned16(dk) || !aligned16(dv))
     return fail(MEA_ERR_MISALIGNED, "tensors must be 16-byte aligned");
@@ -462,6 +466,7 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   float* delta = reinterpret_cast<float*>(ws + L.delta);
   float* lse2 = reinterpret_cast<float*>(ws + L.lse2);
   float* dq_acc = fused ? reinterpret_cast<float*>(ws + L.dq_acc) : nullptr;
+  uint8_t* aug = fused ? ws + L.aug : nullptr;
 
   CUtensorMap mq, mk, mv, mdo, mdq;
   const char* why = "";
@@ -487,7 +492,8 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   }
   {
     ProfScope ps("bwd_preprocess", st);
-    if ((e = launch_bwd_preprocess(out, dout, lse, delta, lse2, dq_acc, (int)B, (int)H, (int)n_q, st)) != cudaSuccess)
+    if ((e = launch_bwd_preprocess(out, dout, lse, delta, lse2, dq_acc, aug, scale, (int)B, (int)H, (int)n_q, st)) !=
+        cudaSuccess)
       return cuda_fail(e, "bwd_preprocess launch");
   }
   BwdParams p{};
@@ -502,6 +508,7 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   p.dk = dk;
   p.dv = dv;
   p.dq_acc = dq_acc;
+  p.aug = aug;
   p.dq = dq;
   p.dq_acc = dq_acc;
   p.num_k_blocks = (int)((n_k + kTileN - 1) / kTileN);

@@ -298,6 +298,12 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_byt
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32) | (1ull << 46) | (2ull << 61);
 }
+// Shared-memory matrix descriptor, no swizzle, K-major: 8-row x 16-byte core matrices; LBO =
+// byte stride between core matrices along K, SBO = along M/N (8-row groups); layout 0.
+__device__ __forceinline__ uint64_t sdesc_noswz(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
 // Instruction descriptor, kind::f16: bf16 A/B, f32 D.
 //   [4,6) D fmt (1=f32), [7,10) A fmt (1=bf16), [10,13) B fmt (1=bf16),
 //   [15] A major (1 = MN), [16] B major (1 = MN), [17,23) N>>3, [24,29) M>>4.
@@ -311,6 +317,23 @@ __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA/ALU pipes for a pair: x = r + f, r = round(x), f in [-1/2, 1/2]; 2^f by a
+// degree-3 minimax polynomial (max relative error 7.5e-5, below the bf16 rounding of P); 2^r
+// added to the exponent field with one IMAD. x is clamped at -126. Used for a few
+// exponential pairs per row to take load off MUFU (16 exp/clk/SM; the polynomial alone 13).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));  // 1.5 * 2^23: round-to-int
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 q = __ffma2_rn(f, make_float2(0.05517164f, 0.05517164f), make_float2(0.24261114f, 0.24261114f));
+  q = __ffma2_rn(q, f, make_float2(0.69326097f, 0.69326097f));
+  q = __ffma2_rn(q, f, make_float2(0.99992806f, 0.99992806f));
+  return make_float2(__uint_as_float(__float_as_uint(t.x) * 8388608u + __float_as_uint(q.x)),
+                     __uint_as_float(__float_as_uint(t.y) * 8388608u + __float_as_uint(q.y)));
 }
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;

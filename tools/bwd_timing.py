@@ -4,6 +4,7 @@ import torch, numpy as np
 from paper_2112_05682_b200 import _lib, api
 lib = ctypes.CDLL(sys.argv[1])
 for name, (res, args) in _lib.SIGNATURES.items():
+    if not hasattr(lib, name): continue
     f = getattr(lib, name); f.restype = res; f.argtypes = args
 _lib._lib = lib
 q = torch.empty((1, 16384, 16, 64), dtype=torch.bfloat16, device="cuda")
@@ -13,10 +14,23 @@ out, lse = api.mea_attention_fwd(q, k, v, want_lse=True)
 dv = torch.zeros_like(q)
 for _ in range(2): api.mea_attention_bwd(q, k, v, out, do, lse=lse, dv=dv)
 torch.cuda.synchronize()
-ts = dv.view(torch.int64).flatten()[:4*16*8].cpu().numpy().reshape(4, 16, 8).astype(np.int64)
+raw = dv.view(torch.int64).flatten()[:512 + 16 * 8].cpu().numpy().astype(np.int64)
+ts = raw[:512].reshape(4, 16, 8)
+mm = raw[512:].reshape(16, 8)
 base = ts[0, 0, 0]
 names = ["wait_S", "compute", "wait_pfree", "store+arrive"]
 for g in range(4):
     for i in range(3):
         r = ts[g, i, :5] - base
         print(f"g{g} i={i+8}", " ".join(f"{x:7d}" for x in r), "| dt:", " ".join(f"{n}={x}" for n, x in zip(names, np.diff(r))))
+
+print("softmax means over 16 tiles (cycles):")
+for g in range(4):
+    d = np.diff(ts[g, :, :5], axis=1).mean(axis=0)
+    per = np.diff(ts[g, :, 0]).mean()
+    print(f"  g{g} period {per:7.0f} | " + " ".join(f"{n}={x:.0f}" for n, x in zip(names, d)))
+mn = ["wait_qdo", "wait_s_loaded", "wait_p_full(+issue S)", "wait_dq_empty(+issue dV dK)"]
+print("MMA warp means (cycles):", " ".join(f"{n}={x:.0f}" for n, x in zip(mn, np.diff(mm[:, :5], axis=1).mean(axis=0))),
+      f"period {np.diff(mm[:, 0]).mean():.0f}")
+for i in range(4):
+    print("  MMA", i + 8, " ".join(f"{x - base:7d}" for x in mm[i, :5]))

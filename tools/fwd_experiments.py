@@ -17,23 +17,30 @@ k, v = torch.empty_like(q), torch.empty_like(q)
 for t, tid in ((q, 1), (k, 2), (v, 3)):
     api.mea_fill_synthetic(t, 0, tid)
 outs = {p: torch.empty_like(q) for p in libs}
+lse = torch.empty((1, H, 16384), dtype=torch.float32, device=dev)
+FLUSH = os.environ.get("FLUSH", "0") == "1"   # 512 MiB read before every call (bench.py's protocol)
+flush = torch.ones(128 << 20, dtype=torch.float32, device=dev) if FLUSH else None
+sink = torch.empty((), dtype=torch.float32, device=dev)
 fns = {}
 for path in libs:
     lib = ctypes.CDLL(path)
     for name, (r, args) in _lib.SIGNATURES.items():
+        if not hasattr(lib, name): continue
         f = getattr(lib, name); f.restype = r; f.argtypes = args
     fns[path] = lib
 
 
 def call(path):
     _lib._lib = fns[path]
-    api.mea_attention_fwd(q, k, v, out=outs[path])
+    api.mea_attention_fwd(q, k, v, out=outs[path], lse=lse)
 
 
 res = {p: [] for p in libs}
 ITERS = int(os.environ.get("ITERS", "40"))
 for i in range(ITERS + 2):
     for path in libs:
+        if FLUSH:
+            torch.sum(flush, dim=0, out=sink)
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record(); call(path); e1.record()
         torch.cuda.synchronize()
