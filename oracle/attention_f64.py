@@ -49,16 +49,30 @@ def scores(q, k, scale):
     return scale * (_f64(q) @ _f64(k).T)
 
 
-def naive(q, k, v, scale, rows=None):
+def causal_mask(s, rows):
+    """Causal attention (not in the paper, which disabled packing to avoid masking, P:353;
+    reimplementations added it): query i sees keys j <= i only (n_q == n_k, top-left
+    alignment). Masked scores are -inf, so their weights e^{s - m} are exactly 0."""
+    j = np.arange(s.shape[1])[None, :]
+    return np.where(j <= np.asarray(rows)[:, None], s, -math.inf)
+
+
+def naive(q, k, v, scale, rows=None, causal=False):
     """Standard attention. Returns (out [n_q, d_v], lse [n_q]).
 
     ``rows`` restricts the evaluation to those query rows (each output row depends
     only on its own query), for sampling large configurations.
+    ``causal``: query i attends keys j <= i only (see ``causal_mask``).
     """
     q, k, v = _check(q, k, v)
+    row_ids = np.arange(q.shape[0]) if rows is None else np.asarray(rows)
+    if causal and q.shape[0] != k.shape[0]:
+        raise ValueError("causal attention needs n_q == n_k")
     if rows is not None:
-        q = q[np.asarray(rows)]
+        q = q[row_ids]
     s = scores(q, k, scale)                      # s_i = dot(q, k_i)
+    if causal:
+        s = causal_mask(s, row_ids)
     m = s.max(axis=1, keepdims=True)             # maximum score per query
     p = np.exp(s - m)                            # e^{s_i - m}
     l = p.sum(axis=1, keepdims=True)             # sum_j e^{s_j - m}
@@ -223,10 +237,12 @@ def partial_triple(q, k, v, scale):
 #     standard softmax calculus. The max carries no gradient
 #     (stop_gradient): the result does not depend on it.
 # ----------------------------------------------------------------------------------
-def backward(q, k, v, dout, scale):
+def backward(q, k, v, dout, scale, causal=False):
     q, k, v = _check(q, k, v)
     dout = _f64(dout)
     s = scores(q, k, scale)
+    if causal:
+        s = causal_mask(s, np.arange(q.shape[0]))      # masked entries: P = 0, so dS = 0
     p = np.exp(s - s.max(axis=1, keepdims=True))
     p /= p.sum(axis=1, keepdims=True)                 # P = softmax(scale q k^T)
     dv = p.T @ dout                                   # dV = P^T dO
@@ -238,7 +254,7 @@ def backward(q, k, v, dout, scale):
     return dq, dk, dv
 
 
-def backward_rows(q, k, v, dout, scale, q_rows, k_rows, block=2048):
+def backward_rows(q, k, v, dout, scale, q_rows, k_rows, block=2048, causal=False):
     """O6 restricted to some outputs, for checking large configurations: dq for the query
     rows ``q_rows`` and dk, dv for the key rows ``k_rows``, each exactly as in ``backward``
     (same formulas; the full softmax statistics lse_i and delta_i = dO_i . O_i of every query
@@ -249,15 +265,21 @@ def backward_rows(q, k, v, dout, scale, q_rows, k_rows, block=2048):
     lse = np.empty(n_q)
     delta = np.empty(n_q)
     for a in range(0, n_q, block):
-        o, l = naive(q[a:a + block], k, v, scale)
+        o, l = naive(q, k, v, scale, rows=np.arange(a, min(a + block, n_q)), causal=causal)
         lse[a:a + block] = l
         delta[a:a + block] = delta_rowsum(o, dout[a:a + block])
     qr = np.asarray(q_rows)
-    p = np.exp(scores(q[qr], k, scale) - lse[qr, None])          # P rows of the sampled queries
+    s = scores(q[qr], k, scale)
+    if causal:
+        s = causal_mask(s, qr)
+    p = np.exp(s - lse[qr, None])                                # P rows of the sampled queries
     ds = p * (dout[qr] @ v.T - delta[qr, None])
     dq = scale * (ds @ k)
     kr = np.asarray(k_rows)
-    pc = np.exp(scores(q, k[kr], scale) - lse[:, None])          # P columns of the sampled keys
+    sc = scores(q, k[kr], scale)
+    if causal:                                                   # key kr[c] is seen by queries >= kr[c]
+        sc = np.where(np.arange(n_q)[:, None] >= kr[None, :], sc, -math.inf)
+    pc = np.exp(sc - lse[:, None])                               # P columns of the sampled keys
     dv = pc.T @ dout
     dsc = pc * (dout @ v[kr].T - delta[:, None])
     dk = scale * (dsc.T @ q)
@@ -272,12 +294,12 @@ def delta_rowsum(out, dout):
 # ----------------------------------------------------------------------------------
 # O7: central finite differences of L = sum(dO o attention(q, k, v)), step h.
 # ----------------------------------------------------------------------------------
-def fd_grad(q, k, v, dout, scale, h=1e-6):
+def fd_grad(q, k, v, dout, scale, h=1e-6, causal=False):
     q, k, v = (np.array(x, dtype=np.float64) for x in _check(q, k, v))
     dout = _f64(dout)
 
     def loss():
-        return float((naive(q, k, v, scale)[0] * dout).sum())
+        return float((naive(q, k, v, scale, causal=causal)[0] * dout).sum())
 
     grads = []
     for x in (q, k, v):
@@ -297,7 +319,7 @@ def fd_grad(q, k, v, dout, scale, h=1e-6):
 # ----------------------------------------------------------------------------------
 # Multi-head wrappers over the library layout [B, n, H, d].
 # ----------------------------------------------------------------------------------
-def mha_forward(q, k, v, scale, rows=None, heads=None):
+def mha_forward(q, k, v, scale, rows=None, heads=None, causal=False):
     """O1 per (b, h). Returns out [B, n_q(or len(rows)), H, d_v] and lse [B, H, n_q]."""
     B, n_q, H, _ = q.shape
     nr = n_q if rows is None else len(rows)
@@ -305,16 +327,16 @@ def mha_forward(q, k, v, scale, rows=None, heads=None):
     lse = np.zeros((B, H, nr))
     for b in range(B):
         for h in (range(H) if heads is None else heads):
-            o, l = naive(q[b, :, h], k[b, :, h], v[b, :, h], scale, rows=rows)
+            o, l = naive(q[b, :, h], k[b, :, h], v[b, :, h], scale, rows=rows, causal=causal)
             out[b, :, h] = o
             lse[b, h] = l
     return out, lse
 
 
-def mha_backward(q, k, v, dout, scale):
+def mha_backward(q, k, v, dout, scale, causal=False):
     dq, dk, dv = (np.zeros(x.shape) for x in (q, k, v))
     for b in range(q.shape[0]):
         for h in range(q.shape[2]):
             dq[b, :, h], dk[b, :, h], dv[b, :, h] = backward(
-                q[b, :, h], k[b, :, h], v[b, :, h], dout[b, :, h], scale)
+                q[b, :, h], k[b, :, h], v[b, :, h], dout[b, :, h], scale, causal=causal)
     return dq, dk, dv

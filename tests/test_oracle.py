@@ -252,3 +252,52 @@ def test_backward_rows_equals_full_backward(rng):
     np.testing.assert_allclose(sq, dq[qr], atol=1e-12)
     np.testing.assert_allclose(sk, dk[kr], atol=1e-12)
     np.testing.assert_allclose(sv, dv[kr], atol=1e-12)
+
+
+# ---------------------------------------------------------------- causal masking
+def test_causal_rows_equal_the_stream_over_their_prefix(rng):
+    """Causal row i == the paper's sequential stream algorithm (O3) over keys 0..i —
+    a different algorithm on a sliced input, not the masked definition again. Row 0 = v_0."""
+    n, d = 23, 8
+    q, k, v = _rand(rng, n, d), _rand(rng, n, d), _rand(rng, n, d)
+    out, lse = O.naive(q, k, v, 0.7, causal=True)
+    for i in range(n):
+        ref = O.sequential(q[i:i + 1], k[:i + 1], v[:i + 1], 0.7)[0]
+        np.testing.assert_allclose(out[i], ref[0], atol=1e-12)
+        assert abs(lse[i] - np.log(np.exp(0.7 * (q[i] @ k[:i + 1].T)).sum())) < 1e-12
+    np.testing.assert_array_equal(out[0], v[0])
+    sub, sub_lse = O.naive(q, k, v, 0.7, rows=[3, 17], causal=True)
+    np.testing.assert_allclose(sub, out[[3, 17]], atol=1e-14)
+
+
+def test_causal_matches_torch_sdpa_f64(rng):
+    """Independent library implementation: torch float64 SDPA with is_causal=True."""
+    B, n, H, d = 2, 33, 3, 16
+    q, k, v = _rand(rng, B, n, H, d), _rand(rng, B, n, H, d), _rand(rng, B, n, H, d)
+    out, _ = O.mha_forward(q, k, v, 1 / math.sqrt(d), causal=True)
+    t = lambda x: torch.from_numpy(x).permute(0, 2, 1, 3)
+    ref = torch.nn.functional.scaled_dot_product_attention(t(q), t(k), t(v), is_causal=True)
+    np.testing.assert_allclose(out, ref.permute(0, 2, 1, 3).numpy(), atol=1e-12, rtol=0)
+
+
+def test_causal_backward_matches_fd_and_autograd(rng):
+    n, d = 9, 4
+    q, k, v, do = _rand(rng, n, d), _rand(rng, n, d), _rand(rng, n, d), _rand(rng, n, d)
+    an = O.backward(q, k, v, do, 0.5, causal=True)
+    fd = O.fd_grad(q, k, v, do, 0.5, causal=True)
+    for a, f in zip(an, fd):
+        assert np.abs(a - f).max() <= 1e-5 * max(1.0, np.abs(f).max())
+    tq, tk, tv = (torch.tensor(x, requires_grad=True) for x in (q, k, v))
+    s = 0.5 * tq @ tk.T
+    s = s.masked_fill(torch.triu(torch.ones(n, n, dtype=torch.bool), 1), float("-inf"))
+    (torch.softmax(s, dim=-1) @ tv).backward(torch.from_numpy(do))
+    for a, t in zip(an, (tq, tk, tv)):
+        np.testing.assert_allclose(a, t.grad.numpy(), atol=1e-12)
+    # the last key is seen by the last query only: dv_{n-1} = P_{n-1,n-1} dO_{n-1}
+    p_last = np.exp(0.5 * q[-1] @ k.T - O.naive(q, k, v, 0.5, causal=True)[1][-1])[-1]
+    np.testing.assert_allclose(an[2][-1], p_last * do[-1], atol=1e-12)
+    qr, kr = np.array([0, 4, 8]), np.array([0, 3, 8])
+    sq, sk, sv = O.backward_rows(q, k, v, do, 0.5, qr, kr, block=4, causal=True)
+    np.testing.assert_allclose(sq, an[0][qr], atol=1e-12)
+    np.testing.assert_allclose(sk, an[1][kr], atol=1e-12)
+    np.testing.assert_allclose(sv, an[2][kr], atol=1e-12)
