@@ -302,6 +302,17 @@ def main():
                                                                      workspace=bwd_ws), max(3, a.steps // 2), 1))
         extras["bwd"] = {"ms": bwd_ms, "tflops": flop_bwd / (bwd_ms * 1e-3) / 1e12,
                          "frac": flop_bwd / (bwd_ms * 1e-3) / 1e12 / pk["tflops"]}
+    # ---------------- causal masking: flops of the visible (i, j <= i) pairs only
+    if a.workload == "cfg3" and not a.fwd_only:
+        vis = n * (n + 1) / 2 * D * Hl * Bl
+        cf_ms = statistics.mean(timed(lambda: api.mea_attention_fwd_causal(q, k, v, out=out, lse=lse),
+                                      max(3, a.steps // 2), 1))
+        cb_ms = statistics.mean(timed(lambda: api.mea_attention_bwd_causal(q, k, v, out, do, lse=lse, dq=dq, dk=dk,
+                                                                           dv=dv, workspace=bwd_ws),
+                                      max(3, a.steps // 2), 1))
+        extras["causal"] = {"fwd_ms": cf_ms, "fwd_tflops": 4 * vis / (cf_ms * 1e-3) / 1e12,
+                            "bwd_ms": cb_ms, "bwd_tflops": 10 * vis / (cb_ms * 1e-3) / 1e12,
+                            "flops": "visible pairs only: 4 (fwd) / 10 (bwd) x n(n+1)/2 x d x H"}
     # ---------------- the paper's literal schedule (query chunk 1024 / key chunk 4096)
     if a.workload == "cfg3":
         ws_kc = api.mea_attention_fwd_workspace_size(Bl, Hl, n, n, D, api.MEA_BF16, 1024, 4096)

@@ -100,6 +100,18 @@ MEA_API mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int6
                                               int64_t k_chunk, size_t* bytes);
 
 /*
+ * Causal self-attention forward (not in the paper, which disabled
+ * packing to avoid masking; reimplementations added it): query i
+ * attends keys j <= i only. q, k, v, out [B,n,H,d] (n_q == n_k == n, top-left aligned), lse as
+ * for mea_attention_fwd. bf16 inputs with d == 64 only (MEA_ERR_UNSUPPORTED otherwise); online
+ * schedule (no key chunks), no workspace. Key tiles past a query tile's diagonal are skipped.
+ */
+MEA_API mea_status_t mea_attention_fwd_causal(const void* q, const void* k, const void* v, void* out,
+                                      int64_t B, int64_t H, int64_t n, int64_t d,
+                                      mea_dtype_t in_dtype, mea_dtype_t out_dtype, float scale,
+                                      float* lse, void* stream);
+
+/*
  * Single-query attention per (b,h) — the paper's O(1)-memory algorithm (PAPER.md:59-63,
  * stabilised as in PAPER.md:85-90). q,out [B,H,d]; k,v [B,n_k,H,d]. Keys are split into
  * ranges processed in parallel (split-K); each range yields a triple (m*, s*, v*) in the
@@ -189,6 +201,18 @@ MEA_API mea_status_t mea_attention_bwd_deterministic_workspace_size(int64_t B, i
 MEA_API mea_status_t mea_attention_bwd_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k,
                                               int64_t d, mea_dtype_t dtype, int lse_given,
                                               size_t* bytes);
+
+/*
+ * Backward of mea_attention_fwd_causal: arguments as mea_attention_bwd with n_q == n_k == n;
+ * lse (nullable) must come from the causal forward. Workspace: mea_attention_bwd_workspace_size
+ * (B, H, n, n, d, dtype, lse_given). scale == 0 is MEA_ERR_UNSUPPORTED here. Each key tile
+ * loops over the query tiles from its diagonal on.
+ */
+MEA_API mea_status_t mea_attention_bwd_causal(const void* q, const void* k, const void* v,
+                                      const void* out, const void* dout, void* dq, void* dk,
+                                      void* dv, int64_t B, int64_t H, int64_t n, int64_t d,
+                                      mea_dtype_t dtype, float scale, const float* lse,
+                                      void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * Synthetic input generator (not part of the method; used by tests and the bench so

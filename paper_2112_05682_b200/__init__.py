@@ -6,7 +6,7 @@ for sm_100a; ``api`` is a thin ctypes binding with the same function names.
 from .api import (  # noqa: F401
     MEA_BF16, MEA_F32, EmptyKeysError, MeaError, mea_attention_bwd, mea_attention_bwd_deterministic,
     mea_attention_bwd_deterministic_workspace_size, mea_attention_bwd_workspace_size,
-    mea_attention_partial_fwd,
+    mea_attention_bwd_causal, mea_attention_fwd_causal, mea_attention_partial_fwd,
     mea_attention_fwd, mea_attention_fwd_workspace_size, mea_debug_umma_tile, mea_fill_synthetic,
     mea_merge_partials, mea_single_query_fwd, mea_single_query_partial, mea_single_query_workspace_size, version,
 )

@@ -107,6 +107,22 @@ def mea_attention_fwd(q, k, v, scale=None, out=None, out_dtype=None, lse=None, w
     return (out, lse) if (want_lse or lse is not None) else out
 
 
+def mea_attention_fwd_causal(q, k, v, scale=None, out=None, out_dtype=None, lse=None, want_lse=False):
+    """Causal self-attention (query i sees keys j <= i); q, k, v [B, n, H, d] bf16, d = 64."""
+    _cuda_contig(q, k, v, out, lse)
+    B, n, H, d = q.shape
+    if k.shape != q.shape or v.shape != q.shape:
+        raise ValueError(f"causal attention needs q, k, v of one shape, got {tuple(q.shape)} {tuple(k.shape)}")
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    if out is None:
+        out = torch.empty((B, n, H, d), dtype=q.dtype if out_dtype is None else out_dtype, device=q.device)
+    if want_lse and lse is None:
+        lse = torch.empty((B, H, n), dtype=torch.float32, device=q.device)
+    _check(_lib.load().mea_attention_fwd_causal(_ptr(q), _ptr(k), _ptr(v), _ptr(out), B, H, n, d, _dtype(q),
+                                                _dtype(out), scale, _ptr(lse), _stream(q.device)))
+    return (out, lse) if (want_lse or lse is not None) else out
+
+
 def mea_attention_partial_fwd(q, k, v, scale=None):
     """Stream state (m*, s*, v*) of every query row over this call's keys (one key range of a
     sharded self-attention). Returns m [B,n_q,H], s [B,n_q,H] and vstar [B,n_q,H,d], float32,
@@ -217,6 +233,16 @@ def mea_attention_bwd(q, k, v, out, dout, lse=None, scale=None, dq=None, dk=None
     """(dq, dk, dv) of out = attention(q, k, v) given dout (recompute-per-tile backward)."""
     return _bwd(_lib.load().mea_attention_bwd, mea_attention_bwd_workspace_size, q, k, v, out, dout, lse, scale,
                 dq, dk, dv, workspace)
+
+
+def mea_attention_bwd_causal(q, k, v, out, dout, lse=None, scale=None, dq=None, dk=None, dv=None, workspace=None):
+    """(dq, dk, dv) of out = mea_attention_fwd_causal(q, k, v) given dout."""
+    lib = _lib.load()
+    fn = lambda q_, k_, v_, o_, do_, dq_, dk_, dv_, B, H, n_q, n_k, d, dt, sc, lse_, ws, nb, st: \
+        lib.mea_attention_bwd_causal(q_, k_, v_, o_, do_, dq_, dk_, dv_, B, H, n_q, d, dt, sc, lse_, ws, nb, st)
+    if q.shape != k.shape:
+        raise ValueError("causal attention needs n_q == n_k")
+    return _bwd(fn, mea_attention_bwd_workspace_size, q, k, v, out, dout, lse, scale, dq, dk, dv, workspace)
 
 
 def mea_attention_bwd_deterministic(q, k, v, out, dout, lse=None, scale=None, dq=None, dk=None, dv=None,

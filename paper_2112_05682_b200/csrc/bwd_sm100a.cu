@@ -107,7 +107,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
   const int kblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int k0 = kblk * kTile;
   const int NQ = (p.n_q + kTile - 1) / kTile;
-  const int nq_pad = NQ * kTile;
+  // causal (n_q == n_k): queries before this key tile see none of its keys; iteration i
+  // (stages, barrier phases) handles query tile i0 + i
+  const int i0 = p.causal ? kblk : 0;
+  const int NT = NQ - i0;
   const size_t bh = (size_t)b * p.H + h;
 
   if (threadIdx.x == 0) {
@@ -157,14 +160,15 @@ __global__ void __launch_bounds__(kBThreads, 1)
         tma_load_4d(sm.v, &mv, &sm.kv_full, 0, h, k0, b, keep);
       }
       __syncwarp();
-      for (int i = 0; i < NQ; ++i) {
+      for (int i = 0; i < NT; ++i) {
         const int st = i % kBStages, n = i / kBStages;
         if (i >= kBStages) mbar_wait(&sm.qdo_empty[st], (n - 1) & 1);
         if (elect_one()) {
           mbar_arrive_expect_tx(&sm.qdo_full[st], 2 * kTileBytes + 2 * kAugTileBytes);
-          tma_load_4d(sm.q[st], &mq, &sm.qdo_full[st], 0, h, i * kTile, b, keep);
-          tma_load_4d(sm.dout[st], &mdo, &sm.qdo_full[st], 0, h, i * kTile, b, keep);
-          bulk_load(sm.aug[st], p.aug + (bh * NQ + i) * (2 * kAugTileBytes), 2 * kAugTileBytes, &sm.qdo_full[st]);
+          tma_load_4d(sm.q[st], &mq, &sm.qdo_full[st], 0, h, (i0 + i) * kTile, b, keep);
+          tma_load_4d(sm.dout[st], &mdo, &sm.qdo_full[st], 0, h, (i0 + i) * kTile, b, keep);
+          bulk_load(sm.aug[st], p.aug + (bh * NQ + i0 + i) * (2 * kAugTileBytes), 2 * kAugTileBytes,
+                    &sm.qdo_full[st]);
         }
         __syncwarp();
       }
@@ -209,9 +213,9 @@ __global__ void __launch_bounds__(kBThreads, 1)
 #else
 #define MPROBE(k)
 #endif
-      for (int i = 0; i < NQ; ++i) {
+      for (int i = 0; i < NT; ++i) {
         const int st = i % kBStages;
-        const bool more = i + 1 < NQ;
+        const bool more = i + 1 < NT;
         MPROBE(0)
         // the next tile's scores as soon as the softmax warps have read ST_i / dPT_i, so they
         // are computed while softmax i runs
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
 #else
 #define TPROBE(k)
 #endif
-    for (int i = 0; i < NQ; ++i) {
+    for (int i = 0; i < NT; ++i) {
       const int st = i % kBStages;
       TPROBE(0)
       mbar_wait(&sm.s_full, i & 1);
@@ -288,6 +292,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&sm.s_loaded);  // ST_i / dPT_i are in registers: the next scores may overwrite
+      const bool diag = p.causal && i == 0;
       uint32_t pk[16], dk[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
@@ -297,6 +302,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
         // P (lse2 = +inf pads -> 0); the pairs in MEA_BPOLY_MASK on the FMA pipe unload MUFU
         float2 pr = (((MEA_BPOLY_MASK) >> u) & 1u) ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
         if (!key_ok) pr = make_float2(0.f, 0.f);
+        if (diag) {  // causal diagonal tile: key j > query (32 g + 2 u + {0, 1}) is masked
+          if (j > 32 * g + 2 * u) pr.x = 0.f;
+          if (j > 32 * g + 2 * u + 1) pr.y = 0.f;
+        }
         const float2 ds = __fmul2_rn(pr, d2);  // P (dP - delta)
         pk[u] = pack_bf16x2(pr.x, pr.y);
         dk[u] = pack_bf16x2(ds.x, ds.y);
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const int quarter = warp & 3;
     const int rq = quarter * 32 + lane;  // query row within the tile (TMEM lane)
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-    for (int i = 0; i < NQ; ++i) {
+    for (int i = 0; i < NT; ++i) {
       const int buf = i % kDqBufs;
       mbar_wait(&sm.dq_full, i & 1);
       // the TMA reduce that last read this staging buffer (tile i - kDqBufs) must be done reading
@@ -376,8 +385,8 @@ __global__ void __launch_bounds__(kBThreads, 1)
       fence_proxy_async_smem();
       named_bar_sync(kBarDq, 128);
       if (warp == 20 && lane == 0) {
-        tma_reduce_add_4d(&mdq, sm.dq_stage[buf][0], 0, h, i * kTile, b);
-        tma_reduce_add_4d(&mdq, sm.dq_stage[buf][1], 32, h, i * kTile, b);
+        tma_reduce_add_4d(&mdq, sm.dq_stage[buf][0], 0, h, (i0 + i) * kTile, b);
+        tma_reduce_add_4d(&mdq, sm.dq_stage[buf][1], 32, h, (i0 + i) * kTile, b);
         bulk_commit_group();
       }
     }

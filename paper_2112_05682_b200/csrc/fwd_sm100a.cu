@@ -121,14 +121,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   FwdSmem& sm = *reinterpret_cast<FwdSmem*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qblk = blockIdx.x % p.num_q_blocks;
+  // causal: the blocks with the most key tiles (the last rows) are scheduled first
+  const int qblk = p.causal ? p.num_q_blocks - 1 - (int)(blockIdx.x % p.num_q_blocks) : blockIdx.x % p.num_q_blocks;
   const int split = blockIdx.x / p.num_q_blocks;
   const int h = blockIdx.y, b = blockIdx.z;
   const int q0 = p.q_begin + qblk * kRowsPerCta;
   const int q_end = min(p.n_q, p.q_begin + p.q_count);
   const int n_tiles = (p.n_k + kTileN - 1) / kTileN;
   const int t_begin = split * p.tiles_per_split;
-  const int t_end = min(n_tiles, t_begin + p.tiles_per_split);
+  // causal (n_q == n_k, no split): query tile qt of this block needs key tiles [0, 2 qblk + qt]
+  // (the last one is its diagonal tile); the producer streams the union.
+  const int t_end = p.causal ? min(n_tiles, 2 * qblk + 2) : min(n_tiles, t_begin + p.tiles_per_split);
   const int T = t_end - t_begin;
   const int key_end = min(p.n_k, t_end * kTileN);
 
@@ -190,6 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // warp walks the schedule (waits are warp-wide); one elected lane issues. Descriptors are
     // precomputed: a K step or a ring stage is a plain add to the start-address field.
     const int qt = __shfl_sync(0xffffffffu, warp >> 1, 0);
+    const int Tq = p.causal ? min(T, 2 * qblk + qt + 1) : T;  // key tiles this query tile uses
     const uint64_t dq = shfl0_u64(sdesc_sw128(smem_u32(sm.q[qt]), 16, 1024));
     const uint64_t dk0 = shfl0_u64(sdesc_sw128(smem_u32(sm.k[0]), 16, 1024));
     const uint64_t dv0 = shfl0_u64(sdesc_sw128(smem_u32(sm.v[0]), 16, 1024));
@@ -214,10 +218,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       umma_commit(&sm.s_full[qt]);
     }
     __syncwarp();
-    for (int t = 0; t < T; ++t) {
+    for (int t = 0; t < Tq; ++t) {
       const int st = t % kStages;
       const int nx = (t + 1) % kStages;
-      const bool more = (t + 1) < T;
+      const bool more = (t + 1) < Tq;
       // S_{t+1} = Q K_{t+1}^T as soon as the softmax warps have read S_t out of TMEM, so the
       // next scores are computed while the current softmax runs.
       if (more) {
@@ -239,6 +243,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&sm.kv_empty[st]);  // this tile is done with K_t, V_t (2 arrivals free it)
         if (!more) umma_commit(&sm.o_done[qt]);
       }
+      __syncwarp();
+    }
+    // key tiles past this query tile's diagonal (causal): release their ring stage without
+    // using it (a commit keeps the arrival ordered after this warp's earlier MMAs)
+    for (int t = Tq; t < T; ++t) {
+      mbar_wait(&sm.kv_full[t % kStages], (t / kStages) & 1);
+      if (elect_one()) umma_commit(&sm.kv_empty[t % kStages]);
       __syncwarp();
     }
   }
@@ -269,20 +280,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #else
 #define TPROBE(k)
 #endif
-    for (int t = 0; t < T; ++t) {
+    const int Tq = p.causal ? min(T, 2 * qblk + qt + 1) : T;
+    const int diag = p.causal ? 2 * qblk + qt : -1;  // the causal diagonal key tile of this query tile
+    for (int t = 0; t < Tq; ++t) {
       TPROBE(0)
       mbar_wait(&sm.s_full[qt], t & 1);
       TPROBE(1)
       tc_fence_after();
       uint32_t sr[64];
-      const int tile_valid = key_end - (t_begin + t) * kTileN;  // keys of this tile in range
+      // keys of this tile in range (causal: keys <= row)
+      const int tile_valid = (p.causal ? min(key_end, row + 1) : key_end) - (t_begin + t) * kTileN;
       const int valid = tile_valid - half * 64;                // ... of my half (may be <= 0)
       uint32_t pk[32];  // P in bf16 pairs
       float ext = 0.f;
       bool have_ext = false;
       // Fast path (full tile, m* already set): exponentiate against the current reference max.
       // The second 32 score columns load while the first 32 are exponentiated.
-      bool fast = (t > 0) && (tile_valid >= kTileN) && (c >= 0.f);
+      bool fast = (t > 0) && (t != diag) && (key_end - (t_begin + t) * kTileN >= kTileN) && (c >= 0.f);
       tmem_ld32_split<64>(lane_base + colS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
       if (fast) {
         tmem_ld_wait();

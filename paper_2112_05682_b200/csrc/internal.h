@@ -27,6 +27,7 @@ struct FwdParams {
   float* tri_m;            // partial mode (mea_attention_partial_fwd): [B,n_q,H] m* (natural log)
   float* tri_s;            //   [B,n_q,H] s*
   float* tri_v;            //   [B,n_q,H,64] v* (unnormalised)
+  int causal;              // query i sees keys j <= i (n_q == n_k, one window, no key split)
 };
 
 struct BwdParams {
@@ -41,6 +42,7 @@ struct BwdParams {
   void* dq;                // [B,n_q,H,64] bf16 (deterministic path writes it directly)
   float* dq_acc;           // [B,n_q,H,64] f32 reduction target (fused path)
   int num_k_blocks;        // ceil(n_k / 128)
+  int causal;              // query i sees keys j <= i (n_q == n_k): query tiles from the diagonal on
 };
 
 // 4-D tensor map over a [B, n, H, d] tensor (d innermost), box {64, 1, box_rows, 1},

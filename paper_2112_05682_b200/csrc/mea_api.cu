@@ -180,11 +180,16 @@ mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
   return MEA_OK;
 }
 
-mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
-                               int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t in_dtype, mea_dtype_t out_dtype,
-                               float scale, float* lse, int64_t q_chunk, int64_t k_chunk, void* workspace,
-                               size_t workspace_bytes, void* stream) {
+}  // extern "C"
+
+static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
+                             int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t in_dtype, mea_dtype_t out_dtype,
+                             float scale, float* lse, int64_t q_chunk, int64_t k_chunk, void* workspace,
+                             size_t workspace_bytes, void* stream, bool causal) {
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, scale)) return s;
+  if (causal && n_q != n_k) return fail(MEA_ERR_UNSUPPORTED, "causal attention needs n_q == n_k");
+  if (causal && in_dtype != MEA_BF16) return fail(MEA_ERR_UNSUPPORTED, "causal attention: bf16 path only");
+  if (causal) q_chunk = k_chunk = 0;  // causal runs the online schedule (no key split)
   if (q_chunk < 0 || k_chunk < 0) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
   if (!valid_dtype(in_dtype) || !valid_dtype(out_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
   if (n_q == 0) return MEA_OK;
@@ -236,6 +241,7 @@ mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void
   p.out = out;
   p.out_f32 = out_dtype == MEA_F32;
   p.lse = lse;
+  p.causal = causal ? 1 : 0;
   p.num_splits = pl.splits;
   p.tiles_per_split = pl.tiles_per_split;
   if (pl.splits > 1) {
@@ -258,6 +264,22 @@ mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void
     }
   }
   return MEA_OK;
+}
+
+extern "C" {
+
+mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
+                               int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t in_dtype, mea_dtype_t out_dtype,
+                               float scale, float* lse, int64_t q_chunk, int64_t k_chunk, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  return fwd_impl(q, k, v, out, B, H, n_q, n_k, d, in_dtype, out_dtype, scale, lse, q_chunk, k_chunk, workspace,
+                  workspace_bytes, stream, false);
+}
+
+mea_status_t mea_attention_fwd_causal(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
+                                      int64_t n, int64_t d, mea_dtype_t in_dtype, mea_dtype_t out_dtype, float scale,
+                                      float* lse, void* stream) {
+  return fwd_impl(q, k, v, out, B, H, n, n, d, in_dtype, out_dtype, scale, lse, 0, 0, nullptr, 0, stream, true);
 }
 
 // ------------------------------------------------------------------ partial self-attention
@@ -437,8 +459,10 @@ mea_status_t mea_attention_bwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
 static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const void* out, const void* dout, void* dq,
                              void* dk, void* dv, int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
                              mea_dtype_t dtype, float scale, const float* lse, void* workspace,
-                             size_t workspace_bytes, void* stream, bool fused) {
+                             size_t workspace_bytes, void* stream, bool fused, bool causal = false) {
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, scale)) return s;
+  if (causal && n_q != n_k) return fail(MEA_ERR_UNSUPPORTED, "causal attention needs n_q == n_k");
+  if (causal && scale == 0.f) return fail(MEA_ERR_UNSUPPORTED, "causal backward needs scale != 0");
   if (!valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
   if (n_k == 0) return fail(MEA_ERR_EMPTY_KEYS, "attention over an empty key list");
   if (dtype != MEA_BF16 || d != kHeadDim) return fail(MEA_ERR_UNSUPPORTED, "backward: bf16 with d == 64");
@@ -485,8 +509,8 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   if (!lse) {
     // B0: the statistics pass — rerun the forward for lse (its output goes to scratch).
     float* lse_tmp = reinterpret_cast<float*>(ws + L.lse_tmp);
-    mea_status_t r = mea_attention_fwd(q, k, v, ws + L.out_tmp, B, H, n_q, n_k, d, MEA_BF16, MEA_BF16, scale, lse_tmp,
-                                       0, 0, nullptr, 0, stream);
+    mea_status_t r = fwd_impl(q, k, v, ws + L.out_tmp, B, H, n_q, n_k, d, MEA_BF16, MEA_BF16, scale, lse_tmp, 0, 0,
+                              nullptr, 0, stream, causal);
     if (r != MEA_OK) return r;
     lse = lse_tmp;
   }
@@ -512,6 +536,7 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   p.dq = dq;
   p.dq_acc = dq_acc;
   p.num_k_blocks = (int)((n_k + kTileN - 1) / kTileN);
+  p.causal = causal ? 1 : 0;
   if (fused) {
     {
       ProfScope ps("bwd_bf16", st);
@@ -539,6 +564,14 @@ mea_status_t mea_attention_bwd(const void* q, const void* k, const void* v, cons
                                size_t workspace_bytes, void* stream) {
   return bwd_impl(q, k, v, out, dout, dq, dk, dv, B, H, n_q, n_k, d, dtype, scale, lse, workspace, workspace_bytes,
                   stream, true);
+}
+
+mea_status_t mea_attention_bwd_causal(const void* q, const void* k, const void* v, const void* out,
+                                      const void* dout, void* dq, void* dk, void* dv, int64_t B, int64_t H, int64_t n,
+                                      int64_t d, mea_dtype_t dtype, float scale, const float* lse, void* workspace,
+                                      size_t workspace_bytes, void* stream) {
+  return bwd_impl(q, k, v, out, dout, dq, dk, dv, B, H, n, n, d, dtype, scale, lse, workspace, workspace_bytes,
+                  stream, true, true);
 }
 
 mea_status_t mea_attention_bwd_deterministic_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k,
