@@ -6,7 +6,7 @@ using namespace mea;
 
 // form: 0 SS K/K N=128 (QK^T)   1 TS A=tmem, B MN N=64 (PV, dV)   2 SS A K-major, B MN N=64 (dK)
 //       3 SS A MN (2 atoms, LBO 16K), B MN N=64 (dQ)             4 SS K/K N=64
-template <int FORM>
+template <int FORM, bool STREAM>
 __global__ void __launch_bounds__(128, 1) kern(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
@@ -34,11 +34,12 @@ __global__ void __launch_bounds__(128, 1) kern(int iters, unsigned long long* ou
           if (FORM == 3) umma_ss(tm, am + kk * 128, b + kk * 128, idesc_bf16_f32(128, 64, true, true), 1);
           if (FORM == 4) umma_ss(tm, a + (kk & 3) * 2, b + (kk & 3) * 2, idesc_bf16_f32(128, 64, false, false), 1);
         }
-        umma_commit(&bar);
+        if (!STREAM || it == iters - 1) umma_commit(&bar);
       }
       __syncwarp();
-      mbar_wait(&bar, it & 1);
+      if (!STREAM) mbar_wait(&bar, it & 1);
     }
+    if (STREAM) mbar_wait(&bar, 0);
     const unsigned long long t1 = clock64();
     if (threadIdx.x == 32) out[blockIdx.x] = (t1 - t0) / iters;
   }
@@ -46,11 +47,11 @@ __global__ void __launch_bounds__(128, 1) kern(int iters, unsigned long long* ou
   if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tm); }
 }
 
-template <int F>
+template <int F, bool S = false>
 void run(const char* name, int n) {
   unsigned long long* d; cudaMalloc(&d, 148 * 8);
-  cudaFuncSetAttribute(kern<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
-  kern<F><<<148, 128, 66 * 1024>>>(200, d);
+  cudaFuncSetAttribute(kern<F, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+  kern<F, S><<<148, 128, 66 * 1024>>>(200, d);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
   const double macs = 8.0 * 128 * n * 16;
@@ -64,5 +65,11 @@ int main() {
   run<1>("TS  A TMEM,    B MN-major, N=64 (PV, dV)", 64);
   run<2>("SS  A K-major, B MN-major, N=64 (dK)", 64);
   run<3>("SS  A MN-major,B MN-major, N=64 (dQ)", 64);
+  printf("streaming (one commit at the end):\n");
+  run<0, true>("SS  A K-major, B K-major, N=128 (QK^T)", 128);
+  run<4, true>("SS  A K-major, B K-major, N=64", 64);
+  run<1, true>("TS  A TMEM,    B MN-major, N=64 (PV, dV)", 64);
+  run<2, true>("SS  A K-major, B MN-major, N=64 (dK)", 64);
+  run<3, true>("SS  A MN-major,B MN-major, N=64 (dQ)", 64);
   return 0;
 }
