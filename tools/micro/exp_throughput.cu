@@ -1,5 +1,6 @@
 // Throughput of ex2.approx (MUFU) vs an FMA-pipe polynomial exp2, per SM, vs warps per SM.
 #include <cstdio>
+#include <cstdint>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 
@@ -16,6 +17,10 @@ __device__ __forceinline__ float2 poly2(float2 x) {
                      __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
 }
 
+__device__ __forceinline__ uint32_t ex2h2(uint32_t x) { uint32_t y; asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x)); return y; }
+__device__ __forceinline__ uint32_t ex2bf2(uint32_t x) { uint32_t y; asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x)); return y; }
+__device__ __forceinline__ uint32_t cvt_h2(float2 v) { uint32_t y; asm("cvt.rn.f16x2.f32 %0, %2, %1;" : "=r"(y) : "f"(v.x), "f"(v.y)); return y; }
+
 template <int MODE>
 __global__ void kern(float* out, int iters) {
   float2 v[8];
@@ -26,7 +31,12 @@ __global__ void kern(float* out, int iters) {
     for (int i = 0; i < 8; ++i) {
       float2 e;
       if (MODE == 0) e = make_float2(ex2(v[i].x), ex2(v[i].y));
-      else e = poly2(v[i]);
+      else if (MODE == 1) e = poly2(v[i]);
+      else {  // packed half-precision: 2 exps per instruction (+ the f32 -> f16x2 conversion)
+        const uint32_t h = cvt_h2(v[i]);
+        const uint32_t r = MODE == 2 ? ex2h2(h) : ex2bf2(h);
+        e = make_float2(__uint_as_float(r << 16), __uint_as_float(r & 0xffff0000u));
+      }
       acc = __fadd2_rn(acc, e);
       v[i].x -= 1e-7f; v[i].y -= 1e-7f;
     }
@@ -37,17 +47,18 @@ __global__ void kern(float* out, int iters) {
 int main() {
   float* d; cudaMalloc(&d, 4);
   const int iters = 4096;
-  for (int mode = 0; mode < 2; ++mode)
+  const char* names[4] = {"mufu f32  ", "poly      ", "f16x2     ", "bf16x2    "};
+  for (int mode = 0; mode < 4; ++mode)
     for (int warps : {4, 8, 16, 32}) {
       cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-      auto k = mode == 0 ? kern<0> : kern<1>;
+      auto k = mode == 0 ? kern<0> : mode == 1 ? kern<1> : mode == 2 ? kern<2> : kern<3>;
       k<<<148, warps * 32>>>(d, iters);
       cudaEventRecord(a);
       k<<<148, warps * 32>>>(d, iters);
       cudaEventRecord(b); cudaEventSynchronize(b);
       float ms; cudaEventElapsedTime(&ms, a, b);
       const double exps = 148.0 * warps * 32 * iters * 16;
-      printf("%s warps/SM=%2d: %.3f ms  %.1f exp/clk/SM (at 1.9 GHz)\n", mode ? "poly " : "mufu ", warps, ms,
+      printf("%s warps/SM=%2d: %.3f ms  %.1f exp/clk/SM (at 1.9 GHz)\n", names[mode], warps, ms,
              exps / (ms * 1e-3) / 148 / 1.9e9);
     }
   return 0;
