@@ -313,6 +313,20 @@ def main():
         extras["causal"] = {"fwd_ms": cf_ms, "fwd_tflops": 4 * vis / (cf_ms * 1e-3) / 1e12,
                             "bwd_ms": cb_ms, "bwd_tflops": 10 * vis / (cb_ms * 1e-3) / 1e12,
                             "flops": "visible pairs only: 4 (fwd) / 10 (bwd) x n(n+1)/2 x d x H"}
+    # ---------------- head dimension 128: forward, configs[2]'s B, H, n
+    if a.workload == "cfg3":
+        q128 = torch.empty((Bl, n, Hl, 128), dtype=torch.bfloat16, device=dev)
+        k128, v128 = torch.empty_like(q128), torch.empty_like(q128)
+        for t, tid in ((q128, gen.TENSOR_Q), (k128, gen.TENSOR_K), (v128, gen.TENSOR_V)):
+            api.mea_fill_synthetic(t, a.seed, tid, offset=rank * q128.numel())
+        o128 = torch.empty_like(q128)
+        l128 = torch.empty((Bl, Hl, n), dtype=torch.float32, device=dev)
+        f128_ms = statistics.mean(timed(lambda: api.mea_attention_fwd(q128, k128, v128, out=o128, lse=l128),
+                                        max(3, a.steps // 2), 1))
+        fl128 = 4 * n * n * 128 * Hl * Bl
+        extras["fwd_d128"] = {"ms": f128_ms, "tflops": fl128 / (f128_ms * 1e-3) / 1e12,
+                              "frac": fl128 / (f128_ms * 1e-3) / 1e12 / pk["tflops"], "kernel": "fwd128_bf16"}
+        del q128, k128, v128, o128, l128
     # ---------------- the paper's literal schedule (query chunk 1024 / key chunk 4096)
     if a.workload == "cfg3":
         ws_kc = api.mea_attention_fwd_workspace_size(Bl, Hl, n, n, D, api.MEA_BF16, 1024, 4096)

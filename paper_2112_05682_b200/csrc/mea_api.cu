@@ -176,7 +176,7 @@ mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
   if (q_chunk < 0 || k_chunk < 0) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
   if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  *bytes = (in_dtype == MEA_BF16) ? plan_fwd(B, H, n_q, n_k, q_chunk, k_chunk).ws : 0;
+  *bytes = (in_dtype == MEA_BF16 && d == kHeadDim) ? plan_fwd(B, H, n_q, n_k, q_chunk, k_chunk).ws : 0;
   return MEA_OK;
 }
 
@@ -211,7 +211,34 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
     return e == cudaSuccess ? MEA_OK : cuda_fail(e, "fwd_f32 launch");
   }
 
-  if (d != kHeadDim) return fail(MEA_ERR_UNSUPPORTED, "bf16 tensor-core path supports d == 64");
+  if (d == 128) {  // fwd128_sm100a.cu: online schedule only
+    if (causal) return fail(MEA_ERR_UNSUPPORTED, "causal attention: d == 64 only");
+    if (k_chunk > 0 && k_chunk < n_k) return fail(MEA_ERR_UNSUPPORTED, "key chunks: d == 64 only");
+    CUtensorMap mq, mk, mv;
+    const char* why = "";
+    cudaError_t e;
+    if ((e = make_bnhd_map(&mq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_q, H, d, 64, kTileM,
+                           CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+        (e = make_bnhd_map(&mk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
+                           CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+        (e = make_bnhd_map(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
+                           CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess)
+      return cuda_fail(e, why);
+    FwdParams p{};
+    p.B = (int)B;
+    p.H = (int)H;
+    p.n_q = (int)n_q;
+    p.n_k = (int)n_k;
+    p.scale = scale;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    p.out = out;
+    p.out_f32 = out_dtype == MEA_F32;
+    p.lse = lse;
+    ProfScope ps("fwd128_bf16", st);
+    if ((e = launch_fwd128_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd128_bf16 launch");
+    return MEA_OK;
+  }
+  if (d != kHeadDim) return fail(MEA_ERR_UNSUPPORTED, "bf16 tensor-core path supports d in {64, 128}");
   const FwdPlan pl = plan_fwd(B, H, n_q, n_k, q_chunk, k_chunk);
   if (pl.ws > 0) {
     if (workspace_bytes < pl.ws || !workspace) return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "key-chunk summaries need workspace");

@@ -1,0 +1,89 @@
+"""GPU parity of the d = 128 forward ("d=64 first; d=128 NEXT"; fwd128_sm100a.cu)
+against the float64 oracle (O1) on the same generated inputs: shapes over several query and key
+tiles with ragged tails, both output dtypes and scales, the rescale stress case, configs[2]'s
+length at d = 128 on sampled rows, and the explicit errors of what d = 128 does not cover.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from tests import helpers as Hh
+
+pytestmark = pytest.mark.gpu
+D = 128
+
+
+def _run(q, k, v, scale=None, out_dtype=None):
+    from paper_2112_05682_b200 import api
+    out, lse = api.mea_attention_fwd(Hh.to_dev(q, torch.bfloat16), Hh.to_dev(k, torch.bfloat16),
+                                     Hh.to_dev(v, torch.bfloat16), scale=scale, out_dtype=out_dtype, want_lse=True)
+    torch.cuda.synchronize()
+    return out.double().cpu().numpy(), lse.double().cpu().numpy()
+
+
+@pytest.mark.parametrize("B,n_q,n_k,H", [(1, 1, 1, 1), (1, 17, 129, 2), (2, 300, 1000, 3), (1, 1000, 17, 1),
+                                         (1, 256, 4097, 2)])
+def test_d128_forward_matches_oracle(B, n_q, n_k, H):
+    q, k, v = Hh.host_inputs(B, n_q, n_k, H, D, seed=41)
+    ref, ref_lse = O.mha_forward(q, k, v, 1 / math.sqrt(D))
+    got, lse = _run(q, k, v)
+    Hh.assert_close_bf16(got, ref)
+    assert np.abs(lse - ref_lse).max() < 1e-3
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_d128_out_dtypes_and_scales(out_dtype):
+    q, k, v = Hh.host_inputs(1, 200, 333, 2, D, seed=42)
+    for scale in (1.0 / 16, 0.0, -0.05):
+        ref, ref_lse = O.mha_forward(q, k, v, scale)
+        got, lse = _run(q, k, v, scale=scale, out_dtype=out_dtype)
+        Hh.assert_close_bf16(got, ref)
+        assert np.abs(lse - ref_lse).max() < 1e-3
+
+
+def test_d128_monotone_scores_rescale_every_tile():
+    n = 900
+    u = np.zeros(D); u[0] = 1.0
+    k = (np.arange(n)[:, None] / n * 8.0) * u[None, :]
+    q = np.tile(8.0 * u, (5, 1))
+    v = Hh.host_inputs(1, 1, n, 1, D, seed=43)[2][0, :, 0]
+    k_b = torch.tensor(k).bfloat16().double().numpy()
+    ref, _ = O.naive(q, k_b, v, 1.0)
+    got, _ = _run(q[None, :, None], k_b[None, :, None], v[None, :, None], scale=1.0)
+    Hh.assert_close_bf16(got[0, :, 0], ref)
+
+
+def test_d128_long_sequence_sampled_rows():
+    """n = 16384 (configs[2]'s length), H = 8, d = 128: full launch, sampled rows vs O1."""
+    from paper_2112_05682_b200 import api
+    from synth import gen
+    B, n, H = 1, 16384, 8
+    q = torch.empty((B, n, H, D), dtype=torch.bfloat16, device="cuda")
+    k, v = torch.empty_like(q), torch.empty_like(q)
+    for t, tid in ((q, gen.TENSOR_Q), (k, gen.TENSOR_K), (v, gen.TENSOR_V)):
+        api.mea_fill_synthetic(t, 0, tid)
+    out, lse = api.mea_attention_fwd(q, k, v, want_lse=True)
+    torch.cuda.synchronize()
+    rows = np.array([0, 127, 128, 9999, 16383])
+    kk = gen.normal_tensor((B, n, H, D), 0, gen.TENSOR_K, "bf16").astype(np.float64)
+    vv = gen.normal_tensor((B, n, H, D), 0, gen.TENSOR_V, "bf16").astype(np.float64)
+    for h in (0, 7):
+        qr = gen.rows_of((B, n, H, D), 0, gen.TENSOR_Q, 0, rows, h)
+        ref, ref_lse = O.naive(qr, kk[0, :, h], vv[0, :, h], 1 / math.sqrt(D))
+        Hh.assert_close_bf16(out[0, rows, h].double().cpu().numpy(), ref)
+        assert np.abs(lse[0, h, rows].double().cpu().numpy() - ref_lse).max() < 1e-3
+
+
+def test_d128_unsupported_paths_fail_loudly():
+    from paper_2112_05682_b200 import api
+    q = torch.zeros(1, 256, 1, D, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(api.MeaError):
+        api.mea_attention_fwd(q, q, q, k_chunk=128)            # key chunks: d = 64 only
+    with pytest.raises(api.MeaError):
+        api.mea_attention_fwd_causal(q, q, q)                 # causal: d = 64 only
+    out, lse = api.mea_attention_fwd(q, q, q, want_lse=True)
+    with pytest.raises(api.MeaError):
+        api.mea_attention_bwd(q, q, q, out, q, lse=lse)       # backward: d = 64 only
