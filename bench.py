@@ -326,6 +326,19 @@ def main():
         fl128 = 4 * n * n * 128 * Hl * Bl
         extras["fwd_d128"] = {"ms": f128_ms, "tflops": fl128 / (f128_ms * 1e-3) / 1e12,
                               "frac": fl128 / (f128_ms * 1e-3) / 1e12 / pk["tflops"], "kernel": "fwd128_bf16"}
+        if not a.fwd_only:
+            do128 = torch.empty_like(q128)
+            api.mea_fill_synthetic(do128, a.seed, gen.TENSOR_DO, offset=rank * do128.numel())
+            g128 = [torch.empty_like(q128) for _ in range(3)]
+            ws128 = torch.empty(api.mea_attention_bwd_workspace_size(Bl, Hl, n, n, 128, api.MEA_BF16, True),
+                                dtype=torch.uint8, device=dev)
+            b128_ms = statistics.mean(timed(lambda: api.mea_attention_bwd(
+                q128, k128, v128, o128, do128, lse=l128, dq=g128[0], dk=g128[1], dv=g128[2], workspace=ws128),
+                max(3, a.steps // 2), 1))
+            extras["bwd_d128"] = {"ms": b128_ms, "tflops": 2.5 * fl128 / (b128_ms * 1e-3) / 1e12,
+                                  "frac": 2.5 * fl128 / (b128_ms * 1e-3) / 1e12 / pk["tflops"],
+                                  "kernels": "bwd_dkdv<128> (64-query tiles) + bwd_dq<128>"}
+            del do128, g128, ws128
         del q128, k128, v128, o128, l128
     # ---------------- the paper's literal schedule (query chunk 1024 / key chunk 4096)
     if a.workload == "cfg3":

@@ -32,30 +32,37 @@ namespace mea {
 namespace {
 
 constexpr int kBStages = 3;  // Q/dO ring
-constexpr int kTile = 128;
-constexpr int kTileBytes = kTile * kHeadDim * 2;  // 16 KiB bf16 tile
+constexpr int kTile = 128;     // keys per CTA
 constexpr int kBThreads = 640;
+// D = 64 (kHeadDim) or 128. Query tiles are QT = 128 rows at D = 64 and 64 rows at D = 128 (so
+// that Sᵀ, dPᵀ, Pᵀ, dSᵀ, dV and dK fit the 512 TMEM columns: 2 QT + QT + 2 D <= 512). A tile of
+// R rows and D columns is D/64 SW128 atoms of R x 128 B.
+template <int D> struct DkvCfg {
+  static constexpr int QT = D == 64 ? 128 : 64;
+  static constexpr int kAtoms = D / 64;
+  static constexpr int kKTileBytes = 128 * D * 2, kQTileBytes = QT * D * 2;
+  static constexpr int kKAtom = 128 * 128, kQAtom = QT * 128;
+  static constexpr uint32_t kColST = 0, kColDPT = QT, kColP = 2 * QT, kColDS = 2 * QT + QT / 2,
+                            kColDV = 3 * QT, kColDK = 3 * QT + D;
+};
 // setmaxnreg budgets. Measured on B200: setmaxnreg.inc only redistributes the registers the
 // CTA was launched with (640 threads x 96 = 480 per lane slot of each SM sub-partition, which
 // holds one control and four softmax warps); a larger total blocks forever. 64 + 4*104 = 480.
 constexpr int kBCtrlRegs = 64, kBSoftRegs = 104;
-constexpr uint32_t kColST = 0, kColDPT = 128, kColP = 256, kColDS = 320, kColDV = 384, kColDK = 448;
-
-constexpr uint32_t kIdSS = idesc_bf16_f32(128, 128, false, false);  // ST, dPT
-constexpr uint32_t kIdTS = idesc_bf16_f32(128, 64, false, true);    // dV, dK: A from TMEM, B MN-major
-
+template <int D>
 struct BwdSmem {
-  uint8_t k[kTileBytes];
-  uint8_t v[kTileBytes];
-  uint8_t q[kBStages][kTileBytes];
-  uint8_t dout[kBStages][kTileBytes];
-  float lse2[kBStages][kTile];
-  float delta[kBStages][kTile];
+  using C = DkvCfg<D>;
+  uint8_t k[C::kKTileBytes];
+  uint8_t v[C::kKTileBytes];
+  uint8_t q[kBStages][C::kQTileBytes];
+  uint8_t dout[kBStages][C::kQTileBytes];
+  float lse2[kBStages][C::QT];
+  float delta[kBStages][C::QT];
   uint64_t kv_full, qdo_full[kBStages], qdo_empty[kBStages];
   uint64_t s_full, s_loaded, p_full, p_free, dkv_done;
   uint32_t tmem_base;
 };
-constexpr size_t kBwdSmemBytes = sizeof(BwdSmem) + 1024;
+template <int D> constexpr size_t dkv_smem_bytes() { return sizeof(BwdSmem<D>) + 1024; }
 
 // 1024-byte alignment (128B-swizzle atoms) by pointer arithmetic on the __shared__ array, so
 // the compiler keeps the shared address space (LDS/STS instead of generic LD/ST).
@@ -72,17 +79,25 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+template <int D>
 __global__ void __launch_bounds__(kBThreads, 1)
     bwd_dkdv_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                     const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
                     const BwdParams p) {
+  using C = DkvCfg<D>;
+  constexpr int QT = C::QT, kAtoms = C::kAtoms;
+  constexpr uint32_t kColST = C::kColST, kColDPT = C::kColDPT, kColP = C::kColP, kColDS = C::kColDS,
+                     kColDV = C::kColDV, kColDK = C::kColDK;
+  constexpr uint32_t kIdSS = idesc_bf16_f32(128, QT, false, false);  // ST, dPT: N = QT queries
+  constexpr uint32_t kIdTS = idesc_bf16_f32(128, D, false, true);    // dV, dK: A from TMEM, B MN-major
+  constexpr int NC = QT / 4;                                          // query columns per softmax thread
   extern __shared__ uint8_t smem_raw[];
-  BwdSmem& sm = *reinterpret_cast<BwdSmem*>(align1024(smem_raw));
+  BwdSmem<D>& sm = *reinterpret_cast<BwdSmem<D>*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int k0 = kblk * kTile;
-  const int NQ = (p.n_q + kTile - 1) / kTile;
-  const int nq_pad = NQ * kTile;
+  const int NQ = (p.n_q + QT - 1) / QT;
+  const int nq_pad = (p.n_q + kTileM - 1) / kTileM * kTileM;  // bwd_preprocess's row padding
   const size_t bh = (size_t)b * p.H + h;
 
   if (threadIdx.x == 0) {
@@ -116,20 +131,26 @@ __global__ void __launch_bounds__(kBThreads, 1)
       // ---------------------------------------------------------------- TMA producer
       const uint64_t keep = policy_evict_last();
       if (elect_one()) {
-        mbar_arrive_expect_tx(&sm.kv_full, 2 * kTileBytes);
-        tma_load_4d(sm.k, &mk, &sm.kv_full, 0, h, k0, b, keep);
-        tma_load_4d(sm.v, &mv, &sm.kv_full, 0, h, k0, b, keep);
+        mbar_arrive_expect_tx(&sm.kv_full, 2 * C::kKTileBytes);
+#pragma unroll
+        for (int a = 0; a < kAtoms; ++a) {
+          tma_load_4d(sm.k + a * C::kKAtom, &mk, &sm.kv_full, 64 * a, h, k0, b, keep);
+          tma_load_4d(sm.v + a * C::kKAtom, &mv, &sm.kv_full, 64 * a, h, k0, b, keep);
+        }
       }
       __syncwarp();
       for (int i = 0; i < NQ; ++i) {
         const int st = i % kBStages, n = i / kBStages;
         if (i >= kBStages) mbar_wait(&sm.qdo_empty[st], (n - 1) & 1);
         if (elect_one()) {
-          mbar_arrive_expect_tx(&sm.qdo_full[st], 2 * kTileBytes + 2 * kTile * 4);
-          tma_load_4d(sm.q[st], &mq, &sm.qdo_full[st], 0, h, i * kTile, b, keep);
-          tma_load_4d(sm.dout[st], &mdo, &sm.qdo_full[st], 0, h, i * kTile, b, keep);
-          bulk_load(sm.lse2[st], p.lse2 + bh * nq_pad + i * kTile, kTile * 4, &sm.qdo_full[st]);
-          bulk_load(sm.delta[st], p.delta + bh * nq_pad + i * kTile, kTile * 4, &sm.qdo_full[st]);
+          mbar_arrive_expect_tx(&sm.qdo_full[st], 2 * C::kQTileBytes + 2 * QT * 4);
+#pragma unroll
+          for (int a = 0; a < kAtoms; ++a) {
+            tma_load_4d(sm.q[st] + a * C::kQAtom, &mq, &sm.qdo_full[st], 64 * a, h, i * QT, b, keep);
+            tma_load_4d(sm.dout[st] + a * C::kQAtom, &mdo, &sm.qdo_full[st], 64 * a, h, i * QT, b, keep);
+          }
+          bulk_load(sm.lse2[st], p.lse2 + bh * nq_pad + i * QT, QT * 4, &sm.qdo_full[st]);
+          bulk_load(sm.delta[st], p.delta + bh * nq_pad + i * QT, QT * 4, &sm.qdo_full[st]);
         }
         __syncwarp();
       }
@@ -139,14 +160,19 @@ __global__ void __launch_bounds__(kBThreads, 1)
       const uint64_t dV = shfl0_u64(sdesc_sw128(smem_u32(sm.v), 16, 1024));
       const uint64_t dQ0 = shfl0_u64(sdesc_sw128(smem_u32(sm.q[0]), 16, 1024));
       const uint64_t dO0 = shfl0_u64(sdesc_sw128(smem_u32(sm.dout[0]), 16, 1024));
-      constexpr uint64_t kStep = kTileBytes >> 4;
+      // Q / dO as the MN-major B of dV, dK: N = D over kAtoms atoms C::kQAtom bytes apart (LBO)
+      const uint64_t dQm0 = shfl0_u64(sdesc_sw128(smem_u32(sm.q[0]), C::kQAtom, 1024));
+      const uint64_t dOm0 = shfl0_u64(sdesc_sw128(smem_u32(sm.dout[0]), C::kQAtom, 1024));
+      constexpr uint64_t kStep = C::kQTileBytes >> 4, kKAt = C::kKAtom >> 4, kQAt = C::kQAtom >> 4;
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
-      auto scores = [&](int st) {  // ST = K Q^T ; dPT = V dO^T
+      auto scores = [&](int st) {  // ST = K Q^T ; dPT = V dO^T  (K = D in steps of 16)
         const uint64_t q = dQ0 + st * kStep, o = dO0 + st * kStep;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) umma_ss(tm + kColST, dK + kk * 2, q + kk * 2, kIdSS, kk > 0);
+        for (int kk = 0; kk < 4 * kAtoms; ++kk)
+          umma_ss(tm + kColST, dK + (kk >> 2) * kKAt + (kk & 3) * 2, q + (kk >> 2) * kQAt + (kk & 3) * 2, kIdSS, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) umma_ss(tm + kColDPT, dV + kk * 2, o + kk * 2, kIdSS, kk > 0);
+        for (int kk = 0; kk < 4 * kAtoms; ++kk)
+          umma_ss(tm + kColDPT, dV + (kk >> 2) * kKAt + (kk & 3) * 2, o + (kk >> 2) * kQAt + (kk & 3) * 2, kIdSS, kk > 0);
       };
       mbar_wait(&sm.kv_full, 0);
       mbar_wait(&sm.qdo_full[0], 0);
@@ -172,13 +198,13 @@ __global__ void __launch_bounds__(kBThreads, 1)
         mbar_wait(&sm.p_full, i & 1);
         tc_fence_after();
         if (elect_one()) {
-          const uint64_t q = dQ0 + st * kStep, o = dO0 + st * kStep;
-          // dV += PT dO ; dK += dST Q : K = 128 queries in steps of 16 (A: 8 TMEM columns per
+          const uint64_t q = dQm0 + st * kStep, o = dOm0 + st * kStep;
+          // dV += PT dO ; dK += dST Q : K = QT queries in steps of 16 (A: 8 TMEM columns per
           // step; B: 16 rows of 128 B, MN-major)
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) umma_ts(tm + kColDV, tm + kColP + kk * 8, o + kk * 128, kIdTS, (i > 0 || kk > 0));
+          for (int kk = 0; kk < QT / 16; ++kk) umma_ts(tm + kColDV, tm + kColP + kk * 8, o + kk * 128, kIdTS, (i > 0 || kk > 0));
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) umma_ts(tm + kColDK, tm + kColDS + kk * 8, q + kk * 128, kIdTS, (i > 0 || kk > 0));
+          for (int kk = 0; kk < QT / 16; ++kk) umma_ts(tm + kColDK, tm + kColDS + kk * 8, q + kk * 128, kIdTS, (i > 0 || kk > 0));
           umma_commit(&sm.p_free);
           umma_commit(&sm.qdo_empty[st]);
           if (!more) umma_commit(&sm.dkv_done);
@@ -189,7 +215,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
   } else {
     setmaxnreg_inc<kBSoftRegs>();
     // ------------------------------------------------------------------ softmax warpgroups
-    const int g = (warp - 4) >> 2;           // query columns [32g, 32g+32)
+    const int g = (warp - 4) >> 2;           // query columns [NC g, NC g + NC)
     const int quarter = warp & 3;
     const int j = quarter * 32 + lane;       // key row within the tile (TMEM lane)
     const bool key_ok = k0 + j < p.n_k;
@@ -209,17 +235,22 @@ __global__ void __launch_bounds__(kBThreads, 1)
       mbar_wait(&sm.s_full, i & 1);
       TPROBE(1)
       tc_fence_after();
-      uint32_t sr[32], dr[32];
-      tmem_ld32(lane_base + kColST + g * 32, sr);
-      tmem_ld32(lane_base + kColDPT + g * 32, dr);
+      uint32_t sr[NC], dr[NC];
+      if constexpr (NC == 32) {
+        tmem_ld32(lane_base + kColST + g * NC, sr);
+        tmem_ld32(lane_base + kColDPT + g * NC, dr);
+      } else {
+        tmem_ld16(lane_base + kColST + g * NC, sr);
+        tmem_ld16(lane_base + kColDPT + g * NC, dr);
+      }
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&sm.s_loaded);  // ST_i / dPT_i are in registers: the next scores may overwrite
-      const float* l2 = sm.lse2[st] + g * 32;
-      const float* dl = sm.delta[st] + g * 32;
-      uint32_t pk[16], dk[16];
+      const float* l2 = sm.lse2[st] + g * NC;
+      const float* dl = sm.delta[st] + g * NC;
+      uint32_t pk[NC / 2], dk[NC / 2];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
+      for (int u = 0; u < NC / 2; ++u) {
         const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
         const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
         const float2 lq = *reinterpret_cast<const float2*>(l2 + 2 * u);
@@ -235,19 +266,27 @@ __global__ void __launch_bounds__(kBThreads, 1)
       if (i > 0) mbar_wait(&sm.p_free, (i - 1) & 1);  // dV_{i-1}, dK_{i-1} no longer read PT / dST
       TPROBE(3)
       tc_fence_after();
-      tmem_st16(lane_base + kColP + g * 16, pk);
-      tmem_st16(lane_base + kColDS + g * 16, dk);
+      if constexpr (NC == 32) {
+        tmem_st16(lane_base + kColP + g * 16, pk);
+        tmem_st16(lane_base + kColDS + g * 16, dk);
+      } else {
+        tmem_st8(lane_base + kColP + g * 8, pk);
+        tmem_st8(lane_base + kColDS + g * 8, dk);
+      }
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm.p_full);
       TPROBE(4)
     }
     // ------------------------------------------------------------------ dV, dK epilogue
-    if (g < 2) {
+    // warpgroup g writes 64 columns: D = 64: g 0 dV, g 1 dK; D = 128: g 0, 1 dV, g 2, 3 dK
+    if (g < 2 * kAtoms) {
       mbar_wait(&sm.dkv_done, 0);
       tc_fence_after();
       uint32_t r[64];
-      const uint32_t col = (g == 0) ? kColDV : kColDK;
+      const bool is_dv = g < kAtoms;
+      const int cpart = g % kAtoms;
+      const uint32_t col = (is_dv ? kColDV : kColDK) + cpart * 64;
       tmem_ld32(lane_base + col, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
       tmem_ld32(lane_base + col + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
       tmem_ld_wait();
@@ -256,9 +295,9 @@ __global__ void __launch_bounds__(kBThreads, 1)
 #else
       if (key_ok) {
 #endif
-        const float sc = (g == 0) ? 1.f : p.scale;
-        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(g == 0 ? p.dv : p.dk) +
-                             (((size_t)b * p.n_k + k0 + j) * p.H + h) * kHeadDim;
+        const float sc = is_dv ? 1.f : p.scale;
+        __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(is_dv ? p.dv : p.dk) +
+                             (((size_t)b * p.n_k + k0 + j) * p.H + h) * D + cpart * 64;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           uint4 w;
@@ -281,14 +320,21 @@ __global__ void __launch_bounds__(kBThreads, 1)
 
 }  // namespace
 
-cudaError_t launch_bwd_dkdv(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                            const CUtensorMap& mdo, cudaStream_t s) {
-  static cudaError_t attr =
-      cudaFuncSetAttribute(bwd_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmemBytes);
+template <int D>
+static cudaError_t launch_bwd_dkdv_d(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
+                                     const CUtensorMap& mv, const CUtensorMap& mdo, cudaStream_t s) {
+  static cudaError_t attr = cudaFuncSetAttribute(bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)dkv_smem_bytes<D>());
   if (attr != cudaSuccess) return attr;
   dim3 grid(p.num_k_blocks, p.H, p.B);
-  bwd_dkdv_kernel<<<grid, kBThreads, kBwdSmemBytes, s>>>(mq, mk, mv, mdo, p);
+  bwd_dkdv_kernel<D><<<grid, kBThreads, dkv_smem_bytes<D>(), s>>>(mq, mk, mv, mdo, p);
   return cudaGetLastError();
+}
+
+// mq / mdo: boxes of DkvCfg<D>::QT rows (128 at D = 64, 64 at D = 128)
+cudaError_t launch_bwd_dkdv(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                            const CUtensorMap& mdo, cudaStream_t s) {
+  return p.d == 128 ? launch_bwd_dkdv_d<128>(p, mq, mk, mv, mdo, s) : launch_bwd_dkdv_d<64>(p, mq, mk, mv, mdo, s);
 }
 
 }  // namespace mea

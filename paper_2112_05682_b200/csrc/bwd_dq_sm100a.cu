@@ -26,18 +26,23 @@
 namespace mea {
 namespace {
 
-constexpr int kQStages = 4;
+// D = 64 (kHeadDim) or 128. A tile of 128 rows is D/64 SW128 atoms (128 rows x 128 B) wide.
+template <int D> struct DqCfg {
+  static constexpr int kAtoms = D / 64;
+  static constexpr int kTileBytes = 128 * D * 2;
+  static constexpr int kStages = D == 64 ? 4 : 2;  // K/V ring (smem: Q, dO resident)
+};
 constexpr int kTile = 128;
-constexpr int kTileBytes = kTile * kHeadDim * 2;
+constexpr int kAtomBytes = 128 * 128;
 constexpr int kQThreads = 640;
 constexpr int kQCtrlRegs = 64, kQSoftRegs = 104;  // 64 + 4*104 = 480 = launch budget per lane slot
-constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256;
-__device__ __forceinline__ uint32_t col_ds(int buf) { return buf ? 384u : 320u; }  // dS double buffer
+constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256;  // dQ: D columns
 
 constexpr uint32_t kIdSS = idesc_bf16_f32(128, 128, false, false);  // S, dP
-constexpr uint32_t kIdDQ = idesc_bf16_f32(128, 64, false, true);    // A = dS (TMEM), B = K MN-major
 
+template <int D>
 struct DqSmem {
+  static constexpr int kTileBytes = DqCfg<D>::kTileBytes, kQStages = DqCfg<D>::kStages;
   uint8_t q[kTileBytes];
   uint8_t dout[kTileBytes];
   uint8_t k[kQStages][kTileBytes];
@@ -46,18 +51,23 @@ struct DqSmem {
   uint64_t s_full, s_loaded, p_full, ds_free[2], o_done;
   uint32_t tmem_base;
 };
-constexpr size_t kDqSmemBytes = sizeof(DqSmem) + 1024;
+template <int D> constexpr size_t dq_smem_bytes() { return sizeof(DqSmem<D>) + 1024; }
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
 
+template <int D>
 __global__ void __launch_bounds__(kQThreads, 1)
     bwd_dq_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
                   const BwdParams p) {
+  auto col_ds = [](int buf) { return kColDQ + D + buf * 64u; };  // dS double buffer after dQ
+  constexpr int kAtoms = DqCfg<D>::kAtoms, kTileBytes = DqCfg<D>::kTileBytes, kQStages = DqCfg<D>::kStages;
+  // dQ += dS K: N = D; B = K MN-major, N over kAtoms atoms 16 KiB apart (LBO)
+  constexpr uint32_t kIdDQ = idesc_bf16_f32(128, D, false, true);
   extern __shared__ uint8_t smem_raw[];
-  DqSmem& sm = *reinterpret_cast<DqSmem*>(align1024(smem_raw));
+  DqSmem<D>& sm = *reinterpret_cast<DqSmem<D>*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int q0 = qblk * kTile;
@@ -98,8 +108,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const uint64_t keep = policy_evict_last(), once = policy_evict_first();
       if (elect_one()) {
         mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
-        tma_load_4d(sm.q, &mq, &sm.q_full, 0, h, q0, b, once);
-        tma_load_4d(sm.dout, &mdo, &sm.q_full, 0, h, q0, b, once);
+#pragma unroll
+        for (int a = 0; a < kAtoms; ++a) {
+          tma_load_4d(sm.q + a * kAtomBytes, &mq, &sm.q_full, 64 * a, h, q0, b, once);
+          tma_load_4d(sm.dout + a * kAtomBytes, &mdo, &sm.q_full, 64 * a, h, q0, b, once);
+        }
       }
       __syncwarp();
       for (int t = 0; t < T; ++t) {
@@ -107,8 +120,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
         if (t >= kQStages) mbar_wait(&sm.kv_empty[st], (n - 1) & 1);
         if (elect_one()) {
           mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTileBytes);
-          tma_load_4d(sm.k[st], &mk, &sm.kv_full[st], 0, h, t * kTile, b, keep);
-          tma_load_4d(sm.v[st], &mv, &sm.kv_full[st], 0, h, t * kTile, b, keep);
+#pragma unroll
+          for (int a = 0; a < kAtoms; ++a) {
+            tma_load_4d(sm.k[st] + a * kAtomBytes, &mk, &sm.kv_full[st], 64 * a, h, t * kTile, b, keep);
+            tma_load_4d(sm.v[st] + a * kAtomBytes, &mv, &sm.kv_full[st], 64 * a, h, t * kTile, b, keep);
+          }
         }
         __syncwarp();
       }
@@ -118,14 +134,21 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const uint64_t dOd = shfl0_u64(sdesc_sw128(smem_u32(sm.dout), 16, 1024));
       const uint64_t dK0 = shfl0_u64(sdesc_sw128(smem_u32(sm.k[0]), 16, 1024));
       const uint64_t dV0 = shfl0_u64(sdesc_sw128(smem_u32(sm.v[0]), 16, 1024));
-      constexpr uint64_t kStep = kTileBytes >> 4;
+      const uint64_t dKm0 = shfl0_u64(sdesc_sw128(smem_u32(sm.k[0]), kAtomBytes, 1024));  // MN-major view
+      constexpr uint64_t kStep = kTileBytes >> 4, kAtomStep = kAtomBytes >> 4;
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       auto scores = [&](int st) {  // S = Q K^T ; dP = dO V^T
         const uint64_t kd = dK0 + st * kStep, vd = dV0 + st * kStep;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) umma_ss(tm + kColS, dQd + kk * 2, kd + kk * 2, kIdSS, kk > 0);
+        for (int kk = 0; kk < 4 * kAtoms; ++kk) {
+          const uint64_t off = (kk >> 2) * kAtomStep + (kk & 3) * 2;
+          umma_ss(tm + kColS, dQd + off, kd + off, kIdSS, kk > 0);
+        }
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) umma_ss(tm + kColDP, dOd + kk * 2, vd + kk * 2, kIdSS, kk > 0);
+        for (int kk = 0; kk < 4 * kAtoms; ++kk) {
+          const uint64_t off = (kk >> 2) * kAtomStep + (kk & 3) * 2;
+          umma_ss(tm + kColDP, dOd + off, vd + off, kIdSS, kk > 0);
+        }
       };
       mbar_wait(&sm.q_full, 0);
       mbar_wait(&sm.kv_full[0], 0);
@@ -152,7 +175,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           // dQ += dS K : K = 128 keys in steps of 16 (dS: 8 TMEM columns; K rows: 2048 B)
-          const uint64_t kd = dK0 + st * kStep;
+          const uint64_t kd = dKm0 + st * kStep;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) umma_ts(tm + kColDQ, tm + col_ds(t & 1) + kk * 8, kd + kk * 128, kIdDQ, (t > 0 || kk > 0));
           umma_commit(&sm.ds_free[t & 1]);
@@ -217,30 +240,34 @@ __global__ void __launch_bounds__(kQThreads, 1)
       TPROBE(5)
     }
     // ------------------------------------------------------------------ epilogue: dq = scale dQ
+    // thread (colhalf, lane half) writes dQ columns colhalf * D/2 + (lane >> 4) * D/4 + [0, D/4)
     mbar_wait(&sm.o_done, 0);
     tc_fence_after();
-    uint32_t o[16];
-    tmem_ld16_split<16>(lane_base + kColDQ + colhalf * 32, o);
+    constexpr int kW = D / 4;  // columns per thread
+    uint32_t o[kW];
+    if constexpr (D == 64) {
+      tmem_ld16_split<16>(lane_base + kColDQ + colhalf * 32, o);
+    } else {
+      tmem_ld32_split<32>(lane_base + kColDQ + colhalf * 64, o);
+    }
     tmem_ld_wait();
 #ifdef MEA_EXP_TIMING
     if (false) {
 #else
     if (row < p.n_q) {
 #endif
-      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.dq) +
-                           (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + colhalf * 32 + (lane >> 4) * 16;
-      uint4 w0, w1;
+      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.dq) + (((size_t)b * p.n_q + row) * p.H + h) * D +
+                           colhalf * (D / 2) + (lane >> 4) * kW;
       const float sc = p.scale;
-      w0.x = pack_bf16x2(__uint_as_float(o[0]) * sc, __uint_as_float(o[1]) * sc);
-      w0.y = pack_bf16x2(__uint_as_float(o[2]) * sc, __uint_as_float(o[3]) * sc);
-      w0.z = pack_bf16x2(__uint_as_float(o[4]) * sc, __uint_as_float(o[5]) * sc);
-      w0.w = pack_bf16x2(__uint_as_float(o[6]) * sc, __uint_as_float(o[7]) * sc);
-      w1.x = pack_bf16x2(__uint_as_float(o[8]) * sc, __uint_as_float(o[9]) * sc);
-      w1.y = pack_bf16x2(__uint_as_float(o[10]) * sc, __uint_as_float(o[11]) * sc);
-      w1.z = pack_bf16x2(__uint_as_float(o[12]) * sc, __uint_as_float(o[13]) * sc);
-      w1.w = pack_bf16x2(__uint_as_float(o[14]) * sc, __uint_as_float(o[15]) * sc);
-      reinterpret_cast<uint4*>(dst)[0] = w0;
-      reinterpret_cast<uint4*>(dst)[1] = w1;
+#pragma unroll
+      for (int i = 0; i < kW / 8; ++i) {
+        uint4 w;
+        w.x = pack_bf16x2(__uint_as_float(o[8 * i + 0]) * sc, __uint_as_float(o[8 * i + 1]) * sc);
+        w.y = pack_bf16x2(__uint_as_float(o[8 * i + 2]) * sc, __uint_as_float(o[8 * i + 3]) * sc);
+        w.z = pack_bf16x2(__uint_as_float(o[8 * i + 4]) * sc, __uint_as_float(o[8 * i + 5]) * sc);
+        w.w = pack_bf16x2(__uint_as_float(o[8 * i + 6]) * sc, __uint_as_float(o[8 * i + 7]) * sc);
+        reinterpret_cast<uint4*>(dst)[i] = w;
+      }
     }
   }
   tc_fence_before();
@@ -253,14 +280,20 @@ __global__ void __launch_bounds__(kQThreads, 1)
 
 }  // namespace
 
-cudaError_t launch_bwd_dq(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                          const CUtensorMap& mdo, cudaStream_t s) {
+template <int D>
+static cudaError_t launch_bwd_dq_d(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
+                                   const CUtensorMap& mv, const CUtensorMap& mdo, cudaStream_t s) {
   static cudaError_t attr =
-      cudaFuncSetAttribute(bwd_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDqSmemBytes);
+      cudaFuncSetAttribute(bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dq_smem_bytes<D>());
   if (attr != cudaSuccess) return attr;
   dim3 grid((p.n_q + kTile - 1) / kTile, p.H, p.B);
-  bwd_dq_kernel<<<grid, kQThreads, kDqSmemBytes, s>>>(mq, mk, mv, mdo, p);
+  bwd_dq_kernel<D><<<grid, kQThreads, dq_smem_bytes<D>(), s>>>(mq, mk, mv, mdo, p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_dq(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                          const CUtensorMap& mdo, cudaStream_t s) {
+  return p.d == 128 ? launch_bwd_dq_d<128>(p, mq, mk, mv, mdo, s) : launch_bwd_dq_d<64>(p, mq, mk, mv, mdo, s);
 }
 
 }  // namespace mea

@@ -417,7 +417,7 @@ __device__ __forceinline__ uint32_t bf16_hi_lo(float x) {
 __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ dout,
                                       const float* __restrict__ lse, float* __restrict__ delta,
                                       float* __restrict__ lse2, float* __restrict__ dq_acc, uint8_t* __restrict__ aug,
-                                      float scale, int B, int H, int n_q, int nq_pad) {
+                                      float scale, int B, int H, int n_q, int nq_pad, int d) {
   const int64_t rows = (int64_t)B * H * nq_pad;
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
   const int part = threadIdx.x & 7;
@@ -427,19 +427,21 @@ __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ out, con
   const int64_t b = bh / H, h = bh % H;
   float acc = 0.f;
   if (q < n_q) {
-    const size_t off = (((size_t)b * n_q + q) * H + h) * kHeadDim + part * 8;
-    const uint4 o = *reinterpret_cast<const uint4*>(out + off);
-    const uint4 d = *reinterpret_cast<const uint4*>(dout + off);
-    const uint32_t ow[4] = {o.x, o.y, o.z, o.w}, dw[4] = {d.x, d.y, d.z, d.w};
+    for (int c = 0; c < d; c += 64) {  // d = 64 or 128: 8 (16) elements per thread
+      const size_t off = (((size_t)b * n_q + q) * H + h) * d + c + part * 8;
+      const uint4 o = *reinterpret_cast<const uint4*>(out + off);
+      const uint4 dd = *reinterpret_cast<const uint4*>(dout + off);
+      const uint32_t ow[4] = {o.x, o.y, o.z, o.w}, dw[4] = {dd.x, dd.y, dd.z, dd.w};
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      acc = fmaf(__uint_as_float(ow[u] << 16), __uint_as_float(dw[u] << 16), acc);
-      acc = fmaf(__uint_as_float(ow[u] & 0xFFFF0000u), __uint_as_float(dw[u] & 0xFFFF0000u), acc);
-    }
-    if (dq_acc) {
-      float4* z = reinterpret_cast<float4*>(dq_acc + off);
-      z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-      z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < 4; ++u) {
+        acc = fmaf(__uint_as_float(ow[u] << 16), __uint_as_float(dw[u] << 16), acc);
+        acc = fmaf(__uint_as_float(ow[u] & 0xFFFF0000u), __uint_as_float(dw[u] & 0xFFFF0000u), acc);
+      }
+      if (dq_acc) {
+        float4* z = reinterpret_cast<float4*>(dq_acc + off);
+        z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+        z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
     }
   }
   acc += __shfl_xor_sync(0xffffffffu, acc, 1);
@@ -474,12 +476,13 @@ __global__ void dq_convert_kernel(const float4* __restrict__ acc, uint2* __restr
 }  // namespace
 
 cudaError_t launch_bwd_preprocess(const void* out, const void* dout, const float* lse, float* delta, float* lse2,
-                                  float* dq_acc, uint8_t* aug, float scale, int B, int H, int n_q, cudaStream_t s) {
+                                  float* dq_acc, uint8_t* aug, float scale, int B, int H, int n_q, int d,
+                                  cudaStream_t s) {
   const int nq_pad = (n_q + kTile - 1) / kTile * kTile;
   const int64_t threads = (int64_t)B * H * nq_pad * 8;
   bwd_preprocess_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
       static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), lse, delta, lse2, dq_acc, aug,
-      scale, B, H, n_q, nq_pad);
+      scale, B, H, n_q, nq_pad, d);
   return cudaGetLastError();
 }
 

@@ -32,6 +32,7 @@ struct FwdParams {
 
 struct BwdParams {
   int B, H, n_q, n_k;
+  int d;                   // head dimension: 64, or 128 (two-kernel path only)
   float scale, scale_log2;
   const float* lse2;       // [B*H][nq_pad]: lse * log2(e), +inf in the padding
   const float* delta;      // [B*H][nq_pad]: dO_i . O_i, 0 in the padding
@@ -73,7 +74,8 @@ cudaError_t launch_merge_partials(const float* m, const float* s, const float* v
 // backward
 // dq_acc nullable: zeroed when given (fused path)
 cudaError_t launch_bwd_preprocess(const void* out, const void* dout, const float* lse, float* delta, float* lse2,
-                                  float* dq_acc, uint8_t* aug, float scale, int B, int H, int n_q, cudaStream_t s);
+                                  float* dq_acc, uint8_t* aug, float scale, int B, int H, int n_q, int d,
+                                  cudaStream_t s);
 constexpr int kAugTileBytes = 4096;   // 128 rows x 16 bf16, no-swizzle K-major core matrices
 cudaError_t launch_bwd_bf16(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                             const CUtensorMap& mdo, const CUtensorMap& mdq, cudaStream_t s);

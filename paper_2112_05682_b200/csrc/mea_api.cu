@@ -492,7 +492,8 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   if (causal && scale == 0.f) return fail(MEA_ERR_UNSUPPORTED, "causal backward needs scale != 0");
   if (!valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
   if (n_k == 0) return fail(MEA_ERR_EMPTY_KEYS, "attention over an empty key list");
-  if (dtype != MEA_BF16 || d != kHeadDim) return fail(MEA_ERR_UNSUPPORTED, "backward: bf16 with d == 64");
+  if (dtype != MEA_BF16 || (d != kHeadDim && d != 128)) return fail(MEA_ERR_UNSUPPORTED, "backward: bf16, d in {64, 128}");
+  if (d == 128 && causal) return fail(MEA_ERR_UNSUPPORTED, "causal backward: d == 64 only");
   if (!k || !v || !dk || !dv) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e;
@@ -507,6 +508,7 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   // The fused kernel folds lse/scale into its score MMA; scale == 0 (all scores 0, P uniform)
   // takes the two-kernel path, whose workspace is a prefix-sized subset of the fused one.
   if (fused && scale == 0.f) fused = false;
+  if (d == 128) fused = false;  // d = 128: the two-kernel path (the fused kernel's TMEM holds d = 64)
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(dout) || !aligned16(dq) ||
       !aligned16(dk) || !aligned16(dv))
     return fail(MEA_ERR_MISALIGNED, "tensors must be 16-byte aligned");
@@ -543,8 +545,8 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   }
   {
     ProfScope ps("bwd_preprocess", st);
-    if ((e = launch_bwd_preprocess(out, dout, lse, delta, lse2, dq_acc, aug, scale, (int)B, (int)H, (int)n_q, st)) !=
-        cudaSuccess)
+    if ((e = launch_bwd_preprocess(out, dout, lse, delta, lse2, dq_acc, aug, scale, (int)B, (int)H, (int)n_q, (int)d,
+                                   st)) != cudaSuccess)
       return cuda_fail(e, "bwd_preprocess launch");
   }
   BwdParams p{};
@@ -564,6 +566,7 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   p.dq_acc = dq_acc;
   p.num_k_blocks = (int)((n_k + kTileN - 1) / kTileN);
   p.causal = causal ? 1 : 0;
+  p.d = (int)d;
   if (fused) {
     {
       ProfScope ps("bwd_bf16", st);
@@ -574,8 +577,16 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
       return cuda_fail(e, "dq_convert launch");
   } else {
     {
+      // d = 128: the dK/dV kernel takes 64-query tiles (TMEM), so its Q / dO boxes are 64 rows
+      CUtensorMap mq_t = mq, mdo_t = mdo;
+      if (d == 128 &&
+          ((e = make_bnhd_map(&mq_t, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_q, H, d, 64, 64,
+                              CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+           (e = make_bnhd_map(&mdo_t, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_q, H, d, 64, 64,
+                              CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess))
+        return cuda_fail(e, why);
       ProfScope ps("bwd_dkdv", st);
-      if ((e = launch_bwd_dkdv(p, mq, mk, mv, mdo, st)) != cudaSuccess) return cuda_fail(e, "bwd_dkdv launch");
+      if ((e = launch_bwd_dkdv(p, mq_t, mk, mv, mdo_t, st)) != cudaSuccess) return cuda_fail(e, "bwd_dkdv launch");
     }
     ProfScope ps("bwd_dq", st);
     if ((e = launch_bwd_dq(p, mq, mk, mv, mdo, st)) != cudaSuccess) return cuda_fail(e, "bwd_dq launch");

@@ -1,4 +1,5 @@
-"""GPU parity of the d = 128 forward ("d=64 first; d=128 NEXT"; fwd128_sm100a.cu)
+"""GPU parity of head dimension 128 ("d=64 first; d=128 NEXT"): the forward
+(fwd128_sm100a.cu) and the backward (bwd_det_sm100a.cu / bwd_dq_sm100a.cu at D = 128)
 against the float64 oracle (O1) on the same generated inputs: shapes over several query and key
 tiles with ragged tails, both output dtypes and scales, the rescale stress case, configs[2]'s
 length at d = 128 on sampled rows, and the explicit errors of what d = 128 does not cover.
@@ -84,6 +85,37 @@ def test_d128_unsupported_paths_fail_loudly():
         api.mea_attention_fwd(q, q, q, k_chunk=128)            # key chunks: d = 64 only
     with pytest.raises(api.MeaError):
         api.mea_attention_fwd_causal(q, q, q)                 # causal: d = 64 only
-    out, lse = api.mea_attention_fwd(q, q, q, want_lse=True)
-    with pytest.raises(api.MeaError):
-        api.mea_attention_bwd(q, q, q, out, q, lse=lse)       # backward: d = 64 only
+
+
+@pytest.mark.parametrize("B,n_q,n_k,H,lse_given", [(1, 130, 300, 2, True), (2, 257, 129, 1, True),
+                                                   (1, 1, 1, 1, True), (1, 200, 333, 2, False)])
+def test_d128_backward_matches_oracle(B, n_q, n_k, H, lse_given):
+    """d = 128 backward (two-kernel path: dK/dV on 64-query tiles, dQ on 128-key tiles) vs O6."""
+    from paper_2112_05682_b200 import api
+    q, k, v, do = Hh.host_inputs(B, n_q, n_k, H, D, seed=44, with_dout=True)
+    scale = 1 / math.sqrt(D)
+    dq_r, dk_r, dv_r = O.mha_backward(q, k, v, do, scale)
+    qd, kd, vd, dod = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v, do))
+    out, lse = api.mea_attention_fwd(qd, kd, vd, want_lse=True)
+    for fn in (api.mea_attention_bwd, api.mea_attention_bwd_deterministic):
+        dq, dk, dv = fn(qd, kd, vd, out, dod, lse=lse if lse_given else None)
+        torch.cuda.synchronize()
+        for got, ref, name in ((dq, dq_r, "dq"), (dk, dk_r, "dk"), (dv, dv_r, "dv")):
+            Hh.assert_close_bf16(got.double().cpu().numpy(), ref, abs_tol=Hh.TOL_BF16_GRAD,
+                                 rel_tol=Hh.REL_NORM_GRAD, what=name)
+
+
+def test_d128_backward_sampled_rows_n4096():
+    from paper_2112_05682_b200 import api
+    B, n, H = 1, 4096, 2
+    q, k, v, do = Hh.host_inputs(B, n, n, H, D, seed=45, with_dout=True)
+    qd, kd, vd, dod = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v, do))
+    out, lse = api.mea_attention_fwd(qd, kd, vd, want_lse=True)
+    dq, dk, dv = api.mea_attention_bwd(qd, kd, vd, out, dod, lse=lse)
+    torch.cuda.synchronize()
+    qr, kr = np.array([0, 63, 64, 2049, 4095]), np.array([0, 127, 128, 3000, 4095])
+    for h in range(H):
+        sq, sk, sv = O.backward_rows(q[0, :, h], k[0, :, h], v[0, :, h], do[0, :, h], 1 / math.sqrt(D), qr, kr)
+        for got, ref, name in ((dq[0, qr, h], sq, "dq"), (dk[0, kr, h], sk, "dk"), (dv[0, kr, h], sv, "dv")):
+            Hh.assert_close_bf16(got.double().cpu().numpy(), ref, abs_tol=Hh.TOL_BF16_GRAD,
+                                 rel_tol=Hh.REL_NORM_GRAD, what=name)

@@ -30,7 +30,8 @@ for i in range(ITERS + 2):
         _lib._lib = fns[path]
         dq, dk, dv = grads[path]
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-        e0.record(); api.mea_attention_bwd(q, k, v, out, do, lse=lse, dq=dq, dk=dk, dv=dv); e1.record()
+        fn = api.mea_attention_bwd_deterministic if os.environ.get("DET") == "1" else api.mea_attention_bwd
+        e0.record(); fn(q, k, v, out, do, lse=lse, dq=dq, dk=dk, dv=dv); e1.record()
         torch.cuda.synchronize()
         if i >= 2: res[path].append(e0.elapsed_time(e1))
 ref = [x.float() for x in grads[libs[0]]]
