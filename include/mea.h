@@ -31,8 +31,10 @@
  *      workspace smaller than needed  -> MEA_ERR_WORKSPACE_TOO_SMALL
  *      CUDA launch/encode failure     -> MEA_ERR_CUDA (detail in mea_last_error_detail)
  *  - Non-finite input values are not checked; they propagate.
- *  - Supported: bf16 inputs with d = 64 (tcgen05 tensor-core kernels); f32 inputs with
- *    1 <= d <= 128 (exact-f32 SIMT kernels, forward and single query).
+ *  - Supported: bf16 inputs with d = 64 (all entry points) or d = 128 (mea_attention_fwd
+ *    without key chunks, mea_attention_bwd, mea_attention_bwd_deterministic) on tcgen05
+ *    tensor-core kernels; f32 inputs with 1 <= d <= 128 (exact-f32 SIMT kernels, forward and
+ *    single query).
  */
 #ifndef MEA_H_
 #define MEA_H_
@@ -85,7 +87,8 @@ MEA_API const char* mea_last_error_detail(void);
  *     query chunks does, so only one chunk's summaries are alive:
  *     workspace = splits * B * H * min(n_q, q_chunk') * (d + 2) * 4 bytes. Without a key
  *     split q_chunk has no effect. Results do not depend on q_chunk.
- *   in_dtype MEA_BF16 requires d == 64 and out_dtype in {BF16, F32};
+ *   in_dtype MEA_BF16 requires d in {64, 128} (key chunks: d == 64) and out_dtype in
+ *   {BF16, F32};
  *   in_dtype MEA_F32 requires d <= 128, out_dtype F32 and k_chunk == 0.
  */
 MEA_API mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void* out,
@@ -171,7 +174,8 @@ MEA_API mea_status_t mea_merge_partials(const float* m, const float* s, const fl
  * residual; NULL makes the call recompute it first (one extra statistics pass).
  * The max carries no gradient (stop_gradient).
  * Workspace: delta [B,H,n_q] f32 + dq accumulator [B,n_q,H,d] f32 (+ lse if NULL).
- * bf16 with d == 64 only.
+ * bf16 with d in {64, 128}; d = 128 (and scale == 0) runs the two-kernel path of
+ * mea_attention_bwd_deterministic (the workspace asked for here covers it).
  */
 MEA_API mea_status_t mea_attention_bwd(const void* q, const void* k, const void* v, const void* out,
                                const void* dout, void* dq, void* dk, void* dv, int64_t B,
