@@ -38,9 +38,6 @@ namespace {
 #ifndef MEA_DQBUFS
 #define MEA_DQBUFS 1
 #endif
-#ifndef MEA_BPOLY_MASK
-#define MEA_BPOLY_MASK 0u
-#endif
 constexpr int kBStages = MEA_BSTAGES;       // Q/dO ring
 constexpr int kDqBufs = MEA_DQBUFS;         // dQ staging buffers
 constexpr int kTile = 128;
@@ -299,8 +296,9 @@ __global__ void __launch_bounds__(kBThreads, 1)
         const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
         const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
         const float2 x = __fmul2_rn(s2, c2);  // c (s - lse/scale) = s c - lse log2 e
-        // P (lse2 = +inf pads -> 0); the pairs in MEA_BPOLY_MASK on the FMA pipe unload MUFU
-        float2 pr = (((MEA_BPOLY_MASK) >> u) & 1u) ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+        // P (padded query rows: lse/scale = +-inf -> 0). MUFU for every pair: moving some pairs
+        // to the FMA-pipe polynomial measured +-1 % here (MUFU is not what bounds this kernel).
+        float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));
         if (!key_ok) pr = make_float2(0.f, 0.f);
         if (diag) {  // causal diagonal tile: key j > query (32 g + 2 u + {0, 1}) is masked
           if (j > 32 * g + 2 * u) pr.x = 0.f;
