@@ -84,3 +84,30 @@ def test_host_only_calls(lib):
     assert lib.mea_single_query_fwd(p, p, p, p, 1, 1, 0, 64, 1, 1, 1.0, None, 0, None) == 2
     assert lib.mea_merge_partials(p, p, p, 0, 1, 1, 64, p, 1, None) == 2
     assert b"no partials" in lib.mea_last_error_detail()
+
+
+def test_host_only_validation_of_the_newer_entry_points(lib):
+    """Causal, partial, d = 128 and backward argument checks all happen before any launch."""
+    p = ctypes.c_void_p(16)
+    # causal: bf16 only (status 3 = unsupported); n == 0 is a no-op; n_k == 0 impossible (n_q == n_k)
+    assert lib.mea_attention_fwd_causal(p, p, p, p, 1, 1, 8, 64, 0, 0, 1.0, None, None) == 3
+    assert lib.mea_attention_fwd_causal(p, p, p, p, 1, 1, 0, 64, 1, 1, 1.0, None, None) == 0
+    assert lib.mea_attention_fwd_causal(p, p, p, p, 1, 1, 8, 128, 1, 1, 1.0, None, None) == 3  # d = 128
+    assert lib.mea_attention_bwd_causal(p, p, p, p, p, p, p, p, 1, 1, 8, 64, 1, 0.0, None, None, 0, None) == 3
+    # key chunks at d = 128: unsupported; f32 key chunks: unsupported
+    assert lib.mea_attention_fwd(p, p, p, p, 1, 1, 300, 300, 128, 1, 1, 1.0, None, 0, 128, None, 0, None) == 3
+    assert lib.mea_attention_fwd(p, p, p, p, 1, 1, 300, 300, 64, 0, 0, 1.0, None, 0, 128, None, 0, None) == 3
+    # backward: d outside {64, 128}, f32 inputs
+    assert lib.mea_attention_bwd(p, p, p, p, p, p, p, p, 1, 1, 8, 8, 32, 1, 1.0, None, None, 0, None) == 3
+    assert lib.mea_attention_bwd(p, p, p, p, p, p, p, p, 1, 1, 8, 8, 64, 0, 1.0, None, None, 0, None) == 3
+    # backward workspace too small (status 5) before any launch
+    assert lib.mea_attention_bwd(p, p, p, p, p, p, p, p, 1, 1, 8, 8, 64, 1, 1.0, None, p, 16, None) == 5
+    # partial forward: bf16 d = 64 only; n_q == 0 no-op
+    assert lib.mea_attention_partial_fwd(p, p, p, p, p, p, 1, 1, 8, 8, 128, 1, 1.0, None) == 3
+    assert lib.mea_attention_partial_fwd(p, p, p, p, p, p, 1, 1, 0, 8, 64, 1, 1.0, None) == 0
+    # d = 128 workspace sizes: forward none, backward covers delta, lse2, dq accumulator
+    n = ctypes.c_size_t(7)
+    assert lib.mea_attention_fwd_workspace_size(1, 2, 300, 300, 128, 1, 0, 0, ctypes.byref(n)) == 0
+    assert n.value == 0
+    assert lib.mea_attention_bwd_workspace_size(1, 2, 300, 300, 128, 1, 1, ctypes.byref(n)) == 0
+    assert n.value >= 300 * 2 * 128 * 4
