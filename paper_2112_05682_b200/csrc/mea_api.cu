@@ -477,7 +477,7 @@ mea_status_t mea_attention_bwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
   if (!bytes) return fail(MEA_ERR_INVALID_VALUE, "bytes is NULL");
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
   if (!valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  *bytes = bwd_layout(B, H, n_q, d, lse_given != 0, true).total;
+  *bytes = bwd_layout(B, H, n_q, d, lse_given != 0, d == kHeadDim).total;  // d = 128: two-kernel path
   return MEA_OK;
 }
 

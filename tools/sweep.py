@@ -34,6 +34,64 @@ def peaks():
     return pk["tflops"], pk["hbm_gbs"]
 
 
+def sweep_one(n, lg, d, rows, fill, scratch, timed, peak_tf):
+    """Forward (default and, at d = 64, the paper's chunk schedule) and both backward entry
+    points at B = 1, H = 16, head dimension d."""
+    q, k, v, do = (fill((1, n, H, d), t) for t in (1, 2, 3, 4))
+    dev = q.device
+    out = torch.empty_like(q)
+    lse = torch.empty((1, H, n), dtype=torch.float32, device=dev)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    ffl, bfl = 4.0 * n * n * d * H, 10.0 * n * n * d * H
+    cases = [
+        ("fwd", "default (online, no key split)", ffl, lambda: api.mea_attention_fwd(q, k, v, out=out, lse=lse)),
+        ("bwd", "mea_attention_bwd" + (" (fused, dQ by TMA reduce-add)" if d == 64 else " (two kernels at d = 128)"),
+         bfl, lambda: api.mea_attention_bwd(q, k, v, out, do, lse=lse, dq=dq, dk=dk, dv=dv)),
+        ("bwd", "deterministic (dK/dV + dQ kernels)", bfl,
+         lambda: api.mea_attention_bwd_deterministic(q, k, v, out, do, lse=lse, dq=dq, dk=dk, dv=dv)),
+    ]
+    if d == 64 and n > 4096:
+        cases.insert(1, ("fwd", "paper q_chunk=1024 k_chunk=4096 (key split + merge)", ffl,
+                         lambda: api.mea_attention_fwd(q, k, v, out=out, lse=lse, q_chunk=1024, k_chunk=4096)))
+    api.mea_attention_fwd(q, k, v, out=out, lse=lse)
+    for kind, sched, fl, fn in cases:
+        sb = scratch(fn)
+        med, mn, it = timed(fn, budget_s=1.0 if lg <= 16 else 3.0)
+        tf = fl / (med * 1e-3) / 1e12
+        std = (1 if kind == "fwd" else 2) * n * n * H * 4
+        r = {"op": kind, "schedule": sched, "B": 1, "H": H, "n": n, "d": d, "ms_median": round(med, 4),
+             "ms_min": round(mn, 4), "iters": it, "tflops": round(tf, 1), "pct_peak": round(100 * tf / peak_tf, 1),
+             "scratch_bytes": sb, "standard_attention_scores_bytes": std,
+             "reduction_vs_standard": round(std / sb, 1) if sb else None}
+        rows.append(r)
+        print(json.dumps(r), flush=True)
+    del q, k, v, do, out, lse, dq, dk, dv
+    torch.cuda.empty_cache()
+
+
+def sweep_causal(n, lg, rows, fill, scratch, timed, peak_tf):
+    """Causal forward / backward at d = 64 (flops of the visible pairs, n(n+1)/2 per head)."""
+    q, k, v, do = (fill((1, n, H, D), t) for t in (1, 2, 3, 4))
+    out = torch.empty_like(q)
+    lse = torch.empty((1, H, n), dtype=torch.float32, device=q.device)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+    vis = n * (n + 1) / 2 * D * H
+    api.mea_attention_fwd_causal(q, k, v, out=out, lse=lse)
+    for kind, fl, fn in (("fwd_causal", 4 * vis, lambda: api.mea_attention_fwd_causal(q, k, v, out=out, lse=lse)),
+                         ("bwd_causal", 10 * vis, lambda: api.mea_attention_bwd_causal(q, k, v, out, do, lse=lse, dq=dq,
+                                                                                       dk=dk, dv=dv))):
+        sb = scratch(fn)
+        med, mn, it = timed(fn, budget_s=1.0)
+        tf = fl / (med * 1e-3) / 1e12
+        r = {"op": kind, "schedule": "causal, visible pairs", "B": 1, "H": H, "n": n, "d": D,
+             "ms_median": round(med, 4), "ms_min": round(mn, 4), "iters": it, "tflops": round(tf, 1),
+             "pct_peak": round(100 * tf / peak_tf, 1), "scratch_bytes": sb}
+        rows.append(r)
+        print(json.dumps(r), flush=True)
+    del q, k, v, do, out, lse, dq, dk, dv
+    torch.cuda.empty_cache()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_sweep.json"))
@@ -80,37 +138,10 @@ def main():
     clk.start()
     for lg in range(10, a.max_log2n + 1, 2):
         n = 1 << lg
-        q, k, v, do = (fill((1, n, H, D), t) for t in (1, 2, 3, 4))
-        out = torch.empty_like(q)
-        lse = torch.empty((1, H, n), dtype=torch.float32, device=dev)
-        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-        ffl, bfl = 4.0 * n * n * D * H, 10.0 * n * n * D * H
-        cases = [
-            ("fwd", "default (online, no key split)", ffl,
-             lambda: api.mea_attention_fwd(q, k, v, out=out, lse=lse)),
-            ("fwd", "paper q_chunk=1024 k_chunk=4096 (key split + merge)", ffl,
-             lambda: api.mea_attention_fwd(q, k, v, out=out, lse=lse, q_chunk=1024, k_chunk=4096)),
-            ("bwd", "fused (dQ by TMA reduce-add)", bfl,
-             lambda: api.mea_attention_bwd(q, k, v, out, do, lse=lse, dq=dq, dk=dk, dv=dv)),
-            ("bwd", "deterministic (dK/dV + dQ kernels)", bfl,
-             lambda: api.mea_attention_bwd_deterministic(q, k, v, out, do, lse=lse, dq=dq, dk=dk, dv=dv)),
-        ]
-        api.mea_attention_fwd(q, k, v, out=out, lse=lse)
-        for kind, sched, fl, fn in cases:
-            if "k_chunk" in sched and n <= 4096:
-                continue  # k_chunk >= n_k is the default schedule
-            sb = scratch(fn)
-            med, mn, it = timed(fn, budget_s=1.0 if lg <= 16 else 3.0)
-            tf = fl / (med * 1e-3) / 1e12
-            std = (1 if kind == "fwd" else 2) * n * n * H * 4
-            r = {"op": kind, "schedule": sched, "B": 1, "H": H, "n": n, "d": D, "ms_median": round(med, 4),
-                 "ms_min": round(mn, 4), "iters": it, "tflops": round(tf, 1), "pct_peak": round(100 * tf / peak_tf, 1),
-                 "scratch_bytes": sb, "standard_attention_scores_bytes": std,
-                 "reduction_vs_standard": round(std / sb, 1) if sb else None}
-            rows.append(r)
-            print(json.dumps(r), flush=True)
-        del q, k, v, do, out, lse, dq, dk, dv
-        torch.cuda.empty_cache()
+        sweep_one(n, lg, D, rows, fill, scratch, timed, peak_tf)
+    for lg in range(10, min(a.max_log2n, 16) + 1, 2):   # d = 128 and causal (d = 64) up to 2^16
+        sweep_one(1 << lg, lg, 128, rows, fill, scratch, timed, peak_tf)
+        sweep_causal(1 << lg, lg, rows, fill, scratch, timed, peak_tf)
     for lg in range(16, a.max_log2nk + 1, 2):
         n_k = 1 << lg
         q = fill((1, 1, D), 1)
