@@ -26,27 +26,28 @@
 namespace mea {
 namespace {
 
-// D = 64 (kHeadDim) or 128. A tile of 128 rows is D/64 SW128 atoms (128 rows x 128 B) wide.
+// D = 64 (kHeadDim) or 128. A tile of R rows is D/64 SW128 atoms (R rows x 128 B) wide. Key
+// tiles are KT = 128 keys at D = 64 and 64 keys at D = 128, so that a 4-stage K/V ring fits
+// next to the resident Q and dO (a 2-stage ring of 128-key tiles left the MMA waiting on loads).
 template <int D> struct DqCfg {
   static constexpr int kAtoms = D / 64;
-  static constexpr int kTileBytes = 128 * D * 2;
-  static constexpr int kStages = D == 64 ? 4 : 2;  // K/V ring (smem: Q, dO resident)
+  static constexpr int KT = D == 64 ? 128 : 64;
+  static constexpr int kQTileBytes = 128 * D * 2, kKTileBytes = KT * D * 2;
+  static constexpr int kQAtom = 128 * 128, kKAtom = KT * 128;
+  static constexpr int kStages = 4;  // K/V ring
+  static constexpr uint32_t kColS = 0, kColDP = KT, kColDQ = 2 * KT;  // + dS double buffer after dQ
 };
-constexpr int kTile = 128;
-constexpr int kAtomBytes = 128 * 128;
+constexpr int kTile = 128;  // query rows per CTA
 constexpr int kQThreads = 640;
 constexpr int kQCtrlRegs = 64, kQSoftRegs = 104;  // 64 + 4*104 = 480 = launch budget per lane slot
-constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256;  // dQ: D columns
-
-constexpr uint32_t kIdSS = idesc_bf16_f32(128, 128, false, false);  // S, dP
-
 template <int D>
 struct DqSmem {
-  static constexpr int kTileBytes = DqCfg<D>::kTileBytes, kQStages = DqCfg<D>::kStages;
-  uint8_t q[kTileBytes];
-  uint8_t dout[kTileBytes];
-  uint8_t k[kQStages][kTileBytes];
-  uint8_t v[kQStages][kTileBytes];
+  using C = DqCfg<D>;
+  static constexpr int kQStages = C::kStages;
+  uint8_t q[C::kQTileBytes];
+  uint8_t dout[C::kQTileBytes];
+  uint8_t k[kQStages][C::kKTileBytes];
+  uint8_t v[kQStages][C::kKTileBytes];
   uint64_t q_full, kv_full[kQStages], kv_empty[kQStages];
   uint64_t s_full, s_loaded, p_full, ds_free[2], o_done;
   uint32_t tmem_base;
@@ -62,16 +63,19 @@ __global__ void __launch_bounds__(kQThreads, 1)
     bwd_dq_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
                   const BwdParams p) {
-  auto col_ds = [](int buf) { return kColDQ + D + buf * 64u; };  // dS double buffer after dQ
-  constexpr int kAtoms = DqCfg<D>::kAtoms, kTileBytes = DqCfg<D>::kTileBytes, kQStages = DqCfg<D>::kStages;
-  // dQ += dS K: N = D; B = K MN-major, N over kAtoms atoms 16 KiB apart (LBO)
+  using C = DqCfg<D>;
+  constexpr int kAtoms = C::kAtoms, KT = C::KT, kQStages = C::kStages;
+  constexpr uint32_t kColS = C::kColS, kColDP = C::kColDP, kColDQ = C::kColDQ;
+  auto col_ds = [](int buf) { return kColDQ + D + buf * (KT / 2u); };  // dS double buffer after dQ
+  constexpr uint32_t kIdSS = idesc_bf16_f32(128, KT, false, false);  // S, dP: N = KT keys
+  // dQ += dS K: N = D; B = K MN-major, N over kAtoms atoms C::kKAtom bytes apart (LBO)
   constexpr uint32_t kIdDQ = idesc_bf16_f32(128, D, false, true);
   extern __shared__ uint8_t smem_raw[];
   DqSmem<D>& sm = *reinterpret_cast<DqSmem<D>*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int q0 = qblk * kTile;
-  const int T = (p.n_k + kTile - 1) / kTile;
+  const int T = (p.n_k + KT - 1) / KT;
   const int nq_pad = (p.n_q + kTile - 1) / kTile * kTile;
   const size_t bh = (size_t)b * p.H + h;
 
@@ -107,11 +111,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
       // ---------------------------------------------------------------- TMA producer
       const uint64_t keep = policy_evict_last(), once = policy_evict_first();
       if (elect_one()) {
-        mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
+        mbar_arrive_expect_tx(&sm.q_full, 2 * C::kQTileBytes);
 #pragma unroll
         for (int a = 0; a < kAtoms; ++a) {
-          tma_load_4d(sm.q + a * kAtomBytes, &mq, &sm.q_full, 64 * a, h, q0, b, once);
-          tma_load_4d(sm.dout + a * kAtomBytes, &mdo, &sm.q_full, 64 * a, h, q0, b, once);
+          tma_load_4d(sm.q + a * C::kQAtom, &mq, &sm.q_full, 64 * a, h, q0, b, once);
+          tma_load_4d(sm.dout + a * C::kQAtom, &mdo, &sm.q_full, 64 * a, h, q0, b, once);
         }
       }
       __syncwarp();
@@ -119,11 +123,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
         const int st = t % kQStages, n = t / kQStages;
         if (t >= kQStages) mbar_wait(&sm.kv_empty[st], (n - 1) & 1);
         if (elect_one()) {
-          mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTileBytes);
+          mbar_arrive_expect_tx(&sm.kv_full[st], 2 * C::kKTileBytes);
 #pragma unroll
           for (int a = 0; a < kAtoms; ++a) {
-            tma_load_4d(sm.k[st] + a * kAtomBytes, &mk, &sm.kv_full[st], 64 * a, h, t * kTile, b, keep);
-            tma_load_4d(sm.v[st] + a * kAtomBytes, &mv, &sm.kv_full[st], 64 * a, h, t * kTile, b, keep);
+            tma_load_4d(sm.k[st] + a * C::kKAtom, &mk, &sm.kv_full[st], 64 * a, h, t * KT, b, keep);
+            tma_load_4d(sm.v[st] + a * C::kKAtom, &mv, &sm.kv_full[st], 64 * a, h, t * KT, b, keep);
           }
         }
         __syncwarp();
@@ -134,21 +138,17 @@ __global__ void __launch_bounds__(kQThreads, 1)
       const uint64_t dOd = shfl0_u64(sdesc_sw128(smem_u32(sm.dout), 16, 1024));
       const uint64_t dK0 = shfl0_u64(sdesc_sw128(smem_u32(sm.k[0]), 16, 1024));
       const uint64_t dV0 = shfl0_u64(sdesc_sw128(smem_u32(sm.v[0]), 16, 1024));
-      const uint64_t dKm0 = shfl0_u64(sdesc_sw128(smem_u32(sm.k[0]), kAtomBytes, 1024));  // MN-major view
-      constexpr uint64_t kStep = kTileBytes >> 4, kAtomStep = kAtomBytes >> 4;
+      const uint64_t dKm0 = shfl0_u64(sdesc_sw128(smem_u32(sm.k[0]), C::kKAtom, 1024));  // MN-major view
+      constexpr uint64_t kStep = C::kKTileBytes >> 4, kQAt = C::kQAtom >> 4, kKAt = C::kKAtom >> 4;
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       auto scores = [&](int st) {  // S = Q K^T ; dP = dO V^T
         const uint64_t kd = dK0 + st * kStep, vd = dV0 + st * kStep;
 #pragma unroll
-        for (int kk = 0; kk < 4 * kAtoms; ++kk) {
-          const uint64_t off = (kk >> 2) * kAtomStep + (kk & 3) * 2;
-          umma_ss(tm + kColS, dQd + off, kd + off, kIdSS, kk > 0);
-        }
+        for (int kk = 0; kk < 4 * kAtoms; ++kk)
+          umma_ss(tm + kColS, dQd + (kk >> 2) * kQAt + (kk & 3) * 2, kd + (kk >> 2) * kKAt + (kk & 3) * 2, kIdSS, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < 4 * kAtoms; ++kk) {
-          const uint64_t off = (kk >> 2) * kAtomStep + (kk & 3) * 2;
-          umma_ss(tm + kColDP, dOd + off, vd + off, kIdSS, kk > 0);
-        }
+        for (int kk = 0; kk < 4 * kAtoms; ++kk)
+          umma_ss(tm + kColDP, dOd + (kk >> 2) * kQAt + (kk & 3) * 2, vd + (kk >> 2) * kKAt + (kk & 3) * 2, kIdSS, kk > 0);
       };
       mbar_wait(&sm.q_full, 0);
       mbar_wait(&sm.kv_full[0], 0);
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
           // dQ += dS K : K = 128 keys in steps of 16 (dS: 8 TMEM columns; K rows: 2048 B)
           const uint64_t kd = dKm0 + st * kStep;
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) umma_ts(tm + kColDQ, tm + col_ds(t & 1) + kk * 8, kd + kk * 128, kIdDQ, (t > 0 || kk > 0));
+          for (int kk = 0; kk < KT / 16; ++kk) umma_ts(tm + kColDQ, tm + col_ds(t & 1) + kk * 8, kd + kk * 128, kIdDQ, (t > 0 || kk > 0));
           umma_commit(&sm.ds_free[t & 1]);
           umma_commit(&sm.kv_empty[st]);
           if (!more) umma_commit(&sm.o_done);
@@ -212,16 +212,22 @@ __global__ void __launch_bounds__(kQThreads, 1)
       mbar_wait(&sm.s_full, t & 1);
       TPROBE(1)
       tc_fence_after();
-      uint32_t sr[32], dr[32];
-      tmem_ld32_split<32>(lane_base + kColS + colhalf * 64, sr);
-      tmem_ld32_split<32>(lane_base + kColDP + colhalf * 64, dr);
+      constexpr int NE = KT / 4;  // key columns per thread: colhalf * KT/2 + (lane >> 4) * KT/4 + [0, NE)
+      uint32_t sr[NE], dr[NE];
+      if constexpr (NE == 32) {
+        tmem_ld32_split<32>(lane_base + kColS + colhalf * 64, sr);
+        tmem_ld32_split<32>(lane_base + kColDP + colhalf * 64, dr);
+      } else {
+        tmem_ld16_split<16>(lane_base + kColS + colhalf * 32, sr);
+        tmem_ld16_split<16>(lane_base + kColDP + colhalf * 32, dr);
+      }
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&sm.s_loaded);  // S_t, dP_t are in registers: the next scores may overwrite them
       TPROBE(2)
-      uint32_t pk[16];
+      uint32_t pk[NE / 2];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
+      for (int u = 0; u < NE / 2; ++u) {
         const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
         const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
         const float2 x = __ffma2_rn(s2, c2, nl2);                              // s c - lse2
@@ -233,7 +239,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
       if (t > 1) mbar_wait(&sm.ds_free[t & 1], ((t >> 1) - 1) & 1);  // dQ_{t-2} has consumed this buffer
       TPROBE(4)
       tc_fence_after();
-      tmem_st16_split<16>(lane_base + col_ds(t & 1) + colhalf * 32, pk);
+      if constexpr (NE == 32) {
+        tmem_st16_split<16>(lane_base + col_ds(t & 1) + colhalf * 32, pk);
+      } else {
+        tmem_st8_split<8>(lane_base + col_ds(t & 1) + colhalf * 16, pk);
+      }
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm.p_full);

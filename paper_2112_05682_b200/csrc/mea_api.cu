@@ -588,8 +588,16 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
       ProfScope ps("bwd_dkdv", st);
       if ((e = launch_bwd_dkdv(p, mq_t, mk, mv, mdo_t, st)) != cudaSuccess) return cuda_fail(e, "bwd_dkdv launch");
     }
+    // d = 128: the dQ kernel takes 64-key tiles (a 4-stage K/V ring next to resident Q, dO)
+    CUtensorMap mk_t = mk, mv_t = mv;
+    if (d == 128 &&
+        ((e = make_bnhd_map(&mk_t, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, 64,
+                            CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+         (e = make_bnhd_map(&mv_t, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, 64,
+                            CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess))
+      return cuda_fail(e, why);
     ProfScope ps("bwd_dq", st);
-    if ((e = launch_bwd_dq(p, mq, mk, mv, mdo, st)) != cudaSuccess) return cuda_fail(e, "bwd_dq launch");
+    if ((e = launch_bwd_dq(p, mq, mk_t, mv_t, mdo, st)) != cudaSuccess) return cuda_fail(e, "bwd_dq launch");
   }
   return MEA_OK;
 }
