@@ -44,6 +44,10 @@ template <int D> struct DkvCfg {
   static constexpr int kKAtom = 128 * 128, kQAtom = QT * 128;
   static constexpr uint32_t kColST = 0, kColDPT = QT, kColP = 2 * QT, kColDS = 2 * QT + QT / 2,
                             kColDV = 3 * QT, kColDK = 3 * QT + D;
+  // D = 128: the K tile also sits in TMEM (bf16 pairs, D/2 columns) as the A operand of a TS
+  // Sᵀ MMA, so Sᵀ = K Qᵀ reads only Q from shared memory (SS at N = 64 is SMEM-bound, 65 %)
+  static constexpr bool kKInTmem = D == 128;
+  static constexpr uint32_t kColKA = 3 * QT + 2 * D;
 };
 // setmaxnreg budgets. Measured on B200: setmaxnreg.inc only redistributes the registers the
 // CTA was launched with (640 threads x 96 = 480 per lane slot of each SM sub-partition, which
@@ -59,7 +63,7 @@ struct BwdSmem {
   float lse2[kBStages][C::QT];
   float delta[kBStages][C::QT];
   uint64_t kv_full, qdo_full[kBStages], qdo_empty[kBStages];
-  uint64_t s_full, s_loaded, p_full, p_free, dkv_done;
+  uint64_t s_full, s_loaded, p_full, p_free, dkv_done, ka_full;
   uint32_t tmem_base;
 };
 template <int D> constexpr size_t dkv_smem_bytes() { return sizeof(BwdSmem<D>) + 1024; }
@@ -111,6 +115,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
     mbar_init(&sm.p_full, 512);
     mbar_init(&sm.p_free, 1);
     mbar_init(&sm.dkv_done, 1);
+    mbar_init(&sm.ka_full, 128);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -168,13 +173,18 @@ __global__ void __launch_bounds__(kBThreads, 1)
       auto scores = [&](int st) {  // ST = K Q^T ; dPT = V dO^T  (K = D in steps of 16)
         const uint64_t q = dQ0 + st * kStep, o = dO0 + st * kStep;
 #pragma unroll
-        for (int kk = 0; kk < 4 * kAtoms; ++kk)
-          umma_ss(tm + kColST, dK + (kk >> 2) * kKAt + (kk & 3) * 2, q + (kk >> 2) * kQAt + (kk & 3) * 2, kIdSS, kk > 0);
+        for (int kk = 0; kk < 4 * kAtoms; ++kk) {
+          if constexpr (C::kKInTmem)
+            umma_ts(tm + kColST, tm + C::kColKA + kk * 8, q + (kk >> 2) * kQAt + (kk & 3) * 2, kIdSS, kk > 0);
+          else
+            umma_ss(tm + kColST, dK + (kk >> 2) * kKAt + (kk & 3) * 2, q + (kk >> 2) * kQAt + (kk & 3) * 2, kIdSS, kk > 0);
+        }
 #pragma unroll
         for (int kk = 0; kk < 4 * kAtoms; ++kk)
           umma_ss(tm + kColDPT, dV + (kk >> 2) * kKAt + (kk & 3) * 2, o + (kk >> 2) * kQAt + (kk & 3) * 2, kIdSS, kk > 0);
       };
       mbar_wait(&sm.kv_full, 0);
+      if constexpr (C::kKInTmem) mbar_wait(&sm.ka_full, 0);
       mbar_wait(&sm.qdo_full[0], 0);
       tc_fence_after();
       if (elect_one()) {
@@ -222,6 +232,24 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     const float c = p.scale_log2;
     const float2 c2 = make_float2(c, c);
+    if constexpr (C::kKInTmem) {
+      if (g == 0) {  // K row j (SW128 smem, D/64 atoms) -> TMEM lane j, columns kColKA + [0, D/2)
+        mbar_wait(&sm.kv_full, 0);
+#pragma unroll
+        for (int a = 0; a < kAtoms; ++a) {
+          uint32_t r[32];
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            const uint4 w = *reinterpret_cast<const uint4*>(sm.k + a * C::kKAtom + j * 128 + ((cc ^ (j & 7)) * 16));
+            r[4 * cc] = w.x; r[4 * cc + 1] = w.y; r[4 * cc + 2] = w.z; r[4 * cc + 3] = w.w;
+          }
+          tmem_st32(lane_base + C::kColKA + a * 32, r);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&sm.ka_full);
+      }
+    }
 #ifdef MEA_EXP_TIMING
     unsigned long long* tdbg = reinterpret_cast<unsigned long long*>(p.dv);
     const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && quarter == 0 && lane == 0;

@@ -7,12 +7,14 @@ for name, (res, args) in _lib.SIGNATURES.items():
     if not hasattr(lib, name): continue
     f = getattr(lib, name); f.restype = res; f.argtypes = args
 _lib._lib = lib
-q = torch.empty((1, 16384, 16, 64), dtype=torch.bfloat16, device="cuda")
+d = int(sys.argv[2]) if len(sys.argv) > 2 else 64   # d = 128 (or DET=1): the two-kernel path's dK/dV kernel
+q = torch.empty((1, 16384, 16, d), dtype=torch.bfloat16, device="cuda")
 k, v, do = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
 for t, tid in ((q, 1), (k, 2), (v, 3), (do, 4)): api.mea_fill_synthetic(t, 0, tid)
 out, lse = api.mea_attention_fwd(q, k, v, want_lse=True)
 dv = torch.zeros_like(q)
-for _ in range(2): api.mea_attention_bwd(q, k, v, out, do, lse=lse, dv=dv)
+fn = api.mea_attention_bwd_deterministic if os.environ.get("DET") == "1" else api.mea_attention_bwd
+for _ in range(2): fn(q, k, v, out, do, lse=lse, dv=dv)
 torch.cuda.synchronize()
 raw = dv.view(torch.int64).flatten()[:512 + 16 * 8].cpu().numpy().astype(np.int64)
 ts = raw[:512].reshape(4, 16, 8)
@@ -26,9 +28,11 @@ for g in range(4):
 
 print("softmax means over 16 tiles (cycles):")
 for g in range(4):
-    d = np.diff(ts[g, :, :5], axis=1).mean(axis=0)
+    dd = np.diff(ts[g, :, :5], axis=1).mean(axis=0)
     per = np.diff(ts[g, :, 0]).mean()
-    print(f"  g{g} period {per:7.0f} | " + " ".join(f"{n}={x:.0f}" for n, x in zip(names, d)))
+    print(f"  g{g} period {per:7.0f} | " + " ".join(f"{n}={x:.0f}" for n, x in zip(names, dd)))
+if d != 64 or os.environ.get("DET") == "1":
+    sys.exit(0)   # the dK/dV kernel has no MMA-warp probes
 mn = ["wait_qdo", "wait_s_loaded", "wait_p_full(+issue S)", "wait_dq_empty(+issue dV dK)"]
 print("MMA warp means (cycles):", " ".join(f"{n}={x:.0f}" for n, x in zip(mn, np.diff(mm[:, :5], axis=1).mean(axis=0))),
       f"period {np.diff(mm[:, 0]).mean():.0f}")
