@@ -22,10 +22,19 @@
 namespace mea {
 namespace {
 
-constexpr int kSqThreads = 512;  // one CTA per SM: 16 warps x 256 B x 2 steps in flight
+#ifndef MEA_SQ_THREADS
+#define MEA_SQ_THREADS 512
+#endif
+#ifndef MEA_SQ_UNROLL
+#define MEA_SQ_UNROLL 2
+#endif
+#ifndef MEA_SQ_CTAS
+#define MEA_SQ_CTAS 148
+#endif
+constexpr int kSqThreads = MEA_SQ_THREADS;  // one CTA per SM: 16 warps x 256 B x 2 steps in flight
 constexpr int kSqWarps = kSqThreads / 32;
 constexpr int kKeysPerWarpStep = 16;  // 4 groups x 4 keys
-constexpr int kUnroll = 2;            // warp steps in flight
+constexpr int kUnroll = MEA_SQ_UNROLL;  // warp steps in flight
 
 struct State {
   float m, l, a[8];
@@ -346,7 +355,7 @@ __global__ void merge_partials_kernel(const float* __restrict__ m, const float* 
 // Splits: one 512-thread CTA per SM streaming (HBM needs ~35 KB in flight per SM; a CTA has
 // 256 KB in flight), at least ~1024 keys per split, so the merge stays small.
 int sq_num_splits(int64_t BH, int64_t n_k) {
-  const int64_t target_ctas = 148;
+  const int64_t target_ctas = MEA_SQ_CTAS;
   int64_t splits = (target_ctas + BH - 1) / BH;
   const int64_t max_by_keys = (n_k + 1023) / 1024;
   if (splits > max_by_keys) splits = max_by_keys;
