@@ -32,8 +32,8 @@
  *      CUDA launch/encode failure     -> MEA_ERR_CUDA (detail in mea_last_error_detail)
  *  - Non-finite input values are not checked; they propagate.
  *  - Supported: bf16 inputs with d = 64 (all entry points) or d = 128 (mea_attention_fwd
- *    without key chunks, mea_attention_bwd, mea_attention_bwd_deterministic) on tcgen05
- *    tensor-core kernels; f32 inputs with 1 <= d <= 128 (exact-f32 SIMT kernels, forward and
+ *    without key chunks, the causal pair, mea_attention_bwd, mea_attention_bwd_deterministic)
+ *    on tcgen05 tensor-core kernels; f32 inputs with 1 <= d <= 128 (exact-f32 SIMT kernels, forward and
  *    single query).
  */
 #ifndef MEA_H_
@@ -106,7 +106,7 @@ MEA_API mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int6
  * Causal self-attention forward (not in the paper, which disabled
  * packing to avoid masking; reimplementations added it): query i
  * attends keys j <= i only. q, k, v, out [B,n,H,d] (n_q == n_k == n, top-left aligned), lse as
- * for mea_attention_fwd. bf16 inputs with d == 64 only (MEA_ERR_UNSUPPORTED otherwise); online
+ * for mea_attention_fwd. bf16 inputs with d in {64, 128} (MEA_ERR_UNSUPPORTED otherwise); online
  * schedule (no key chunks), no workspace. Key tiles past a query tile's diagonal are skipped.
  */
 MEA_API mea_status_t mea_attention_fwd_causal(const void* q, const void* k, const void* v, void* out,

@@ -101,6 +101,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
   const int kblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int k0 = kblk * kTile;
   const int NQ = (p.n_q + QT - 1) / QT;
+  // causal (n_q == n_k): query tiles before this key tile see none of its keys; iteration i
+  // (stages, barrier phases) handles query tile i0 + i
+  const int i0 = p.causal ? k0 / QT : 0;
+  const int NT = NQ - i0;
   const int nq_pad = (p.n_q + kTileM - 1) / kTileM * kTileM;  // bwd_preprocess's row padding
   const size_t bh = (size_t)b * p.H + h;
 
@@ -144,18 +148,18 @@ __global__ void __launch_bounds__(kBThreads, 1)
         }
       }
       __syncwarp();
-      for (int i = 0; i < NQ; ++i) {
+      for (int i = 0; i < NT; ++i) {
         const int st = i % kBStages, n = i / kBStages;
         if (i >= kBStages) mbar_wait(&sm.qdo_empty[st], (n - 1) & 1);
         if (elect_one()) {
           mbar_arrive_expect_tx(&sm.qdo_full[st], 2 * C::kQTileBytes + 2 * QT * 4);
 #pragma unroll
           for (int a = 0; a < kAtoms; ++a) {
-            tma_load_4d(sm.q[st] + a * C::kQAtom, &mq, &sm.qdo_full[st], 64 * a, h, i * QT, b, keep);
-            tma_load_4d(sm.dout[st] + a * C::kQAtom, &mdo, &sm.qdo_full[st], 64 * a, h, i * QT, b, keep);
+            tma_load_4d(sm.q[st] + a * C::kQAtom, &mq, &sm.qdo_full[st], 64 * a, h, (i0 + i) * QT, b, keep);
+            tma_load_4d(sm.dout[st] + a * C::kQAtom, &mdo, &sm.qdo_full[st], 64 * a, h, (i0 + i) * QT, b, keep);
           }
-          bulk_load(sm.lse2[st], p.lse2 + bh * nq_pad + i * QT, QT * 4, &sm.qdo_full[st]);
-          bulk_load(sm.delta[st], p.delta + bh * nq_pad + i * QT, QT * 4, &sm.qdo_full[st]);
+          bulk_load(sm.lse2[st], p.lse2 + bh * nq_pad + (i0 + i) * QT, QT * 4, &sm.qdo_full[st]);
+          bulk_load(sm.delta[st], p.delta + bh * nq_pad + (i0 + i) * QT, QT * 4, &sm.qdo_full[st]);
         }
         __syncwarp();
       }
@@ -192,9 +196,9 @@ __global__ void __launch_bounds__(kBThreads, 1)
         umma_commit(&sm.s_full);
       }
       __syncwarp();
-      for (int i = 0; i < NQ; ++i) {
+      for (int i = 0; i < NT; ++i) {
         const int st = i % kBStages;
-        const bool more = i + 1 < NQ;
+        const bool more = i + 1 < NT;
         if (more) {
           mbar_wait(&sm.qdo_full[(i + 1) % kBStages], ((i + 1) / kBStages) & 1);
           mbar_wait(&sm.s_loaded, i & 1);
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
 #else
 #define TPROBE(k)
 #endif
-    for (int i = 0; i < NQ; ++i) {
+    for (int i = 0; i < NT; ++i) {
       const int st = i % kBStages;
       TPROBE(0)
       mbar_wait(&sm.s_full, i & 1);
@@ -276,6 +280,8 @@ __global__ void __launch_bounds__(kBThreads, 1)
       mbar_arrive(&sm.s_loaded);  // ST_i / dPT_i are in registers: the next scores may overwrite
       const float* l2 = sm.lse2[st] + g * NC;
       const float* dl = sm.delta[st] + g * NC;
+      const int qbase = (i0 + i) * QT + NC * g;                     // first query column of this thread
+      const bool overlap = p.causal && (i0 + i) * QT < k0 + kTile;  // tile crosses the diagonal
       uint32_t pk[NC / 2], dk[NC / 2];
 #pragma unroll
       for (int u = 0; u < NC / 2; ++u) {
@@ -286,6 +292,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
         const float2 x = __ffma2_rn(s2, c2, make_float2(-lq.x, -lq.y));  // s c - lse2
         float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));        // P (lse2 = +inf pads -> 0)
         if (!key_ok) pr = make_float2(0.f, 0.f);
+        if (overlap) {  // causal: key k0 + j > query qbase + 2u (+1) is masked
+          if (k0 + j > qbase + 2 * u) pr.x = 0.f;
+          if (k0 + j > qbase + 2 * u + 1) pr.y = 0.f;
+        }
         const float2 ds = __fmul2_rn(pr, __fadd2_rn(d2, make_float2(-de.x, -de.y)));  // P (dP - delta)
         pk[u] = pack_bf16x2(pr.x, pr.y);
         dk[u] = pack_bf16x2(ds.x, ds.y);

@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(kQThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int qblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int q0 = qblk * kTile;
-  const int T = (p.n_k + KT - 1) / KT;
+  // causal (n_q == n_k): keys up to this block's last query row only
+  const int T = p.causal ? min((p.n_k + KT - 1) / KT, (q0 + kTile + KT - 1) / KT) : (p.n_k + KT - 1) / KT;
   const int nq_pad = (p.n_q + kTile - 1) / kTile * kTile;
   const size_t bh = (size_t)b * p.H + h;
 
@@ -231,7 +232,12 @@ __global__ void __launch_bounds__(kQThreads, 1)
         const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
         const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
         const float2 x = __ffma2_rn(s2, c2, nl2);                              // s c - lse2
-        const float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));       // P
+        float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));             // P
+        if (p.causal) {  // key t KT + col > query row: masked
+          const int key = t * KT + colhalf * (KT / 2) + (lane >> 4) * (KT / 4) + 2 * u;
+          if (key > row) pr.x = 0.f;
+          if (key + 1 > row) pr.y = 0.f;
+        }
         const float2 ds = __fmul2_rn(pr, __fadd2_rn(d2, nd2));                 // P (dP - delta)
         pk[u] = pack_bf16x2(ds.x, ds.y);
       }

@@ -55,8 +55,13 @@ __global__ void __launch_bounds__(kThreads128, 1)
   Fwd128Smem& sm = *reinterpret_cast<Fwd128Smem*>(align1024_128(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.y, b = blockIdx.z;
-  const int q0 = blockIdx.x * 128;
-  const int T = (p.n_k + kTileN - 1) / kTileN;
+  // causal (n_q == n_k): query tile qb needs key tiles [0, qb] (the last one is its diagonal);
+  // the blocks with the most key tiles are scheduled first
+  const int qb = p.causal ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;
+  const int q0 = qb * 128;
+  const int n_tiles = (p.n_k + kTileN - 1) / kTileN;
+  const int T = p.causal ? min(n_tiles, qb + 1) : n_tiles;
+  const int diag = p.causal ? qb : -1;
   const int key_end = p.n_k;
 
   if (threadIdx.x == 0) {
@@ -179,10 +184,10 @@ __global__ void __launch_bounds__(kThreads128, 1)
       mbar_wait(&sm.s_full[buf], (t >> 1) & 1);
       tc_fence_after();
       uint32_t sr[64];
-      const int tile_valid = key_end - t * kTileN;
+      const int tile_valid = (p.causal ? min(key_end, row + 1) : key_end) - t * kTileN;  // keys <= row if causal
       const int valid = tile_valid - half * 64;
       uint32_t pk[32];
-      bool fast = (t > 0) && (tile_valid >= kTileN) && (c >= 0.f);
+      bool fast = (t > 0) && (t != diag) && (key_end - t * kTileN >= kTileN) && (c >= 0.f);
       tmem_ld32_split<64>(lane_base + colS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
       if (fast) {
         tmem_ld_wait();

@@ -212,7 +212,6 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
   }
 
   if (d == 128) {  // fwd128_sm100a.cu: online schedule only
-    if (causal) return fail(MEA_ERR_UNSUPPORTED, "causal attention: d == 64 only");
     if (k_chunk > 0 && k_chunk < n_k) return fail(MEA_ERR_UNSUPPORTED, "key chunks: d == 64 only");
     CUtensorMap mq, mk, mv;
     const char* why = "";
@@ -234,6 +233,7 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
     p.out = out;
     p.out_f32 = out_dtype == MEA_F32;
     p.lse = lse;
+    p.causal = causal ? 1 : 0;
     ProfScope ps("fwd128_bf16", st);
     if ((e = launch_fwd128_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd128_bf16 launch");
     return MEA_OK;
@@ -493,7 +493,6 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   if (!valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
   if (n_k == 0) return fail(MEA_ERR_EMPTY_KEYS, "attention over an empty key list");
   if (dtype != MEA_BF16 || (d != kHeadDim && d != 128)) return fail(MEA_ERR_UNSUPPORTED, "backward: bf16, d in {64, 128}");
-  if (d == 128 && causal) return fail(MEA_ERR_UNSUPPORTED, "causal backward: d == 64 only");
   if (!k || !v || !dk || !dv) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e;

@@ -92,7 +92,7 @@ def test_host_only_validation_of_the_newer_entry_points(lib):
     # causal: bf16 only (status 3 = unsupported); n == 0 is a no-op; n_k == 0 impossible (n_q == n_k)
     assert lib.mea_attention_fwd_causal(p, p, p, p, 1, 1, 8, 64, 0, 0, 1.0, None, None) == 3
     assert lib.mea_attention_fwd_causal(p, p, p, p, 1, 1, 0, 64, 1, 1, 1.0, None, None) == 0
-    assert lib.mea_attention_fwd_causal(p, p, p, p, 1, 1, 8, 128, 1, 1, 1.0, None, None) == 3  # d = 128
+    assert lib.mea_attention_fwd_causal(p, p, p, p, 1, 1, 8, 32, 1, 1, 1.0, None, None) == 3  # d = 32
     assert lib.mea_attention_bwd_causal(p, p, p, p, p, p, p, p, 1, 1, 8, 64, 1, 0.0, None, None, 0, None) == 3
     # key chunks at d = 128: unsupported; f32 key chunks: unsupported
     assert lib.mea_attention_fwd(p, p, p, p, 1, 1, 300, 300, 128, 1, 1, 1.0, None, 0, 128, None, 0, None) == 3

@@ -2,7 +2,8 @@
 (fwd128_sm100a.cu) and the backward (bwd_det_sm100a.cu / bwd_dq_sm100a.cu at D = 128)
 against the float64 oracle (O1) on the same generated inputs: shapes over several query and key
 tiles with ragged tails, both output dtypes and scales, the rescale stress case, configs[2]'s
-length at d = 128 on sampled rows, and the explicit errors of what d = 128 does not cover.
+length at d = 128 on sampled rows, and the explicit error of what d = 128 does not cover (key
+chunks). Causal attention at d = 128: tests/test_gpu_causal.py.
 """
 import math
 
@@ -83,8 +84,6 @@ def test_d128_unsupported_paths_fail_loudly():
     q = torch.zeros(1, 256, 1, D, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(api.MeaError):
         api.mea_attention_fwd(q, q, q, k_chunk=128)            # key chunks: d = 64 only
-    with pytest.raises(api.MeaError):
-        api.mea_attention_fwd_causal(q, q, q)                 # causal: d = 64 only
 
 
 @pytest.mark.parametrize("B,n_q,n_k,H,lse_given", [(1, 130, 300, 2, True), (2, 257, 129, 1, True),
