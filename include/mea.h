@@ -31,9 +31,9 @@
  *      workspace smaller than needed  -> MEA_ERR_WORKSPACE_TOO_SMALL
  *      CUDA launch/encode failure     -> MEA_ERR_CUDA (detail in mea_last_error_detail)
  *  - Non-finite input values are not checked; they propagate.
- *  - Supported: bf16 inputs with d = 64 (all entry points) or d = 128 (mea_attention_fwd
- *    without key chunks, the causal pair, mea_attention_bwd, mea_attention_bwd_deterministic)
- *    on tcgen05 tensor-core kernels; f32 inputs with 1 <= d <= 128 (exact-f32 SIMT kernels, forward and
+ *  - Supported: bf16 inputs with d = 64 (all entry points) or d = 128 (all but the key-chunk
+ *    schedule of mea_attention_fwd) on tcgen05 tensor-core kernels (single query: streaming
+ *    SIMT kernels); f32 inputs with 1 <= d <= 128 (exact-f32 SIMT kernels, forward and
  *    single query).
  */
 #ifndef MEA_H_
@@ -146,7 +146,7 @@ MEA_API mea_status_t mea_single_query_workspace_size(int64_t B, int64_t H, int64
  * Self-attention over one key range, as a stream state per query row (multi-GPU building block:
  * key-range sharding of long-context self-attention; the merge is
  * mea_merge_partials with H := n_q * H).
- *   q [B,n_q,H,d], k,v [B,n_k,H,d] bf16, d == 64 (MEA_ERR_UNSUPPORTED otherwise).
+ *   q [B,n_q,H,d], k,v [B,n_k,H,d] bf16, d in {64, 128} (MEA_ERR_UNSUPPORTED otherwise).
  *   m [B,n_q,H], s [B,n_q,H], vstar [B,n_q,H,d] float32 outputs, same meaning as for
  *   mea_single_query_partial (m in natural-log units of the scaled score).
  *   n_k == 0 yields the empty triple (-inf, 0, 0) for every row; n_q == 0 is a no-op.

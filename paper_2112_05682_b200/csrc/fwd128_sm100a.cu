@@ -285,7 +285,19 @@ __global__ void __launch_bounds__(kThreads128, 1)
     tmem_ld32_split<64>(lane_base + kColO, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
     tmem_ld32_split<64>(lane_base + kColO + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
     tmem_ld_wait();
-    if (row < p.n_q) {
+    if (row < p.n_q && p.tri_v) {
+      // this call's (m*, s*, v*) per row, for a merge across key ranges
+      const size_t idx = ((size_t)b * p.n_q + row) * p.H + h;
+      float4* dst = reinterpret_cast<float4*>(p.tri_v + idx * kD + half * 64);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]), __uint_as_float(o[4 * i + 2]),
+                             __uint_as_float(o[4 * i + 3]));
+      if (half == 0) {
+        p.tri_m[idx] = m_ref * 0.6931471805599453f;
+        p.tri_s[idx] = lrow;
+      }
+    } else if (row < p.n_q) {
       const size_t bh = (size_t)b * p.H + h;
       const float inv = 1.f / lrow;
       const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kD + half * 64;

@@ -315,7 +315,8 @@ mea_status_t mea_attention_partial_fwd(const void* q, const void* k, const void*
                                        mea_dtype_t in_dtype, float scale, void* stream) {
   if (mea_status_t r = check_common(B, H, n_q, n_k, d, scale)) return r;
   if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  if (in_dtype != MEA_BF16 || d != kHeadDim) return fail(MEA_ERR_UNSUPPORTED, "partial forward: bf16, d == 64");
+  if (in_dtype != MEA_BF16 || (d != kHeadDim && d != 128))
+    return fail(MEA_ERR_UNSUPPORTED, "partial forward: bf16, d in {64, 128}");
   if (n_q == 0) return MEA_OK;
   if (!m || !s || !vstar || !q) return fail(MEA_ERR_INVALID_VALUE, "NULL pointer");
   if (!aligned16(q) || !aligned16(vstar) || (reinterpret_cast<uintptr_t>(m) & 3u) ||
@@ -354,6 +355,11 @@ mea_status_t mea_attention_partial_fwd(const void* q, const void* k, const void*
   p.tri_m = m;
   p.tri_s = s;
   p.tri_v = vstar;
+  if (d == 128) {
+    ProfScope ps("fwd128_bf16", st);
+    if ((e = launch_fwd128_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd128_bf16 launch");
+    return MEA_OK;
+  }
   ProfScope ps("fwd_bf16", st);
   if ((e = launch_fwd_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_bf16 launch");
   return MEA_OK;
@@ -375,7 +381,8 @@ static mea_status_t sq_common(const void* q, const void* k, const void* v, int64
                               int* splits_out) {
   if (mea_status_t s = check_common(B, H, 1, n_k, d, scale)) return s;
   if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  if (in_dtype == MEA_BF16 && d != kHeadDim) return fail(MEA_ERR_UNSUPPORTED, "bf16 single query supports d == 64");
+  if (in_dtype == MEA_BF16 && d != kHeadDim && d != 128)
+    return fail(MEA_ERR_UNSUPPORTED, "bf16 single query supports d in {64, 128}");
   if (in_dtype == MEA_F32 && d > 128) return fail(MEA_ERR_UNSUPPORTED, "f32 single query supports d <= 128");
   if (B * H > 65535) return fail(MEA_ERR_UNSUPPORTED, "B*H > 65535");
   if (!q || (n_k > 0 && (!k || !v))) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");

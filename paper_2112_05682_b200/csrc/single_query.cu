@@ -33,7 +33,13 @@ namespace {
 #endif
 constexpr int kSqThreads = MEA_SQ_THREADS;  // one CTA per SM: 16 warps x 256 B x 2 steps in flight
 constexpr int kSqWarps = kSqThreads / 32;
-constexpr int kKeysPerWarpStep = 16;  // 4 groups x 4 keys
+// D = 64: 8 lanes per 128-byte key row, 4 key groups per warp; D = 128: 16 lanes per 256-byte
+// row, 2 groups. Every lane holds 8 dims of its group's state.
+template <int D> struct SqCfg {
+  static constexpr int LPR = D / 8;                  // lanes per key row
+  static constexpr int G = 32 / LPR;                 // key groups per warp
+  static constexpr int kKeysPerWarpStep = 4 * G;     // 4 keys per group per step
+};
 constexpr int kUnroll = MEA_SQ_UNROLL;  // warp steps in flight
 
 struct State {
@@ -68,24 +74,27 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
   return r;
 }
 
+template <int D>
 __global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_bfloat16* __restrict__ q,
                                                                      const __nv_bfloat16* __restrict__ k,
                                                                      const __nv_bfloat16* __restrict__ v, int H,
                                                                      int n_k, float scale_log2, int splits,
                                                                      float* __restrict__ part) {
   asm volatile("griddepcontrol.launch_dependents;");
+  using C = SqCfg<D>;
+  constexpr int LPR = C::LPR, kKeysPerWarpStep = C::kKeysPerWarpStep;
   const int split = blockIdx.x, bh = blockIdx.y;
   const int b = bh / H, h = bh % H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 3, cidx = lane & 7;  // key group in the warp, 16-byte chunk of the row
+  const int g = lane / LPR, cidx = lane % LPR;  // key group in the warp, 16-byte chunk of the row
   const int per = (n_k + splits - 1) / splits;
   const int k_lo = split * per, k_hi = min(n_k, k_lo + per);
-  const size_t row_stride = (size_t)H * kHeadDim;  // elements between consecutive keys
-  const __nv_bfloat16* kb = k + ((size_t)b * n_k * H + h) * kHeadDim + cidx * 8;
-  const __nv_bfloat16* vb = v + ((size_t)b * n_k * H + h) * kHeadDim + cidx * 8;
+  const size_t row_stride = (size_t)H * D;  // elements between consecutive keys
+  const __nv_bfloat16* kb = k + ((size_t)b * n_k * H + h) * D + cidx * 8;
+  const __nv_bfloat16* vb = v + ((size_t)b * n_k * H + h) * D + cidx * 8;
 
   float qf[8];
-  bf16x8_to_f32(*reinterpret_cast<const uint4*>(q + (size_t)bh * kHeadDim + cidx * 8), qf);
+  bf16x8_to_f32(*reinterpret_cast<const uint4*>(q + (size_t)bh * D + cidx * 8), qf);
 #pragma unroll
   for (int i = 0; i < 8; ++i) qf[i] *= scale_log2;
 
@@ -102,7 +111,7 @@ __global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_
     for (int s = 0; s < kUnroll; ++s)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int key = base + s * kStep + u * 4 + g;
+        const int key = base + s * kStep + u * C::G + g;
         if (key < k_hi) {
           kr[s][u] = ld_stream(kb + (size_t)key * row_stride);
           vr[s][u] = ld_stream(vb + (size_t)key * row_stride);
@@ -121,10 +130,9 @@ __global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_
         float dot = 0.f;
 #pragma unroll
         for (int i = 0; i < 8; ++i) dot = fmaf(qf[i], kf[i], dot);
-        dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-        dot += __shfl_xor_sync(0xffffffffu, dot, 2);
-        dot += __shfl_xor_sync(0xffffffffu, dot, 4);
-        const int key = base + s * kStep + u * 4 + g;
+#pragma unroll
+        for (int o = 1; o < LPR; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        const int key = base + s * kStep + u * C::G + g;
         sc[u] = key < k_hi ? dot : -INFINITY;
       }
       const float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
@@ -146,9 +154,9 @@ __global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_
       st.m = m_new;
     }
   }
-  // merge the 4 key groups of the warp (lanes with equal cidx hold the same 8 dims)
+  // merge the key groups of the warp (lanes with equal cidx hold the same 8 dims)
 #pragma unroll
-  for (int off = 8; off <= 16; off <<= 1) {
+  for (int off = LPR; off <= 16; off <<= 1) {
     State o;
     o.m = __shfl_xor_sync(0xffffffffu, st.m, off);
     o.l = __shfl_xor_sync(0xffffffffu, st.l, off);
@@ -156,8 +164,8 @@ __global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_
     for (int i = 0; i < 8; ++i) o.a[i] = __shfl_xor_sync(0xffffffffu, st.a[i], off);
     merge_state(st, o);
   }
-  __shared__ float sm_m[kSqWarps], sm_l[kSqWarps], sm_a[kSqWarps][kHeadDim];
-  if (lane < 8) {
+  __shared__ float sm_m[kSqWarps], sm_l[kSqWarps], sm_a[kSqWarps][D];
+  if (lane < LPR) {
     if (lane == 0) {
       sm_m[warp] = st.m;
       sm_l[warp] = st.l;
@@ -166,7 +174,7 @@ __global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_
     for (int i = 0; i < 8; ++i) sm_a[warp][cidx * 8 + i] = st.a[i];
   }
   __syncthreads();
-  if (threadIdx.x < kHeadDim) {
+  if (threadIdx.x < D) {
     const int f = threadIdx.x;
     float M = -INFINITY;
     for (int w = 0; w < kSqWarps; ++w) M = fmaxf(M, sm_m[w]);
@@ -178,7 +186,7 @@ __global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_
         a += wt * sm_a[w][f];
       }
     }
-    float* dst = part + ((size_t)bh * splits + split) * (kHeadDim + 2);
+    float* dst = part + ((size_t)bh * splits + split) * (D + 2);
     if (f == 0) {
       dst[0] = M;
       dst[1] = l;
@@ -368,10 +376,14 @@ cudaError_t launch_sq_partial(const void* q, const void* k, const void* v, int b
                               float scale, int splits, float* ws, cudaStream_t s) {
   const float c = scale * 1.4426950408889634f;
   dim3 grid(splits, B * H);
-  if (bf16) {
-    sq_partial_bf16_kernel<<<grid, kSqThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(q),
-                                                      static_cast<const __nv_bfloat16*>(k),
-                                                      static_cast<const __nv_bfloat16*>(v), H, n_k, c, splits, ws);
+  if (bf16 && d == 128) {
+    sq_partial_bf16_kernel<128><<<grid, kSqThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(q),
+                                                           static_cast<const __nv_bfloat16*>(k),
+                                                           static_cast<const __nv_bfloat16*>(v), H, n_k, c, splits, ws);
+  } else if (bf16) {
+    sq_partial_bf16_kernel<64><<<grid, kSqThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(q),
+                                                          static_cast<const __nv_bfloat16*>(k),
+                                                          static_cast<const __nv_bfloat16*>(v), H, n_k, c, splits, ws);
   } else {
     sq_partial_f32_kernel<<<grid, 128, 0, s>>>(static_cast<const float*>(q), static_cast<const float*>(k),
                                                static_cast<const float*>(v), H, n_k, d, c, splits, ws);

@@ -102,8 +102,8 @@ def test_host_only_validation_of_the_newer_entry_points(lib):
     assert lib.mea_attention_bwd(p, p, p, p, p, p, p, p, 1, 1, 8, 8, 64, 0, 1.0, None, None, 0, None) == 3
     # backward workspace too small (status 5) before any launch
     assert lib.mea_attention_bwd(p, p, p, p, p, p, p, p, 1, 1, 8, 8, 64, 1, 1.0, None, p, 16, None) == 5
-    # partial forward: bf16 d = 64 only; n_q == 0 no-op
-    assert lib.mea_attention_partial_fwd(p, p, p, p, p, p, 1, 1, 8, 8, 128, 1, 1.0, None) == 3
+    # partial forward: bf16 d in {64, 128}; n_q == 0 no-op
+    assert lib.mea_attention_partial_fwd(p, p, p, p, p, p, 1, 1, 8, 8, 96, 1, 1.0, None) == 3
     assert lib.mea_attention_partial_fwd(p, p, p, p, p, p, 1, 1, 0, 8, 64, 1, 1.0, None) == 0
     # d = 128 workspace sizes: forward none; backward (two-kernel path) delta and lse2 only,
     # each padded to 128 rows per (b, h) and 256-byte aligned

@@ -40,6 +40,23 @@ def test_partial_triple_matches_oracle(B, n_q, n_k, H):
             assert np.abs((m[b, :, h] + np.log(s[b, :, h])) - (rm + np.log(rs))).max() < 1e-3
 
 
+def test_partial_d128_ranges_merge_to_full_attention():
+    """d = 128 (fwd128's triple epilogue): two ragged key ranges merged == attention over all keys."""
+    from paper_2112_05682_b200 import api
+    B, n_q, n_k, H, d = 1, 200, 700, 2, 128
+    q, k, v = Hh.host_inputs(B, n_q, n_k, H, d, seed=24)
+    ref, _ = O.mha_forward(q, k, v, 1 / math.sqrt(d))
+    qd = Hh.to_dev(q, torch.bfloat16)
+    parts = [api.mea_attention_partial_fwd(qd, Hh.to_dev(k[:, a:b], torch.bfloat16), Hh.to_dev(v[:, a:b], torch.bfloat16))
+             for a, b in ((0, 300), (300, n_k))]
+    out = api.mea_merge_partials(torch.stack([p_[0].reshape(-1) for p_ in parts]),
+                                 torch.stack([p_[1].reshape(-1) for p_ in parts]),
+                                 torch.stack([p_[2].reshape(-1, d) for p_ in parts]), B, n_q * H,
+                                 out_dtype=torch.float32).reshape(B, n_q, H, d)
+    torch.cuda.synchronize()
+    Hh.assert_close_bf16(out.double().cpu().numpy(), ref)
+
+
 def test_key_ranges_merge_to_full_attention():
     """Ragged key ranges, one of them empty, merged == attention over all keys."""
     from paper_2112_05682_b200 import api

@@ -41,6 +41,18 @@ def test_single_query_bf16(B, H, n_k):
         Hh.assert_close_bf16(out.double().cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("B,H,n_k", [(1, 1, 1), (2, 3, 1000), (1, 2, 70001)])
+def test_single_query_bf16_d128(B, H, n_k):
+    """d = 128: 16 lanes per 256-byte key row, two key groups per warp."""
+    from paper_2112_05682_b200 import api
+    q, k, v = _sq_inputs(B, H, n_k, 128, seed=n_k + 1)
+    ref = _ref(q, k, v, 1 / math.sqrt(128))
+    out = api.mea_single_query_fwd(Hh.to_dev(q, torch.bfloat16), Hh.to_dev(k, torch.bfloat16),
+                                   Hh.to_dev(v, torch.bfloat16), out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    Hh.assert_close_bf16(out.double().cpu().numpy(), ref)
+
+
 @pytest.mark.parametrize("d,n_k", [(64, 3000), (5, 100), (128, 777)])
 def test_single_query_f32(d, n_k):
     from paper_2112_05682_b200 import api
