@@ -31,9 +31,8 @@
  *      workspace smaller than needed  -> MEA_ERR_WORKSPACE_TOO_SMALL
  *      CUDA launch/encode failure     -> MEA_ERR_CUDA (detail in mea_last_error_detail)
  *  - Non-finite input values are not checked; they propagate.
- *  - Supported: bf16 inputs with d = 64 (all entry points) or d = 128 (all but the key-chunk
- *    schedule of mea_attention_fwd) on tcgen05 tensor-core kernels (single query: streaming
- *    SIMT kernels); f32 inputs with 1 <= d <= 128 (exact-f32 SIMT kernels, forward and
+ *  - Supported: bf16 inputs with d = 64 or d = 128 on every entry point (tcgen05 tensor-core
+ *    kernels; single query: streaming SIMT kernels); f32 inputs with 1 <= d <= 128 (exact-f32 SIMT kernels, forward and
  *    single query).
  */
 #ifndef MEA_H_
@@ -87,8 +86,7 @@ MEA_API const char* mea_last_error_detail(void);
  *     query chunks does, so only one chunk's summaries are alive:
  *     workspace = splits * B * H * min(n_q, q_chunk') * (d + 2) * 4 bytes. Without a key
  *     split q_chunk has no effect. Results do not depend on q_chunk.
- *   in_dtype MEA_BF16 requires d in {64, 128} (key chunks: d == 64) and out_dtype in
- *   {BF16, F32};
+ *   in_dtype MEA_BF16 requires d in {64, 128} and out_dtype in {BF16, F32};
  *   in_dtype MEA_F32 requires d <= 128, out_dtype F32 and k_chunk == 0.
  */
 MEA_API mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void* out,

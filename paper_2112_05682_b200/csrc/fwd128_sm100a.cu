@@ -57,12 +57,19 @@ __global__ void __launch_bounds__(kThreads128, 1)
   const int h = blockIdx.y, b = blockIdx.z;
   // causal (n_q == n_k): query tile qb needs key tiles [0, qb] (the last one is its diagonal);
   // the blocks with the most key tiles are scheduled first
-  const int qb = p.causal ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;
-  const int q0 = qb * 128;
+  // key split (the paper's key chunks): blockIdx.x = split * num_q_blocks + query block; the
+  // query blocks cover this launch's window [q_begin, q_begin + q_count)
+  const int qblk_raw = blockIdx.x % p.num_q_blocks;
+  const int qb = p.causal ? p.num_q_blocks - 1 - qblk_raw : qblk_raw;
+  const int split = blockIdx.x / p.num_q_blocks;
+  const int q0 = p.q_begin + qb * 128;
+  const int q_end = min(p.n_q, p.q_begin + p.q_count);
   const int n_tiles = (p.n_k + kTileN - 1) / kTileN;
-  const int T = p.causal ? min(n_tiles, qb + 1) : n_tiles;
+  const int t_begin = split * p.tiles_per_split;
+  const int t_end = p.causal ? min(n_tiles, qb + 1) : min(n_tiles, t_begin + p.tiles_per_split);
+  const int T = t_end - t_begin;
   const int diag = p.causal ? qb : -1;
-  const int key_end = p.n_k;
+  const int key_end = min(p.n_k, t_end * kTileN);
 
   if (threadIdx.x == 0) {
     mbar_init(&sm.q_full, 1);
@@ -102,7 +109,7 @@ __global__ void __launch_bounds__(kThreads128, 1)
     for (int t = 0; t < T; ++t) {
       const int st = t % kStages128, n = t / kStages128;
       if (t >= kStages128) mbar_wait(&sm.kv_empty[st], (n - 1) & 1);
-      const int krow = t * kTileN;
+      const int krow = (t_begin + t) * kTileN;
       if (elect_one()) {
         mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTile128Bytes);
         tma_load_4d(sm.k[st], &mk, &sm.kv_full[st], 0, h, krow, b, keep);
@@ -184,10 +191,10 @@ __global__ void __launch_bounds__(kThreads128, 1)
       mbar_wait(&sm.s_full[buf], (t >> 1) & 1);
       tc_fence_after();
       uint32_t sr[64];
-      const int tile_valid = (p.causal ? min(key_end, row + 1) : key_end) - t * kTileN;  // keys <= row if causal
+      const int tile_valid = (p.causal ? min(key_end, row + 1) : key_end) - (t_begin + t) * kTileN;  // keys <= row if causal
       const int valid = tile_valid - half * 64;
       uint32_t pk[32];
-      bool fast = (t > 0) && (t != diag) && (key_end - t * kTileN >= kTileN) && (c >= 0.f);
+      bool fast = (t > 0) && (t != diag) && (key_end - (t_begin + t) * kTileN >= kTileN) && (c >= 0.f);
       tmem_ld32_split<64>(lane_base + colS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
       if (fast) {
         tmem_ld_wait();
@@ -285,7 +292,7 @@ __global__ void __launch_bounds__(kThreads128, 1)
     tmem_ld32_split<64>(lane_base + kColO, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
     tmem_ld32_split<64>(lane_base + kColO + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
     tmem_ld_wait();
-    if (row < p.n_q && p.tri_v) {
+    if (row < q_end && p.tri_v) {
       // this call's (m*, s*, v*) per row, for a merge across key ranges
       const size_t idx = ((size_t)b * p.n_q + row) * p.H + h;
       float4* dst = reinterpret_cast<float4*>(p.tri_v + idx * kD + half * 64);
@@ -297,7 +304,15 @@ __global__ void __launch_bounds__(kThreads128, 1)
         p.tri_m[idx] = m_ref * 0.6931471805599453f;
         p.tri_s[idx] = lrow;
       }
-    } else if (row < p.n_q) {
+    } else if (row < q_end && p.num_splits > 1) {
+      const size_t prow = ((size_t)split * p.B * p.H + (size_t)b * p.H + h) * p.q_count + (row - p.q_begin);
+      float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kD + half * 64);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]), __uint_as_float(o[4 * i + 2]),
+                             __uint_as_float(o[4 * i + 3]));
+      if (half == 0) reinterpret_cast<float2*>(p.part_ml)[prow] = make_float2(m_ref, lrow);
+    } else if (row < q_end) {
       const size_t bh = (size_t)b * p.H + h;
       const float inv = 1.f / lrow;
       const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kD + half * 64;
@@ -337,7 +352,7 @@ cudaError_t launch_fwd128_bf16(const FwdParams& p, const CUtensorMap& mq, const 
   static cudaError_t attr = cudaFuncSetAttribute(fwd128_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)kFwd128SmemBytes);
   if (attr != cudaSuccess) return attr;
-  dim3 grid((p.n_q + 127) / 128, p.H, p.B);
+  dim3 grid(p.num_q_blocks * p.num_splits, p.H, p.B);
   fwd128_bf16_kernel<<<grid, kThreads128, kFwd128SmemBytes, s>>>(mq, mk, mv, p);
   return cudaGetLastError();
 }

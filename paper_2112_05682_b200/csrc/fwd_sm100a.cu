@@ -468,27 +468,30 @@ __global__ void merge_rows_kernel(const FwdParams p) {
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
   const int64_t stride = rows;  // rows per split
+  const int d = p.d, per = d / 32;  // 2 (d = 64) or 4 (d = 128) features per lane
   const float2* ml = reinterpret_cast<const float2*>(p.part_ml);
   float M = -INFINITY;
   for (int s = 0; s < p.num_splits; ++s) M = fmaxf(M, ml[s * stride + r].x);
-  float den = 0.f, a0 = 0.f, a1 = 0.f;
+  float den = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
   for (int s = 0; s < p.num_splits; ++s) {
     const float2 t = ml[s * stride + r];
     const float w = ex2_approx(t.x - M);
     den += w * t.y;
-    const float2 o = reinterpret_cast<const float2*>(p.part_o + (s * stride + r) * kHeadDim)[lane];
-    a0 += w * o.x;
-    a1 += w * o.y;
+    const float* o = p.part_o + (s * stride + r) * d + per * lane;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < per) acc[i] += w * o[i];
   }
   const int64_t bh = r / p.q_count, row = p.q_begin + r % p.q_count;
   if (row >= p.n_q) return;
   const int64_t b = bh / p.H, h = bh % p.H;
-  const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + 2 * lane;
+  const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * d + per * lane;
   const float inv = 1.f / den;
-  if (p.out_f32) {
-    reinterpret_cast<float2*>(static_cast<float*>(p.out) + off)[0] = make_float2(a0 * inv, a1 * inv);
-  } else {
-    reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(p.out) + off)[0] = pack_bf16x2(a0 * inv, a1 * inv);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i >= per) break;
+    if (p.out_f32) static_cast<float*>(p.out)[off + i] = acc[i] * inv;
+    else static_cast<__nv_bfloat16*>(p.out)[off + i] = __float2bfloat16_rn(acc[i] * inv);
   }
   if (p.lse && lane == 0) p.lse[bh * p.n_q + row] = (M + __log2f(den)) * 0.6931471805599453f;
 }

@@ -28,6 +28,7 @@ struct FwdParams {
   float* tri_s;            //   [B,n_q,H] s*
   float* tri_v;            //   [B,n_q,H,64] v* (unnormalised)
   int causal;              // query i sees keys j <= i (n_q == n_k, one window, no key split)
+  int d;                   // head dimension (64: fwd_bf16, 128: fwd128_bf16); merge_rows reads it
 };
 
 struct BwdParams {

@@ -123,7 +123,7 @@ struct FwdPlan {
 // rows are processed in windows of q_chunk rows (rounded up to the 256-row CTA), one after the
 // other, as Figure 1's outer map over query chunks does, so the summaries of
 // only one query chunk are alive at a time: workspace = splits * B * H * q_window * (d + 2) f32.
-FwdPlan plan_fwd(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t q_chunk, int64_t k_chunk) {
+FwdPlan plan_fwd(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t q_chunk, int64_t k_chunk, int64_t d) {
   FwdPlan pl;
   const int64_t n_tiles = (n_k + kTileN - 1) / kTileN;
   pl.tiles_per_split = (int)n_tiles;
@@ -135,7 +135,7 @@ FwdPlan plan_fwd(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t q_chunk
       pl.splits = (int)splits;
       pl.tiles_per_split = (int)tps;
       if (q_chunk > 0) pl.q_window = std::min(n_q, (q_chunk + kRowsPerCta - 1) / kRowsPerCta * kRowsPerCta);
-      pl.ws = (size_t)splits * B * H * pl.q_window * (kHeadDim + 2) * sizeof(float);
+      pl.ws = (size_t)splits * B * H * pl.q_window * (d + 2) * sizeof(float);
     }
   }
   return pl;
@@ -176,7 +176,8 @@ mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
   if (q_chunk < 0 || k_chunk < 0) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
   if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  *bytes = (in_dtype == MEA_BF16 && d == kHeadDim) ? plan_fwd(B, H, n_q, n_k, q_chunk, k_chunk).ws : 0;
+  *bytes = (in_dtype == MEA_BF16 && (d == kHeadDim || d == 128)) ? plan_fwd(B, H, n_q, n_k, q_chunk, k_chunk, d).ws
+                                                                   : 0;
   return MEA_OK;
 }
 
@@ -211,40 +212,14 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
     return e == cudaSuccess ? MEA_OK : cuda_fail(e, "fwd_f32 launch");
   }
 
-  if (d == 128) {  // fwd128_sm100a.cu: online schedule only
-    if (k_chunk > 0 && k_chunk < n_k) return fail(MEA_ERR_UNSUPPORTED, "key chunks: d == 64 only");
-    CUtensorMap mq, mk, mv;
-    const char* why = "";
-    cudaError_t e;
-    if ((e = make_bnhd_map(&mq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_q, H, d, 64, kTileM,
-                           CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
-        (e = make_bnhd_map(&mk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
-                           CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
-        (e = make_bnhd_map(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
-                           CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess)
-      return cuda_fail(e, why);
-    FwdParams p{};
-    p.B = (int)B;
-    p.H = (int)H;
-    p.n_q = (int)n_q;
-    p.n_k = (int)n_k;
-    p.scale = scale;
-    p.scale_log2 = scale * 1.4426950408889634f;
-    p.out = out;
-    p.out_f32 = out_dtype == MEA_F32;
-    p.lse = lse;
-    p.causal = causal ? 1 : 0;
-    ProfScope ps("fwd128_bf16", st);
-    if ((e = launch_fwd128_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd128_bf16 launch");
-    return MEA_OK;
-  }
-  if (d != kHeadDim) return fail(MEA_ERR_UNSUPPORTED, "bf16 tensor-core path supports d in {64, 128}");
-  const FwdPlan pl = plan_fwd(B, H, n_q, n_k, q_chunk, k_chunk);
+  if (d != kHeadDim && d != 128) return fail(MEA_ERR_UNSUPPORTED, "bf16 tensor-core path supports d in {64, 128}");
+  const FwdPlan pl = plan_fwd(B, H, n_q, n_k, q_chunk, k_chunk, d);
+  const int rows_per_cta = d == 128 ? 128 : kRowsPerCta;  // fwd128: one query tile per CTA
   if (pl.ws > 0) {
     if (workspace_bytes < pl.ws || !workspace) return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "key-chunk summaries need workspace");
     if (!aligned16(workspace)) return fail(MEA_ERR_MISALIGNED, "workspace must be 16-byte aligned");
   }
-  const int64_t nqb = (n_q + kRowsPerCta - 1) / kRowsPerCta;
+  const int64_t nqb = (n_q + rows_per_cta - 1) / rows_per_cta;
   if (nqb * pl.splits > kMaxInt) return fail(MEA_ERR_UNSUPPORTED, "grid too large");
 
   CUtensorMap mq, mk, mv;
@@ -269,19 +244,23 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
   p.out_f32 = out_dtype == MEA_F32;
   p.lse = lse;
   p.causal = causal ? 1 : 0;
+  p.d = (int)d;
   p.num_splits = pl.splits;
   p.tiles_per_split = pl.tiles_per_split;
   if (pl.splits > 1) {
     const size_t rows = (size_t)pl.splits * B * H * pl.q_window;
     p.part_o = static_cast<float*>(workspace);
-    p.part_ml = p.part_o + rows * kHeadDim;
+    p.part_ml = p.part_o + rows * d;
   }
   // one window (all rows) unless the key-split schedule runs query chunk by query chunk
   for (int64_t w0 = 0; w0 < n_q; w0 += pl.q_window) {
     p.q_begin = (int)w0;
     p.q_count = (int)std::min<int64_t>(pl.q_window, n_q - w0);
-    p.num_q_blocks = (p.q_count + kRowsPerCta - 1) / kRowsPerCta;
-    {
+    p.num_q_blocks = (p.q_count + rows_per_cta - 1) / rows_per_cta;
+    if (d == 128) {
+      ProfScope ps("fwd128_bf16", st);
+      if ((e = launch_fwd128_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd128_bf16 launch");
+    } else {
       ProfScope ps("fwd_bf16", st);
       if ((e = launch_fwd_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_bf16 launch");
     }
@@ -351,7 +330,8 @@ mea_status_t mea_attention_partial_fwd(const void* q, const void* k, const void*
   p.tiles_per_split = (int)((n_k + kTileN - 1) / kTileN);
   p.q_begin = 0;
   p.q_count = (int)n_q;
-  p.num_q_blocks = (int)((n_q + kRowsPerCta - 1) / kRowsPerCta);
+  p.num_q_blocks = (int)((n_q + (d == 128 ? 128 : kRowsPerCta) - 1) / (d == 128 ? 128 : kRowsPerCta));
+  p.d = (int)d;
   p.tri_m = m;
   p.tri_s = s;
   p.tri_v = vstar;

@@ -94,8 +94,11 @@ def test_host_only_validation_of_the_newer_entry_points(lib):
     assert lib.mea_attention_fwd_causal(p, p, p, p, 1, 1, 0, 64, 1, 1, 1.0, None, None) == 0
     assert lib.mea_attention_fwd_causal(p, p, p, p, 1, 1, 8, 32, 1, 1, 1.0, None, None) == 3  # d = 32
     assert lib.mea_attention_bwd_causal(p, p, p, p, p, p, p, p, 1, 1, 8, 64, 1, 0.0, None, None, 0, None) == 3
-    # key chunks at d = 128: unsupported; f32 key chunks: unsupported
-    assert lib.mea_attention_fwd(p, p, p, p, 1, 1, 300, 300, 128, 1, 1, 1.0, None, 0, 128, None, 0, None) == 3
+    # key chunks at d = 128 need their summaries' workspace (status 5); f32 key chunks: unsupported
+    assert lib.mea_attention_fwd(p, p, p, p, 1, 1, 300, 300, 128, 1, 1, 1.0, None, 0, 128, None, 0, None) == 5
+    n1 = ctypes.c_size_t(0)
+    assert lib.mea_attention_fwd_workspace_size(1, 2, 300, 300, 128, 1, 0, 128, ctypes.byref(n1)) == 0
+    assert n1.value == 3 * 2 * 300 * 130 * 4
     assert lib.mea_attention_fwd(p, p, p, p, 1, 1, 300, 300, 64, 0, 0, 1.0, None, 0, 128, None, 0, None) == 3
     # backward: d outside {64, 128}, f32 inputs
     assert lib.mea_attention_bwd(p, p, p, p, p, p, p, p, 1, 1, 8, 8, 32, 1, 1.0, None, None, 0, None) == 3

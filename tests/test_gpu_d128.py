@@ -2,8 +2,8 @@
 (fwd128_sm100a.cu) and the backward (bwd_det_sm100a.cu / bwd_dq_sm100a.cu at D = 128)
 against the float64 oracle (O1) on the same generated inputs: shapes over several query and key
 tiles with ragged tails, both output dtypes and scales, the rescale stress case, configs[2]'s
-length at d = 128 on sampled rows, and the explicit error of what d = 128 does not cover (key
-chunks). Causal attention at d = 128: tests/test_gpu_causal.py.
+length at d = 128 on sampled rows, and the key-chunk schedule. Causal attention at d = 128:
+tests/test_gpu_causal.py.
 """
 import math
 
@@ -18,10 +18,11 @@ pytestmark = pytest.mark.gpu
 D = 128
 
 
-def _run(q, k, v, scale=None, out_dtype=None):
+def _run(q, k, v, scale=None, out_dtype=None, **kw):
     from paper_2112_05682_b200 import api
     out, lse = api.mea_attention_fwd(Hh.to_dev(q, torch.bfloat16), Hh.to_dev(k, torch.bfloat16),
-                                     Hh.to_dev(v, torch.bfloat16), scale=scale, out_dtype=out_dtype, want_lse=True)
+                                     Hh.to_dev(v, torch.bfloat16), scale=scale, out_dtype=out_dtype, want_lse=True,
+                                     **kw)
     torch.cuda.synchronize()
     return out.double().cpu().numpy(), lse.double().cpu().numpy()
 
@@ -79,11 +80,15 @@ def test_d128_long_sequence_sampled_rows():
         assert np.abs(lse[0, h, rows].double().cpu().numpy() - ref_lse).max() < 1e-3
 
 
-def test_d128_unsupported_paths_fail_loudly():
-    from paper_2112_05682_b200 import api
-    q = torch.zeros(1, 256, 1, D, dtype=torch.bfloat16, device="cuda")
-    with pytest.raises(api.MeaError):
-        api.mea_attention_fwd(q, q, q, k_chunk=128)            # key chunks: d = 64 only
+def test_d128_key_chunk_schedule():
+    """Figure 1's key-chunk summaries at d = 128 (fwd128 split mode + merge_rows), with and without
+    query-chunk windows, equal the oracle."""
+    q, k, v = Hh.host_inputs(2, 300, 1100, 2, D, seed=46)
+    ref, ref_lse = O.mha_forward(q, k, v, 0.1)
+    for qc, kc in ((0, 256), (128, 300), (1000, 128)):
+        got, lse = _run(q, k, v, scale=0.1, q_chunk=qc, k_chunk=kc)
+        Hh.assert_close_bf16(got, ref)
+        assert np.abs(lse - ref_lse).max() < 1e-3
 
 
 @pytest.mark.parametrize("B,n_q,n_k,H,lse_given", [(1, 130, 300, 2, True), (2, 257, 129, 1, True),
