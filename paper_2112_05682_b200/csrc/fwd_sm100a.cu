@@ -52,9 +52,15 @@ constexpr int kTileBytes = kTileN * kHeadDim * 2;  // 16 KiB: 128 rows x 128 B
 constexpr int kThreads = 640;  // 4 producer/MMA/alloc warps + 4 softmax warpgroups
 // setmaxnreg.inc can only redistribute the registers the CTA was launched with (640 x 96:
 // 480 per lane slot of an SM sub-partition, which holds 1 control + 4 softmax warps); a larger
-// total blocks forever (measured). 64 + 4 * 104 = 480.
-constexpr int kSoftmaxRegs = 104;
-constexpr int kControlRegs = 56;
+// total blocks forever (measured).
+// 112 / 32 (32 + 4 * 112 = 480): the softmax's scores, P pairs and the redo copy spilled at 104
+// (76 bytes per thread, ~4 % of the kernel time); the producer / MMA-issuer warps fit in 32.
+#ifndef MEA_FREG_SOFT
+#define MEA_FREG_SOFT 112
+#define MEA_FREG_CTRL 32
+#endif
+constexpr int kSoftmaxRegs = MEA_FREG_SOFT;
+constexpr int kControlRegs = MEA_FREG_CTRL;
 __host__ __device__ constexpr uint32_t col_s(int wg) { return wg ? 128u : 0u; }
 __host__ __device__ constexpr uint32_t col_o(int wg) { return wg ? 320u : 256u; }
 __host__ __device__ constexpr uint32_t col_p(int wg) { return wg ? 448u : 384u; }
