@@ -51,7 +51,14 @@
 extern "C" {
 #endif
 
-typedef enum { MEA_F32 = 0, MEA_BF16 = 1 } mea_dtype_t;
+/*
+ * MEA_F32_SPLIT (mea_attention_fwd's in_dtype only): float32 tensors computed on the bf16 tensor
+ * cores by split precision (q, k in three bf16 parts, v and P in two; d == 64, float32 output,
+ * no key chunks, not causal). Scores and the lse are fp32-accurate; each output element is within
+ * 3 * 2^-18 * max|v| (~1.1e-5 max|v|) of exact — the P.V terms keep 16 bits. MEA_F32 is exact
+ * fp32 FFMA arithmetic (any d <= 128) and is what the fp32 parity bar of BASELINE.json is held to.
+ */
+typedef enum { MEA_F32 = 0, MEA_BF16 = 1, MEA_F32_SPLIT = 2 } mea_dtype_t;
 
 typedef enum {
   MEA_OK = 0,

@@ -82,15 +82,23 @@ def mea_attention_fwd_workspace_size(B, H, n_q, n_k, d, in_dtype, q_chunk=0, k_c
     return n.value
 
 
+MEA_F32_SPLIT = 2
+
+
 def mea_attention_fwd(q, k, v, scale=None, out=None, out_dtype=None, lse=None, want_lse=False,
-                      q_chunk=0, k_chunk=0, workspace=None):
-    """out = attention(q, k, v) (Figure 1). Returns out, or (out, lse)."""
+                      q_chunk=0, k_chunk=0, workspace=None, f32_split=False):
+    """out = attention(q, k, v) (Figure 1). Returns out, or (out, lse).
+    f32_split: float32 inputs on the tensor cores by split precision (MEA_F32_SPLIT, mea.h)."""
     _cuda_contig(q, k, v, out, lse)
     B, n_q, H, d = q.shape
     n_k = k.shape[1]
     if k.shape != (B, n_k, H, d) or v.shape != k.shape:
         raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
     dt = _dtype(q)
+    if f32_split:
+        if dt != MEA_F32:
+            raise TypeError("f32_split needs float32 inputs")
+        dt = MEA_F32_SPLIT
     if k.dtype != q.dtype or v.dtype != q.dtype:
         raise TypeError("q, k, v must share a dtype")
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)

@@ -141,6 +141,11 @@ FwdPlan plan_fwd(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t q_chunk
   return pl;
 }
 
+// f32 inputs at d = 64: bf16 parts of q, k (three each) and v (two): 6 + 6 + 4 bytes per element
+size_t f32tc_workspace(int64_t B, int64_t H, int64_t n_q, int64_t n_k) {
+  return (size_t)B * H * kHeadDim * (6 * n_q + 10 * n_k);
+}
+
 mea_status_t check_common(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d, float scale) {
   if (B < 1 || H < 1 || d < 1 || n_q < 0 || n_k < 0) return fail(MEA_ERR_INVALID_VALUE, "B, H, d must be >= 1; n >= 0");
   if (!std::isfinite(scale)) return fail(MEA_ERR_INVALID_VALUE, "scale must be finite");
@@ -175,9 +180,13 @@ mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
   if (!bytes) return fail(MEA_ERR_INVALID_VALUE, "bytes is NULL");
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
   if (q_chunk < 0 || k_chunk < 0) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
-  if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  *bytes = (in_dtype == MEA_BF16 && (d == kHeadDim || d == 128)) ? plan_fwd(B, H, n_q, n_k, q_chunk, k_chunk, d).ws
-                                                                   : 0;
+  if (!valid_dtype(in_dtype) && in_dtype != MEA_F32_SPLIT) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  if (in_dtype == MEA_F32_SPLIT)
+    *bytes = (d == kHeadDim) ? f32tc_workspace(B, H, n_q, n_k) : 0;
+  else if (in_dtype == MEA_F32)
+    *bytes = 0;
+  else
+    *bytes = (d == kHeadDim || d == 128) ? plan_fwd(B, H, n_q, n_k, q_chunk, k_chunk, d).ws : 0;
   return MEA_OK;
 }
 
@@ -192,7 +201,10 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
   if (causal && in_dtype != MEA_BF16) return fail(MEA_ERR_UNSUPPORTED, "causal attention: bf16 path only");
   if (causal) q_chunk = k_chunk = 0;  // causal runs the online schedule (no key split)
   if (q_chunk < 0 || k_chunk < 0) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
-  if (!valid_dtype(in_dtype) || !valid_dtype(out_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  if ((!valid_dtype(in_dtype) && in_dtype != MEA_F32_SPLIT) || !valid_dtype(out_dtype))
+    return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  if (in_dtype == MEA_F32_SPLIT && (d != kHeadDim || out_dtype != MEA_F32 || causal || (k_chunk > 0 && k_chunk < n_k)))
+    return fail(MEA_ERR_UNSUPPORTED, "MEA_F32_SPLIT: d == 64, float32 output, no key chunks, not causal");
   if (n_q == 0) return MEA_OK;
   if (n_k == 0) return fail(MEA_ERR_EMPTY_KEYS, "attention over an empty key list");
   if (!q || !k || !v || !out) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
@@ -201,10 +213,52 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
   if (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)) return fail(MEA_ERR_MISALIGNED, "lse must be 4-byte aligned");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
-  if (in_dtype == MEA_F32) {
+  if (in_dtype == MEA_F32 || in_dtype == MEA_F32_SPLIT) {
     if (d > 128) return fail(MEA_ERR_UNSUPPORTED, "f32 path supports d <= 128");
     if (out_dtype != MEA_F32) return fail(MEA_ERR_UNSUPPORTED, "f32 inputs need f32 output");
     if (k_chunk > 0 && k_chunk < n_k) return fail(MEA_ERR_UNSUPPORTED, "key chunking is a bf16-path schedule");
+    if (in_dtype == MEA_F32_SPLIT) {
+      // split-precision tensor-core path (fwd_f32tc_sm100a.cu): q, k, v -> bf16 hi/lo in the workspace
+      const size_t need = f32tc_workspace(B, H, n_q, n_k);
+      if (!workspace || workspace_bytes < need) return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "f32 split workspace");
+      if (!aligned16(workspace)) return fail(MEA_ERR_MISALIGNED, "workspace must be 16-byte aligned");
+      uint8_t* w = static_cast<uint8_t*>(workspace);
+      const size_t nq_el = (size_t)B * n_q * H * d, nk_el = (size_t)B * n_k * H * d;
+      // q, k: three bf16 parts each; v: two
+      void* qp[3] = {w, w + nq_el * 2, w + nq_el * 4};
+      uint8_t* wk = w + nq_el * 6;
+      void* kp[3] = {wk, wk + nk_el * 2, wk + nk_el * 4};
+      uint8_t* wv = wk + nk_el * 6;
+      void* vp[2] = {wv, wv + nk_el * 2};
+      cudaError_t e;
+      {
+        ProfScope ps("split_f32", st);
+        if ((e = launch_split_f32(static_cast<const float*>(q), qp, 3, (int64_t)nq_el, st)) != cudaSuccess ||
+            (e = launch_split_f32(static_cast<const float*>(k), kp, 3, (int64_t)nk_el, st)) != cudaSuccess ||
+            (e = launch_split_f32(static_cast<const float*>(v), vp, 2, (int64_t)nk_el, st)) != cudaSuccess)
+          return cuda_fail(e, "split_f32 launch");
+      }
+      CUtensorMap maps[8];
+      const char* why = "";
+      const void* bases[8] = {qp[0], qp[1], qp[2], kp[0], kp[1], kp[2], vp[0], vp[1]};
+      for (int i = 0; i < 8; ++i)
+        if ((e = make_bnhd_map(&maps[i], bases[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, i < 3 ? n_q : n_k, H, d,
+                               64, 128, CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess)
+          return cuda_fail(e, why);
+      FwdParams p{};
+      p.B = (int)B;
+      p.H = (int)H;
+      p.n_q = (int)n_q;
+      p.n_k = (int)n_k;
+      p.scale = scale;
+      p.scale_log2 = scale * 1.4426950408889634f;
+      p.out = out;
+      p.out_f32 = 1;
+      p.lse = lse;
+      ProfScope ps("fwd_f32tc", st);
+      if ((e = launch_fwd_f32tc(p, maps, st)) != cudaSuccess) return cuda_fail(e, "fwd_f32tc launch");
+      return MEA_OK;
+    }
     ProfScope ps("fwd_f32", st);
     cudaError_t e = launch_fwd_f32(static_cast<const float*>(q), static_cast<const float*>(k),
                                    static_cast<const float*>(v), static_cast<float*>(out), lse, (int)B, (int)H,

@@ -73,6 +73,8 @@ def test_host_only_calls(lib):
                                  None) == 0  # n_q == 0 no-op
     assert lib.mea_attention_fwd(None, None, None, None, 0, 1, 4, 5, 64, 1, 1, 1.0, None, 0, 0, None, 0,
                                  None) == 1
+    assert lib.mea_attention_fwd(None, None, None, None, 1, 1, 4, 5, 64, 2, 1, 1.0, None, 0, 0, None, 0,
+                                 None) == 3  # MEA_F32_SPLIT needs float32 output
     assert lib.mea_attention_fwd(None, None, None, None, 1, 1, 4, 5, 64, 7, 1, 1.0, None, 0, 0, None, 0,
                                  None) == 1  # bad dtype
     assert lib.mea_attention_fwd(None, None, None, None, 1, 1, 4, 5, 64, 1, 1, float("nan"), None, 0, 0, None,
