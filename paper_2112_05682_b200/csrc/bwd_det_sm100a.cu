@@ -361,8 +361,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
 template <int D>
 static cudaError_t launch_bwd_dkdv_d(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                                      const CUtensorMap& mv, const CUtensorMap& mdo, cudaStream_t s) {
-  static cudaError_t attr = cudaFuncSetAttribute(bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)dkv_smem_bytes<D>());
+  const cudaError_t attr = ensure_smem_attr<bwd_dkdv_kernel<D>>((int)dkv_smem_bytes<D>());
   if (attr != cudaSuccess) return attr;
   dim3 grid(p.num_k_blocks, p.H, p.B);
   bwd_dkdv_kernel<D><<<grid, kBThreads, dkv_smem_bytes<D>(), s>>>(mq, mk, mv, mdo, p);

@@ -299,8 +299,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
 template <int D>
 static cudaError_t launch_bwd_dq_d(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                                    const CUtensorMap& mv, const CUtensorMap& mdo, cudaStream_t s) {
-  static cudaError_t attr =
-      cudaFuncSetAttribute(bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dq_smem_bytes<D>());
+  const cudaError_t attr = ensure_smem_attr<bwd_dq_kernel<D>>((int)dq_smem_bytes<D>());
   if (attr != cudaSuccess) return attr;
   dim3 grid((p.n_q + kTile - 1) / kTile, p.H, p.B);
   bwd_dq_kernel<D><<<grid, kQThreads, dq_smem_bytes<D>(), s>>>(mq, mk, mv, mdo, p);

@@ -486,8 +486,7 @@ cudaError_t launch_bwd_preprocess(const void* out, const void* dout, const float
 
 cudaError_t launch_bwd_bf16(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                             const CUtensorMap& mdo, const CUtensorMap& mdq, cudaStream_t s) {
-  static cudaError_t attr =
-      cudaFuncSetAttribute(bwd_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmemBytes);
+  const cudaError_t attr = ensure_smem_attr<bwd_bf16_kernel>((int)kBwdSmemBytes);
   if (attr != cudaSuccess) return attr;
   dim3 grid(p.num_k_blocks, p.H, p.B);
   bwd_bf16_kernel<<<grid, kBThreads, kBwdSmemBytes, s>>>(mq, mk, mv, mdo, mdq, p);

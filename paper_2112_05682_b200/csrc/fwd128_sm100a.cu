@@ -349,8 +349,7 @@ __global__ void __launch_bounds__(kThreads128, 1)
 
 cudaError_t launch_fwd128_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                                const CUtensorMap& mv, cudaStream_t s) {
-  static cudaError_t attr = cudaFuncSetAttribute(fwd128_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)kFwd128SmemBytes);
+  const cudaError_t attr = ensure_smem_attr<fwd128_bf16_kernel>((int)kFwd128SmemBytes);
   if (attr != cudaSuccess) return attr;
   dim3 grid(p.num_q_blocks * p.num_splits, p.H, p.B);
   fwd128_bf16_kernel<<<grid, kThreads128, kFwd128SmemBytes, s>>>(mq, mk, mv, p);

@@ -306,8 +306,7 @@ cudaError_t launch_split_f32(const float* x, void* const* parts, int nparts, int
 }
 
 cudaError_t launch_fwd_f32tc(const FwdParams& p, const CUtensorMap (&maps)[8], cudaStream_t s) {
-  static cudaError_t attr =
-      cudaFuncSetAttribute(fwd_f32tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmemBytes);
+  const cudaError_t attr = ensure_smem_attr<fwd_f32tc_kernel>((int)kTcSmemBytes);
   if (attr != cudaSuccess) return attr;
   SplitMaps m{maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7]};
   dim3 grid((p.n_q + 127) / 128, p.H, p.B);

@@ -579,8 +579,7 @@ __global__ void __launch_bounds__(128, 1)
 
 cudaError_t launch_fwd_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                             const CUtensorMap& mv, cudaStream_t s) {
-  static cudaError_t attr = cudaFuncSetAttribute(fwd_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)kFwdSmemBytes);
+  const cudaError_t attr = ensure_smem_attr<fwd_bf16_kernel>((int)kFwdSmemBytes);
   if (attr != cudaSuccess) return attr;
   dim3 grid(p.num_q_blocks * p.num_splits, p.H, p.B);
   fwd_bf16_kernel<<<grid, kThreads, kFwdSmemBytes, s>>>(mq, mk, mv, p);

@@ -4,7 +4,25 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 namespace mea {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute is per
+// device, and one process may drive several GPUs (a plain function-local static would set it on
+// the first device only).
+template <auto Kernel>
+inline cudaError_t ensure_smem_attr(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+  return e;
+}
 
 constexpr int kHeadDim = 64;      // tensor-core path head dimension
 constexpr int kTileM = 128;       // query rows per softmax warpgroup (UMMA M)
