@@ -98,7 +98,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   BwdSmem<D>& sm = *reinterpret_cast<BwdSmem<D>*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  // causal: 1-D grid, key block 0 (the most query tiles) first across all (b, h)
+  const int kblk = p.causal ? (int)(blockIdx.x / (p.H * p.B)) : (int)blockIdx.x;
+  const int h = p.causal ? (int)(blockIdx.x % p.H) : (int)blockIdx.y;
+  const int b = p.causal ? (int)((blockIdx.x / p.H) % p.B) : (int)blockIdx.z;
   const int k0 = kblk * kTile;
   const int NQ = (p.n_q + QT - 1) / QT;
   // causal (n_q == n_k): query tiles before this key tile see none of its keys; iteration i
@@ -363,7 +366,7 @@ static cudaError_t launch_bwd_dkdv_d(const BwdParams& p, const CUtensorMap& mq, 
                                      const CUtensorMap& mv, const CUtensorMap& mdo, cudaStream_t s) {
   const cudaError_t attr = ensure_smem_attr<bwd_dkdv_kernel<D>>((int)dkv_smem_bytes<D>());
   if (attr != cudaSuccess) return attr;
-  dim3 grid(p.num_k_blocks, p.H, p.B);
+  const dim3 grid = p.causal ? dim3(p.num_k_blocks * p.H * p.B) : dim3(p.num_k_blocks, p.H, p.B);
   bwd_dkdv_kernel<D><<<grid, kBThreads, dkv_smem_bytes<D>(), s>>>(mq, mk, mv, mdo, p);
   return cudaGetLastError();
 }

@@ -73,7 +73,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   DqSmem<D>& sm = *reinterpret_cast<DqSmem<D>*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  // causal: 1-D grid, the last query block (the most key tiles) first across all (b, h)
+  const int nqb = (p.n_q + kTile - 1) / kTile;
+  const int qblk = p.causal ? nqb - 1 - (int)(blockIdx.x / (p.H * p.B)) : (int)blockIdx.x;
+  const int h = p.causal ? (int)(blockIdx.x % p.H) : (int)blockIdx.y;
+  const int b = p.causal ? (int)((blockIdx.x / p.H) % p.B) : (int)blockIdx.z;
   const int q0 = qblk * kTile;
   // causal (n_q == n_k): keys up to this block's last query row only
   const int T = p.causal ? min((p.n_k + KT - 1) / KT, (q0 + kTile + KT - 1) / KT) : (p.n_k + KT - 1) / KT;
@@ -301,7 +305,8 @@ static cudaError_t launch_bwd_dq_d(const BwdParams& p, const CUtensorMap& mq, co
                                    const CUtensorMap& mv, const CUtensorMap& mdo, cudaStream_t s) {
   const cudaError_t attr = ensure_smem_attr<bwd_dq_kernel<D>>((int)dq_smem_bytes<D>());
   if (attr != cudaSuccess) return attr;
-  dim3 grid((p.n_q + kTile - 1) / kTile, p.H, p.B);
+  const int nqb = (p.n_q + kTile - 1) / kTile;
+  const dim3 grid = p.causal ? dim3(nqb * p.H * p.B) : dim3(nqb, p.H, p.B);
   bwd_dq_kernel<D><<<grid, kQThreads, dq_smem_bytes<D>(), s>>>(mq, mk, mv, mdo, p);
   return cudaGetLastError();
 }

@@ -101,7 +101,10 @@ __global__ void __launch_bounds__(kBThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   BwdSmem& sm = *reinterpret_cast<BwdSmem*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kblk = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  // causal: 1-D grid, key block 0 (the most query tiles) first across all (b, h)
+  const int kblk = p.causal ? (int)(blockIdx.x / (p.H * p.B)) : (int)blockIdx.x;
+  const int h = p.causal ? (int)(blockIdx.x % p.H) : (int)blockIdx.y;
+  const int b = p.causal ? (int)((blockIdx.x / p.H) % p.B) : (int)blockIdx.z;
   const int k0 = kblk * kTile;
   const int NQ = (p.n_q + kTile - 1) / kTile;
   // causal (n_q == n_k): queries before this key tile see none of its keys; iteration i
@@ -488,7 +491,7 @@ cudaError_t launch_bwd_bf16(const BwdParams& p, const CUtensorMap& mq, const CUt
                             const CUtensorMap& mdo, const CUtensorMap& mdq, cudaStream_t s) {
   const cudaError_t attr = ensure_smem_attr<bwd_bf16_kernel>((int)kBwdSmemBytes);
   if (attr != cudaSuccess) return attr;
-  dim3 grid(p.num_k_blocks, p.H, p.B);
+  const dim3 grid = p.causal ? dim3(p.num_k_blocks * p.H * p.B) : dim3(p.num_k_blocks, p.H, p.B);
   bwd_bf16_kernel<<<grid, kBThreads, kBwdSmemBytes, s>>>(mq, mk, mv, mdo, mdq, p);
   return cudaGetLastError();
 }

@@ -54,14 +54,14 @@ __global__ void __launch_bounds__(kThreads128, 1)
   extern __shared__ uint8_t smem_raw[];
   Fwd128Smem& sm = *reinterpret_cast<Fwd128Smem*>(align1024_128(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = blockIdx.y, b = blockIdx.z;
+  const int h = p.causal ? (int)(blockIdx.x % p.H) : (int)blockIdx.y;  // causal: 1-D grid, heaviest first
+  const int b = p.causal ? (int)((blockIdx.x / p.H) % p.B) : (int)blockIdx.z;
   // causal (n_q == n_k): query tile qb needs key tiles [0, qb] (the last one is its diagonal);
   // the blocks with the most key tiles are scheduled first
   // key split (the paper's key chunks): blockIdx.x = split * num_q_blocks + query block; the
   // query blocks cover this launch's window [q_begin, q_begin + q_count)
-  const int qblk_raw = blockIdx.x % p.num_q_blocks;
-  const int qb = p.causal ? p.num_q_blocks - 1 - qblk_raw : qblk_raw;
-  const int split = blockIdx.x / p.num_q_blocks;
+  const int qb = p.causal ? p.num_q_blocks - 1 - (int)(blockIdx.x / (p.H * p.B)) : (int)(blockIdx.x % p.num_q_blocks);
+  const int split = p.causal ? 0 : blockIdx.x / p.num_q_blocks;
   const int q0 = p.q_begin + qb * 128;
   const int q_end = min(p.n_q, p.q_begin + p.q_count);
   const int n_tiles = (p.n_k + kTileN - 1) / kTileN;
@@ -351,7 +351,7 @@ cudaError_t launch_fwd128_bf16(const FwdParams& p, const CUtensorMap& mq, const 
                                const CUtensorMap& mv, cudaStream_t s) {
   const cudaError_t attr = ensure_smem_attr<fwd128_bf16_kernel>((int)kFwd128SmemBytes);
   if (attr != cudaSuccess) return attr;
-  dim3 grid(p.num_q_blocks * p.num_splits, p.H, p.B);
+  const dim3 grid = p.causal ? dim3(p.num_q_blocks * p.H * p.B) : dim3(p.num_q_blocks * p.num_splits, p.H, p.B);
   fwd128_bf16_kernel<<<grid, kThreads128, kFwd128SmemBytes, s>>>(mq, mk, mv, p);
   return cudaGetLastError();
 }

@@ -128,9 +128,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   FwdSmem& sm = *reinterpret_cast<FwdSmem*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // causal: the blocks with the most key tiles (the last rows) are scheduled first
-  const int qblk = p.causal ? p.num_q_blocks - 1 - (int)(blockIdx.x % p.num_q_blocks) : blockIdx.x % p.num_q_blocks;
-  const int split = blockIdx.x / p.num_q_blocks;
-  const int h = blockIdx.y, b = blockIdx.z;
+  // causal: a 1-D grid ordered heaviest block first across all (b, h) (the block scheduler then
+  // runs a longest-job-first schedule); otherwise x = split * num_q_blocks + block, y = h, z = b
+  const int cidx = blockIdx.x / (p.H * p.B);
+  const int qblk = p.causal ? p.num_q_blocks - 1 - cidx : blockIdx.x % p.num_q_blocks;
+  const int split = p.causal ? 0 : blockIdx.x / p.num_q_blocks;
+  const int h = p.causal ? (int)(blockIdx.x % p.H) : (int)blockIdx.y;
+  const int b = p.causal ? (int)((blockIdx.x / p.H) % p.B) : (int)blockIdx.z;
   const int q0 = p.q_begin + qblk * kRowsPerCta;
   const int q_end = min(p.n_q, p.q_begin + p.q_count);
   const int n_tiles = (p.n_k + kTileN - 1) / kTileN;
@@ -581,7 +585,7 @@ cudaError_t launch_fwd_bf16(const FwdParams& p, const CUtensorMap& mq, const CUt
                             const CUtensorMap& mv, cudaStream_t s) {
   const cudaError_t attr = ensure_smem_attr<fwd_bf16_kernel>((int)kFwdSmemBytes);
   if (attr != cudaSuccess) return attr;
-  dim3 grid(p.num_q_blocks * p.num_splits, p.H, p.B);
+  const dim3 grid = p.causal ? dim3(p.num_q_blocks * p.H * p.B) : dim3(p.num_q_blocks * p.num_splits, p.H, p.B);
   fwd_bf16_kernel<<<grid, kThreads, kFwdSmemBytes, s>>>(mq, mk, mv, p);
   return cudaGetLastError();
 }
