@@ -1,0 +1,384 @@
+// fwd_db_sm100a.cu — d = 64 self-attention forward with double-buffered scores (bf16 in, fp32
+// accumulate): the default d = 64 forward (no causal mask, no key split, no triple output).
+//
+// Same method as fwd_sm100a.cu (the paper's per-query stream, key chunk by
+// key chunk, Figure 1 lines 12-19 = PAPER.md:118-126; lazy rescale "as needed"), same
+// CTA shape (two 128-row query tiles of one (b, h), 16 softmax warps, a thread = one
+// row-half), but the key tile is 96 wide so that each query tile gets TWO score buffers:
+//
+//   TMEM (512 columns): S[qt][0] S[qt][1] = 4 x 96 columns at 0, 96, 192, 288;
+//                       O0 [384,448), O1 [448,512).
+//   P_t (bf16 pairs, 48 columns) is written over the first half of the buffer S_t came from.
+//
+// With one buffer (fwd_sm100a.cu) S_{t+1} could only be computed after the softmax had read
+// S_t, and it queued behind the PV products of both tiles on the tensor pipe: the softmax
+// waited for scores ~150 cycles and for PV_{t-1} ~300 cycles per tile, and the two query tiles
+// drifted into phase, leaving the exponential unit (the binding unit at d = 64: 2 exps per
+// 128 MMA flops) idle ~22 % of the time. Here QK_{t+2} is issued as soon as PV_t has consumed
+// P_t, a whole softmax step ahead, so the scores of the next tile are always waiting; the
+// softmax prefetches them (tcgen05.ld) before storing P_t, hiding the TMEM latency, and never
+// waits on PV except before a (rare) O rescale.
+//
+// Warp roles: 0 TMA producer (Q0, Q1 once; kStages-deep K/V ring of 96-row tiles), 1 / 3 MMA
+// issuers for query tile 0 / 1, 2 TMEM allocator, 4-19 softmax (as fwd_sm100a.cu).
+#include <cuda_bf16.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace mea {
+namespace {
+
+constexpr int kN = 96;                                // keys per tile
+#ifndef MEA_DB_STAGES
+#define MEA_DB_STAGES 6
+#endif
+constexpr int kStages = MEA_DB_STAGES;                // K/V ring depth
+constexpr int kQTileBytes = kTileM * kHeadDim * 2;    // 16 KiB
+constexpr int kKVTileBytes = kN * kHeadDim * 2;       // 12 KiB (a multiple of the 1 KiB swizzle atom)
+constexpr int kThreads = 640;
+constexpr int kSoftmaxRegs = 112;                     // 32 + 4 x 112 = 480 per lane slot
+constexpr int kControlRegs = 32;
+constexpr float kLazyThreshold = 8.0f;
+constexpr float kSafeSum = 18446744073709551616.0f;   // 2^64
+__host__ __device__ constexpr uint32_t col_s(int qt, int b) { return (uint32_t)((qt * 2 + b) * kN); }
+__host__ __device__ constexpr uint32_t col_o(int qt) { return qt ? 448u : 384u; }
+
+constexpr uint32_t kIdescQK = idesc_bf16_f32(128, kN, false, false);   // A = Q, B = K, both K-major
+constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 64, false, true);    // A = P (TMEM), B = V MN-major
+
+#ifndef MEA_DB_POLY_MASK
+#define MEA_DB_POLY_MASK 0x00080080u  // pairs 7 and 19 of the 24 pairs of a half row on the FMA pipe
+#endif
+__device__ __forceinline__ constexpr bool poly_pair(int i) { return ((MEA_DB_POLY_MASK) >> i) & 1u; }
+
+struct DbSmem {
+  uint8_t q[2][kQTileBytes];
+  uint8_t k[kStages][kKVTileBytes];
+  uint8_t v[kStages][kKVTileBytes];
+  uint64_t q_full;
+  uint64_t kv_full[kStages];
+  uint64_t kv_empty[kStages];
+  uint64_t s_full[2][2];  // [query tile][buffer]
+  uint64_t p_full[2];
+  uint64_t pv_done[2];
+  uint64_t o_done[2];
+  uint32_t tmem_base;
+};
+constexpr size_t kDbSmemBytes = sizeof(DbSmem) + 1024;
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    fwd_db_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+                  const __grid_constant__ CUtensorMap mv, const FwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  DbSmem& sm = *reinterpret_cast<DbSmem*>(align1024(smem_raw));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qblk = blockIdx.x;
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int q0 = p.q_begin + qblk * kRowsPerCta;
+  const int q_end = min(p.n_q, p.q_begin + p.q_count);
+  const int T = (p.n_k + kN - 1) / kN;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.q_full, 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&sm.kv_full[i], 1);
+      mbar_init(&sm.kv_empty[i], 2);  // one commit per query tile
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.s_full[i][0], 1);
+      mbar_init(&sm.s_full[i][1], 1);
+      mbar_init(&sm.p_full[i], 256);
+      mbar_init(&sm.pv_done[i], 1);
+      mbar_init(&sm.o_done[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mq);
+    tma_prefetch_desc(&mk);
+    tma_prefetch_desc(&mv);
+  }
+  if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp < 4) {
+    setmaxnreg_dec<kControlRegs>();
+    if (warp == 0) {
+      // ---------------------------------------------------------- TMA producer
+      const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&sm.q_full, 2 * kQTileBytes);
+        tma_load_4d(sm.q[0], &mq, &sm.q_full, 0, h, q0, b, stream);
+        tma_load_4d(sm.q[1], &mq, &sm.q_full, 0, h, q0 + kTileM, b, stream);
+      }
+      __syncwarp();
+      for (int t = 0; t < T; ++t) {
+        const int st = t % kStages;
+        if (t >= kStages) mbar_wait(&sm.kv_empty[st], ((t / kStages) - 1) & 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kKVTileBytes);
+          tma_load_4d(sm.k[st], &mk, &sm.kv_full[st], 0, h, t * kN, b, keep);
+          tma_load_4d(sm.v[st], &mv, &sm.kv_full[st], 0, h, t * kN, b, keep);
+        }
+        __syncwarp();
+      }
+    } else if (warp == 1 || warp == 3) {
+      // ---------------------------------------------------------- MMA issuers
+      const int qt = warp >> 1;
+      const uint64_t dq = shfl0_u64(sdesc_sw128(smem_u32(sm.q[qt]), 16, 1024));
+      const uint64_t dk0 = shfl0_u64(sdesc_sw128(smem_u32(sm.k[0]), 16, 1024));
+      const uint64_t dv0 = shfl0_u64(sdesc_sw128(smem_u32(sm.v[0]), 16, 1024));
+      constexpr uint64_t kStageStep = kKVTileBytes >> 4;
+      const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t to = tmem_u + col_o(qt);
+      auto qk = [&](int t) {  // S[qt][t & 1] = Q K_t^T
+        const uint64_t dk = dk0 + (t % kStages) * kStageStep;
+        const uint32_t ts = tmem_u + col_s(qt, t & 1);
+#pragma unroll
+        for (int kk = 0; kk < kHeadDim / 16; ++kk) umma_ss(ts, dq + kk * 2, dk + kk * 2, kIdescQK, kk > 0);
+        umma_commit(&sm.s_full[qt][t & 1]);
+      };
+      auto pv = [&](int t) {  // O += P_t V_t, P_t over the first 48 columns of S[qt][t & 1]
+        const uint64_t dv = dv0 + (t % kStages) * kStageStep;
+        const uint32_t tp = tmem_u + col_s(qt, t & 1);
+#pragma unroll
+        for (int kk = 0; kk < kN / 16; ++kk)
+          umma_ts(to, tp + kk * 8, dv + kk * 128, kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
+      };
+      mbar_wait(&sm.q_full, 0);
+      for (int t = 0; t < 2 && t < T; ++t) {
+        mbar_wait(&sm.kv_full[t], 0);
+        tc_fence_after();
+        if (elect_one()) qk(t);
+        __syncwarp();
+      }
+#ifdef MEA_EXP_TIMING
+#define IPROBE(k) if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && t >= 8 && t < 24) \
+    reinterpret_cast<unsigned long long*>(p.lse)[512 + (qt * 16 + (t - 8)) * 8 + (k)] = clock64();
+#else
+#define IPROBE(k)
+#endif
+      // The issuer's waits poll (mbarrier.test_wait) instead of suspending: it resumes as soon as
+      // the last softmax warp has stored P_t (-2 % kernel time vs try_wait, measured).
+      for (int t = 0; t < T; ++t) {
+        mbar_spin(&sm.p_full[qt], t & 1);
+        IPROBE(0)
+        tc_fence_after();
+        if (elect_one()) {
+          pv(t);
+          umma_commit(&sm.kv_empty[t % kStages]);
+          umma_commit(&sm.pv_done[qt]);
+          if (t + 1 == T) umma_commit(&sm.o_done[qt]);
+        }
+        __syncwarp();
+        IPROBE(1)
+        if (t + 2 < T) {
+          // S_{t+2} goes into the buffer P_t occupies: wait until PV_t has read it
+          mbar_spin(&sm.kv_full[(t + 2) % kStages], ((t + 2) / kStages) & 1);
+          mbar_spin(&sm.pv_done[qt], t & 1);
+          IPROBE(2)
+          tc_fence_after();
+          if (elect_one()) qk(t + 2);
+          __syncwarp();
+          IPROBE(3)
+        }
+      }
+    }
+  } else {
+    setmaxnreg_inc<kSoftmaxRegs>();
+    // ------------------------------------------------------------ softmax warps
+    // warp (qt, sub, quarter) owns rows quarter*32 + sub*16 + [0,16) of query tile qt; with the
+    // 16x32bx2 shape lanes 0-15 hold key columns [0,48) and lanes 16-31 [48,96) of those rows.
+    const int sw = warp - 4;
+    const int qt = sw >> 3;
+    const int sub = (sw >> 2) & 1;
+    const int quarter = warp & 3;
+    const int half = lane >> 4;
+    const int rloc = quarter * 32 + sub * 16 + (lane & 15);
+    const int row = q0 + qt * kTileM + rloc;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32 + sub * 16) << 16);
+    const uint32_t colO = col_o(qt);
+    const float c = p.scale_log2;
+    float m_ref = -INFINITY;  // reference max m* (log2 units of the scaled score)
+    float l = 0.f;            // this half's part of s*
+#ifdef MEA_EXP_TIMING
+    unsigned long long* tdbg = reinterpret_cast<unsigned long long*>(p.lse);
+    const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && quarter == 0 && sub == 0 && (lane & 15) == 0;
+#define TPROBE(k) if (probe && t >= 8 && t < 24) tdbg[((qt * 2 + half) * 16 + (t - 8)) * 8 + (k)] = clock64();
+#else
+#define TPROBE(k)
+#endif
+    uint32_t sr[48];
+    auto load_s = [&](int t) {
+      const uint32_t a = lane_base + col_s(qt, t & 1);
+      tmem_ld32_split<48>(a, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld16_split<48>(a + 32, *reinterpret_cast<uint32_t(*)[16]>(&sr[32]));
+    };
+    if (T > 0) {
+      mbar_wait(&sm.s_full[qt][0], 0);
+      tc_fence_after();
+      load_s(0);
+    }
+    for (int t = 0; t < T; ++t) {
+      TPROBE(0)
+      tmem_ld_wait();
+      TPROBE(1)
+#ifdef MEA_EXP_TIMING
+      if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && t >= 8 && t < 12) {
+        tdbg[1024 + (t - 8) * 32 + sw * 2 + 1] = clock64();
+      }
+#endif
+      const int valid = (p.n_k - t * kN) - half * 48;  // keys of this tile in my half (may be <= 0)
+      uint32_t pk[24];
+      bool fast = (t > 0) && (p.n_k - t * kN >= kN) && (c >= 0.f);
+      if (fast) {
+        const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
+        float2 rs = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 24; ++i) {
+          const float2 s2 = make_float2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]));
+          const float2 x = __ffma2_rn(s2, c2, nm2);  // s*c - m*
+          const float2 e = poly_pair(i) ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          rs = __fadd2_rn(rs, e);
+          pk[i] = pack_bf16x2(e.x, e.y);
+        }
+        // a finite half-row sum below 2^64 certifies every 2^(s c - m*) term (fwd_sm100a.cu)
+        const float rsum = rs.x + rs.y;
+        const bool need = !(rsum <= kSafeSum);
+        if (__any_sync(0xffffffffu, need)) fast = false;
+        else l += rsum;
+      }
+      if (!fast) {
+        float ext, e0;
+        if (c >= 0.f) {
+          e0 = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < 48; ++i)
+            if (i < valid) e0 = fmaxf(e0, __uint_as_float(sr[i]));
+          ext = fmaxf(e0, __shfl_xor_sync(0xffffffffu, e0, 16));
+        } else {
+          e0 = INFINITY;
+#pragma unroll
+          for (int i = 0; i < 48; ++i)
+            if (i < valid) e0 = fminf(e0, __uint_as_float(sr[i]));
+          ext = fminf(e0, __shfl_xor_sync(0xffffffffu, e0, 16));
+        }
+        const float m_cand = ext * c;
+        const bool need = m_cand > m_ref + kLazyThreshold;  // always true on the first tile
+        float alpha = 1.f;
+        if (need) {
+          alpha = ex2_approx(m_ref - m_cand);  // 0 when m_ref = -inf
+          m_ref = m_cand;
+          l *= alpha;
+        }
+        if (t > 0 && __any_sync(0xffffffffu, need)) {
+          // v* <- v* alpha once PV_{t-1} has finished (lanes 0-15: O columns [0,32), 16-31: [32,64))
+          mbar_wait(&sm.pv_done[qt], (t - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            uint32_t o[16];
+            tmem_ld16_split<32>(lane_base + colO + part * 16, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st16_split<32>(lane_base + colO + part * 16, o);
+          }
+        }
+        const float neg_m = -m_ref;
+        float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < 24; ++i) {
+          const float p0 = (2 * i < valid) ? ex2_approx(fmaf(__uint_as_float(sr[2 * i]), c, neg_m)) : 0.f;
+          const float p1 = (2 * i + 1 < valid) ? ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), c, neg_m)) : 0.f;
+          rs0 += p0;
+          rs1 += p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+        l += rs0 + rs1;
+      }
+      TPROBE(4)
+      // prefetch S_{t+1} (already computed: it sits in the other buffer), then store P_t over
+      // the first half of S_t's buffer
+      if (t + 1 < T) {
+        mbar_wait(&sm.s_full[qt][(t + 1) & 1], ((t + 1) >> 1) & 1);
+        tc_fence_after();
+        load_s(t + 1);
+      }
+      TPROBE(2)
+      const uint32_t pa = lane_base + col_s(qt, t & 1);
+      tmem_st16_split<24>(pa, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+      tmem_st8_split<24>(pa + 16, *reinterpret_cast<uint32_t(*)[8]>(&pk[16]));
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&sm.p_full[qt]);
+      TPROBE(5)
+#ifdef MEA_EXP_TIMING
+      if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && t >= 8 && t < 12) {
+        tdbg[1024 + (t - 8) * 32 + sw * 2] = clock64();
+      }
+#endif
+    }
+    // ------------------------------------------------------------ epilogue: out = v*/s*
+    const float lrow = l + __shfl_xor_sync(0xffffffffu, l, 16);
+    mbar_wait(&sm.o_done[qt], 0);
+    tc_fence_after();
+    uint32_t o[32];
+    tmem_ld32_split<32>(lane_base + colO, o);
+    tmem_ld_wait();
+    if (row < q_end) {
+      const size_t bh = (size_t)b * p.H + h;
+      const float inv = 1.f / lrow;
+      const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + half * 32;
+      if (p.out_f32) {
+        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          dst[i] = make_float4(__uint_as_float(o[4 * i]) * inv, __uint_as_float(o[4 * i + 1]) * inv,
+                               __uint_as_float(o[4 * i + 2]) * inv, __uint_as_float(o[4 * i + 3]) * inv);
+      } else {
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv);
+          w.y = pack_bf16x2(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv);
+          w.z = pack_bf16x2(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv);
+          w.w = pack_bf16x2(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv);
+          dst[i] = w;
+        }
+      }
+#ifndef MEA_EXP_TIMING
+      if (p.lse && half == 0) p.lse[bh * p.n_q + row] = (m_ref + __log2f(lrow)) * 0.6931471805599453f;
+#endif
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+int fwd_db_key_tile() { return kN; }
+
+cudaError_t launch_fwd_db_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
+                               const CUtensorMap& mv, cudaStream_t s) {
+  const cudaError_t attr = ensure_smem_attr<fwd_db_kernel>((int)kDbSmemBytes);
+  if (attr != cudaSuccess) return attr;
+  fwd_db_kernel<<<dim3(p.num_q_blocks, p.H, p.B), kThreads, kDbSmemBytes, s>>>(mq, mk, mv, p);
+  return cudaGetLastError();
+}
+
+}  // namespace mea

@@ -228,7 +228,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       umma_commit(&sm.s_full[qt]);
     }
     __syncwarp();
+#ifdef MEA_EXP_TIMING
+#define IPROBE(k) if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && t >= 8 && t < 24) \
+    reinterpret_cast<unsigned long long*>(p.lse)[512 + (qt * 16 + (t - 8)) * 8 + (k)] = clock64();
+#else
+#define IPROBE(k)
+#endif
     for (int t = 0; t < Tq; ++t) {
+      IPROBE(0)
       const int st = t % kStages;
       const int nx = (t + 1) % kStages;
       const bool more = (t + 1) < Tq;
@@ -236,16 +243,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       // next scores are computed while the current softmax runs.
       if (more) {
         mbar_wait(&sm.kv_full[nx], ((t + 1) / kStages) & 1);
+        IPROBE(1)
         mbar_wait(&sm.s_loaded[qt], t & 1);
+        IPROBE(2)
         tc_fence_after();
         if (elect_one()) {
           qk(nx);
           umma_commit(&sm.s_full[qt]);
         }
         __syncwarp();
+        IPROBE(3)
       }
       // O += P_t V_t once P_t is in TMEM
       mbar_wait(&sm.p_full[qt], t & 1);
+      IPROBE(4)
       tc_fence_after();
       if (elect_one()) {
         pv(st, t > 0);
@@ -254,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!more) umma_commit(&sm.o_done[qt]);
       }
       __syncwarp();
+      IPROBE(5)
     }
     // key tiles past this query tile's diagonal (causal): release their ring stage without
     // using it (a commit keeps the arrival ordered after this warp's earlier MMAs)

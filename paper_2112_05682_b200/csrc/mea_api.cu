@@ -82,6 +82,10 @@ struct ProfScope {
 
 }  // namespace
 
+#ifndef MEA_FWD_DB
+#define MEA_FWD_DB 1
+#endif
+
 namespace mea {
 
 cudaError_t make_bnhd_map(CUtensorMap* map, const void* base, CUtensorMapDataType elem, int elem_bytes, int64_t B,
@@ -276,14 +280,17 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
   const int64_t nqb = (n_q + rows_per_cta - 1) / rows_per_cta;
   if (nqb * pl.splits > kMaxInt) return fail(MEA_ERR_UNSUPPORTED, "grid too large");
 
+  // the plain d = 64 forward (online over all keys, no mask) runs the double-buffered kernel
+  const bool use_db = MEA_FWD_DB && d == kHeadDim && !causal && pl.splits == 1;
+  const int key_box = use_db ? fwd_db_key_tile() : kTileN;
   CUtensorMap mq, mk, mv;
   const char* why = "";
   cudaError_t e;
   if ((e = make_bnhd_map(&mq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_q, H, d, 64, kTileM,
                          CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
-      (e = make_bnhd_map(&mk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
+      (e = make_bnhd_map(&mk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, key_box,
                          CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
-      (e = make_bnhd_map(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
+      (e = make_bnhd_map(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, key_box,
                          CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess)
     return cuda_fail(e, why);
 
@@ -314,6 +321,9 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
     if (d == 128) {
       ProfScope ps("fwd128_bf16", st);
       if ((e = launch_fwd128_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd128_bf16 launch");
+    } else if (use_db) {
+      ProfScope ps("fwd_bf16", st);
+      if ((e = launch_fwd_db_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_db_bf16 launch");
     } else {
       ProfScope ps("fwd_bf16", st);
       if ((e = launch_fwd_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_bf16 launch");

@@ -35,6 +35,17 @@ def test_bf16_forward_matches_oracle(B, n_q, n_k, H):
     assert np.abs(lse - ref_lse).max() < 1e-3
 
 
+@pytest.mark.parametrize("n_k", [95, 96, 97, 191, 192, 193, 2 * 96 * 6 + 1])
+def test_bf16_forward_key_tile_boundaries(n_k):
+    """The default d = 64 forward streams 96-key tiles through two score buffers per query tile
+    and a 6-stage K/V ring: key counts at and around tile / buffer / ring boundaries."""
+    q, k, v = Hh.host_inputs(1, 300, n_k, 2, 64, seed=7)
+    ref, ref_lse = O.mha_forward(q, k, v, 0.125)
+    got, lse = _run(q, k, v, scale=0.125)
+    Hh.assert_close_bf16(got, ref)
+    assert np.abs(lse - ref_lse).max() < 1e-3
+
+
 @pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
 def test_bf16_forward_out_dtypes_and_scale(out_dtype):
     q, k, v = Hh.host_inputs(1, 200, 333, 2, 64, seed=2)
