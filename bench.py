@@ -438,7 +438,9 @@ def main():
         bufs.append({nm: torch.empty_like(t) for nm, t in bufs[0].items()})
         ws_e2e = [bwd_ws, torch.empty_like(bwd_ws) if bwd_ws is not None else None]
         s_in, s_c, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_qkv = [torch.cuda.Event() for _ in range(2)]   # q, k, v of a set have landed
+        ev_in = [torch.cuda.Event() for _ in range(2)]    # ... and dO
+        ev_f = [torch.cuda.Event() for _ in range(2)]     # forward of a set done (out final)
         ev_c = [torch.cuda.Event() for _ in range(2)]
         ev_out = [torch.cuda.Event() for _ in range(2)]
 
@@ -455,20 +457,25 @@ def main():
                     if i >= 2:
                         s_in.wait_event(ev_c[bi])      # step i-2 has finished reading this set
                     S["q"].copy_(hq, non_blocking=True); S["k"].copy_(hk, non_blocking=True)
-                    S["v"].copy_(hv, non_blocking=True); S["do"].copy_(hdo, non_blocking=True)
+                    S["v"].copy_(hv, non_blocking=True)
+                    ev_qkv[bi].record(s_in)
+                    S["do"].copy_(hdo, non_blocking=True)
                     ev_in[bi].record(s_in)
                 with torch.cuda.stream(s_c):
-                    s_c.wait_event(ev_in[bi])
+                    s_c.wait_event(ev_qkv[bi])         # the forward needs q, k, v only
                     if i >= 2:
                         s_c.wait_event(ev_out[bi])     # step i-2's results have been copied out
                     api.mea_attention_fwd(S["q"], S["k"], S["v"], out=S["out"], lse=S["lse"])
+                    ev_f[bi].record(s_c)
                     if run_bwd:
+                        s_c.wait_event(ev_in[bi])
                         api.mea_attention_bwd(S["q"], S["k"], S["v"], S["out"], S["do"], lse=S["lse"], dq=S["dq"],
                                               dk=S["dk"], dv=S["dv"], workspace=ws_e2e[bi])
                     ev_c[bi].record(s_c)
                 with torch.cuda.stream(s_out):
-                    s_out.wait_event(ev_c[bi])
+                    s_out.wait_event(ev_f[bi])         # out is final once the forward is done
                     ho.copy_(S["out"], non_blocking=True)
+                    s_out.wait_event(ev_c[bi])
                     if run_bwd:
                         hdq.copy_(S["dq"], non_blocking=True); hdk.copy_(S["dk"], non_blocking=True)
                         hdv.copy_(S["dv"], non_blocking=True)
@@ -487,7 +494,9 @@ def main():
         d2h = (4 if run_bwd else 1) * numel * 2
         e2e = {"value": world * flops_step / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "pipelining": "H2D of step i+1 and D2H of step i-1 overlap step i (3 streams, 2 buffer sets)"}
+               "pipelining": "H2D of step i+1 and D2H of step i-1 overlap step i (3 streams, 2 buffer sets); "
+                              "the forward starts once q, k, v have landed and out is read back while the "
+                              "backward runs"}
         del bufs, ws_e2e
 
     # ---------------- cpu baseline: the oracle on the host cores (rank 0, N == 1 only)

@@ -1,5 +1,6 @@
 // fwd_db_sm100a.cu — d = 64 self-attention forward with double-buffered scores (bf16 in, fp32
-// accumulate): the default d = 64 forward (no causal mask, no key split, no triple output).
+// accumulate): the d = 64 forward online over all keys, with or without the causal mask (the
+// key-split schedule and the triple output run fwd_sm100a.cu).
 //
 // Same method as fwd_sm100a.cu (the paper's per-query stream, key chunk by
 // key chunk, Figure 1 lines 12-19 = PAPER.md:118-126; lazy rescale "as needed"), same
@@ -77,11 +78,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   DbSmem& sm = *reinterpret_cast<DbSmem*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qblk = blockIdx.x;
-  const int h = blockIdx.y, b = blockIdx.z;
+  // causal: a 1-D grid ordered heaviest block (last rows) first across all (b, h)
+  const int qblk = p.causal ? p.num_q_blocks - 1 - (int)(blockIdx.x / (p.H * p.B)) : (int)blockIdx.x;
+  const int h = p.causal ? (int)(blockIdx.x % p.H) : (int)blockIdx.y;
+  const int b = p.causal ? (int)((blockIdx.x / p.H) % p.B) : (int)blockIdx.z;
   const int q0 = p.q_begin + qblk * kRowsPerCta;
   const int q_end = min(p.n_q, p.q_begin + p.q_count);
-  const int T = (p.n_k + kN - 1) / kN;
+  // key tiles query tile qt needs (causal, n_q == n_k: keys below its last row + 1); the
+  // producer streams the union (query tile 1's)
+  auto tiles_for = [&](int qt) {
+    return ((p.causal ? min(p.n_k, q0 + (qt + 1) * kTileM) : p.n_k) + kN - 1) / kN;
+  };
+  const int T = tiles_for(1);
 
   if (threadIdx.x == 0) {
     mbar_init(&sm.q_full, 1);
@@ -133,6 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1 || warp == 3) {
       // ---------------------------------------------------------- MMA issuers
       const int qt = warp >> 1;
+      const int Tq = tiles_for(qt);
       const uint64_t dq = shfl0_u64(sdesc_sw128(smem_u32(sm.q[qt]), 16, 1024));
       const uint64_t dk0 = shfl0_u64(sdesc_sw128(smem_u32(sm.k[0]), 16, 1024));
       const uint64_t dv0 = shfl0_u64(sdesc_sw128(smem_u32(sm.v[0]), 16, 1024));
@@ -154,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_ts(to, tp + kk * 8, dv + kk * 128, kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
       };
       mbar_wait(&sm.q_full, 0);
-      for (int t = 0; t < 2 && t < T; ++t) {
+      for (int t = 0; t < 2 && t < Tq; ++t) {
         mbar_wait(&sm.kv_full[t], 0);
         tc_fence_after();
         if (elect_one()) qk(t);
@@ -168,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       // The issuer's waits poll (mbarrier.test_wait) instead of suspending: it resumes as soon as
       // the last softmax warp has stored P_t (-2 % kernel time vs try_wait, measured).
-      for (int t = 0; t < T; ++t) {
+      for (int t = 0; t < Tq; ++t) {
         mbar_spin(&sm.p_full[qt], t & 1);
         IPROBE(0)
         tc_fence_after();
@@ -176,11 +185,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           pv(t);
           umma_commit(&sm.kv_empty[t % kStages]);
           umma_commit(&sm.pv_done[qt]);
-          if (t + 1 == T) umma_commit(&sm.o_done[qt]);
+          if (t + 1 == Tq) umma_commit(&sm.o_done[qt]);
         }
         __syncwarp();
         IPROBE(1)
-        if (t + 2 < T) {
+        if (t + 2 < Tq) {
           // S_{t+2} goes into the buffer P_t occupies: wait until PV_t has read it
           mbar_spin(&sm.kv_full[(t + 2) % kStages], ((t + 2) / kStages) & 1);
           mbar_spin(&sm.pv_done[qt], t & 1);
@@ -190,6 +199,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           IPROBE(3)
         }
+      }
+      // key tiles past this query tile's last row (causal): release their ring stages unused
+      for (int t = Tq; t < T; ++t) {
+        mbar_wait(&sm.kv_full[t % kStages], (t / kStages) & 1);
+        if (elect_one()) umma_commit(&sm.kv_empty[t % kStages]);
+        __syncwarp();
       }
     }
   } else {
@@ -203,7 +218,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int half = lane >> 4;
     const int rloc = quarter * 32 + sub * 16 + (lane & 15);
-    const int row = q0 + qt * kTileM + rloc;
+    const int r0 = q0 + qt * kTileM;  // first row of this query tile
+    const int row = r0 + rloc;
+    const int Tq = tiles_for(qt);
+    const int key_lim = p.causal ? min(p.n_k, row + 1) : p.n_k;  // keys this row sees: [0, key_lim)
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32 + sub * 16) << 16);
     const uint32_t colO = col_o(qt);
     const float c = p.scale_log2;
@@ -222,12 +240,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld32_split<48>(a, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
       tmem_ld16_split<48>(a + 32, *reinterpret_cast<uint32_t(*)[16]>(&sr[32]));
     };
-    if (T > 0) {
+    if (Tq > 0) {
       mbar_wait(&sm.s_full[qt][0], 0);
       tc_fence_after();
       load_s(0);
     }
-    for (int t = 0; t < T; ++t) {
+    for (int t = 0; t < Tq; ++t) {
       TPROBE(0)
       tmem_ld_wait();
       TPROBE(1)
@@ -236,9 +254,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tdbg[1024 + (t - 8) * 32 + sw * 2 + 1] = clock64();
       }
 #endif
-      const int valid = (p.n_k - t * kN) - half * 48;  // keys of this tile in my half (may be <= 0)
+      const int valid = (key_lim - t * kN) - half * 48;  // keys of this tile in my half (may be <= 0)
       uint32_t pk[24];
-      bool fast = (t > 0) && (p.n_k - t * kN >= kN) && (c >= 0.f);
+      // fast path: m* set, and every row of the query tile sees every key of this tile
+      bool fast = (t > 0) && (p.n_k - t * kN >= kN) && (!p.causal || (t + 1) * kN <= r0 + 1) && (c >= 0.f);
       if (fast) {
         const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
         float2 rs = make_float2(0.f, 0.f);
@@ -246,7 +265,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 24; ++i) {
           const float2 s2 = make_float2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]));
           const float2 x = __ffma2_rn(s2, c2, nm2);  // s*c - m*
+#ifdef MEA_EXP_NOEXP
+          const float2 e = __fmul2_rn(x, make_float2(1e-30f, 1e-30f));  // timing experiment only
+#else
           const float2 e = poly_pair(i) ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+#endif
           rs = __fadd2_rn(rs, e);
           pk[i] = pack_bf16x2(e.x, e.y);
         }
@@ -308,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       TPROBE(4)
       // prefetch S_{t+1} (already computed: it sits in the other buffer), then store P_t over
       // the first half of S_t's buffer
-      if (t + 1 < T) {
+      if (t + 1 < Tq) {
         mbar_wait(&sm.s_full[qt][(t + 1) & 1], ((t + 1) >> 1) & 1);
         tc_fence_after();
         load_s(t + 1);
@@ -377,7 +400,8 @@ cudaError_t launch_fwd_db_bf16(const FwdParams& p, const CUtensorMap& mq, const 
                                const CUtensorMap& mv, cudaStream_t s) {
   const cudaError_t attr = ensure_smem_attr<fwd_db_kernel>((int)kDbSmemBytes);
   if (attr != cudaSuccess) return attr;
-  fwd_db_kernel<<<dim3(p.num_q_blocks, p.H, p.B), kThreads, kDbSmemBytes, s>>>(mq, mk, mv, p);
+  const dim3 grid = p.causal ? dim3(p.num_q_blocks * p.H * p.B) : dim3(p.num_q_blocks, p.H, p.B);
+  fwd_db_kernel<<<grid, kThreads, kDbSmemBytes, s>>>(mq, mk, mv, p);
   return cudaGetLastError();
 }
 

@@ -74,8 +74,8 @@ cudaError_t make_bnhd_map(CUtensorMap* map, const void* base, CUtensorMapDataTyp
 cudaError_t launch_fwd_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                             const CUtensorMap& mv, cudaStream_t s);
 cudaError_t launch_merge_rows(const FwdParams& p, cudaStream_t s);
-// d = 64 forward with double-buffered 96-key score tiles (fwd_db_sm100a.cu): no causal mask,
-// no key split, no triple output; K/V maps with fwd_db_key_tile() rows per box.
+// d = 64 forward with double-buffered 96-key score tiles (fwd_db_sm100a.cu): online over all
+// keys (causal or not), no key split, no triple output; K/V maps with fwd_db_key_tile() rows.
 int fwd_db_key_tile();
 cudaError_t launch_fwd_db_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                                const CUtensorMap& mv, cudaStream_t s);

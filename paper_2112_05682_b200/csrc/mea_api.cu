@@ -281,7 +281,7 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
   if (nqb * pl.splits > kMaxInt) return fail(MEA_ERR_UNSUPPORTED, "grid too large");
 
   // the plain d = 64 forward (online over all keys, no mask) runs the double-buffered kernel
-  const bool use_db = MEA_FWD_DB && d == kHeadDim && !causal && pl.splits == 1;
+  const bool use_db = MEA_FWD_DB && d == kHeadDim && pl.splits == 1;
   const int key_box = use_db ? fwd_db_key_tile() : kTileN;
   CUtensorMap mq, mk, mv;
   const char* why = "";
