@@ -11,7 +11,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
 for w in fwd bwd sq fwd128; do
   timeout 300 python tools/prof_kernel.py $w > gpurun_out/plain_$w.log 2>&1; echo "plain $w $?"
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd_bf16 -s 1 -c 1 -f -o gpurun_out/prof_fwd_r01 python tools/prof_kernel.py fwd > gpurun_out/ncu_fwd.log 2>&1; echo "ncu fwd $?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd_db -s 1 -c 1 -f -o gpurun_out/prof_fwd_r01 python tools/prof_kernel.py fwd > gpurun_out/ncu_fwd.log 2>&1; echo "ncu fwd $?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:bwd_bf16 -s 1 -c 1 -f -o gpurun_out/prof_bwd_r01 python tools/prof_kernel.py bwd > gpurun_out/ncu_bwd.log 2>&1; echo "ncu bwd $?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sq_partial -s 1 -c 1 -f -o gpurun_out/prof_sq_r01 python tools/prof_kernel.py sq > gpurun_out/ncu_sq.log 2>&1; echo "ncu sq $?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fwd128 -s 1 -c 1 -f -o gpurun_out/prof_fwd128_r01 python tools/prof_kernel.py fwd128 > gpurun_out/ncu_fwd128.log 2>&1; echo "ncu fwd128 $?"
+for w in fwd bwd fwd128; do timeout 60 python tools/power_probe.py $w 5; done > gpurun_out/power.txt 2>&1; echo "power $?"
+timeout 900 python tools/sweep.py --out gpurun_out/sweep.json > gpurun_out/sweep.log 2>&1; echo "sweep $?"
+timeout 900 python tools/paper_tables.py --out gpurun_out/paper_tables.json > gpurun_out/paper_tables.log 2>&1; echo "tables $?"
