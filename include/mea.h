@@ -60,6 +60,10 @@ extern "C" {
  */
 typedef enum { MEA_F32 = 0, MEA_BF16 = 1, MEA_F32_SPLIT = 2 } mea_dtype_t;
 
+/* k_chunk value selecting the paper's sqrt(n) key chunk, ceil(sqrt(n_k)) keys (PAPER.md:179:
+ * "Assuming a chunk size of sqrt(n) for the keys and values ... O(sqrt(n)) memory"). */
+#define MEA_CHUNK_SQRT_N (-1)
+
 typedef enum {
   MEA_OK = 0,
   MEA_ERR_INVALID_VALUE = 1,
@@ -83,7 +87,8 @@ MEA_API const char* mea_last_error_detail(void);
  *   q [B,n_q,H,d], k,v [B,n_k,H,d] of in_dtype; out [B,n_q,H,d] of out_dtype.
  *   lse [B,H,n_q] float32, nullable: lse_i = log sum_j e^{s_ij}, the per-row residual
  *     the backward pass consumes.
- *   q_chunk, k_chunk: the paper's query_chunk_size / key_chunk_size.
+ *   q_chunk, k_chunk: the paper's query_chunk_size / key_chunk_size;
+ *     k_chunk = MEA_CHUNK_SQRT_N picks ceil(sqrt(n_k)).
  *     0 = default schedule: every work item streams all keys with an on-chip running
  *     (v*, s*, m*), zero workspace. k_chunk in (0, n_k) selects the paper's key-chunk
  *     summaries: each chunk's (m*, s*, v*) goes to the workspace
@@ -102,10 +107,37 @@ MEA_API mea_status_t mea_attention_fwd(const void* q, const void* k, const void*
                                float* lse, int64_t q_chunk, int64_t k_chunk,
                                void* workspace, size_t workspace_bytes, void* stream);
 
-/* Workspace bytes mea_attention_fwd needs for these arguments (0 unless 0 < k_chunk < n_k). */
+/* Workspace bytes mea_attention_fwd needs for these arguments (0 unless 0 < k_chunk < n_k;
+ * k_chunk = MEA_CHUNK_SQRT_N selects ceil(sqrt(n_k)) in both calls). */
 MEA_API mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k,
                                               int64_t d, mea_dtype_t in_dtype, int64_t q_chunk,
                                               int64_t k_chunk, size_t* bytes);
+
+/*
+ * The paper's chunked forward with multi-stage (tree) summarisation ("A multi-stage
+ * summarization approach could achieve O(log n) but would complicate the implementation";
+ * SURVEY.md §8(f) item 1). For each query chunk of q_chunk rows (0 = all rows; rounded up to the
+ * CTA's 256 rows, 128 at d = 128), processed one after another, the key chunks
+ * of k_chunk keys (MEA_CHUNK_SQRT_N or 0 = ceil(sqrt(n_k)); rounded up to a multiple of 128) are
+ * summarised one after another (Figure 1 lines 12-19) and merged like a binary
+ * counter with Figure 1's rescale for two summaries: level l holds the
+ * summary of 2^l consecutive chunks, a new summary carries upward while its level is occupied,
+ * and the occupied levels are merged and normalised at the end (out = v* / s*).
+ * At most floor(log2(chunks)) + 2 summaries per query row are alive:
+ *   workspace = (floor(log2(chunks)) + 2) * B * H * q_rows * (d + 2) * 4 bytes
+ * (mea_attention_fwd_tree_workspace_size) instead of Figure 1's chunks * (...). Same arguments,
+ * layouts and results (within rounding) as mea_attention_fwd; bf16 inputs with d in {64, 128}
+ * (MEA_ERR_UNSUPPORTED otherwise). One kernel launch per (query chunk, key chunk): a schedule
+ * for memory fidelity, not speed (the default online schedule needs no workspace at all).
+ */
+MEA_API mea_status_t mea_attention_fwd_tree(const void* q, const void* k, const void* v, void* out,
+                                    int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                                    mea_dtype_t in_dtype, mea_dtype_t out_dtype, float scale,
+                                    float* lse, int64_t q_chunk, int64_t k_chunk,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+MEA_API mea_status_t mea_attention_fwd_tree_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k,
+                                                   int64_t d, mea_dtype_t in_dtype, int64_t q_chunk,
+                                                   int64_t k_chunk, size_t* bytes);
 
 /*
  * Causal self-attention forward (not in the paper, which disabled

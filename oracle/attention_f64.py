@@ -232,6 +232,50 @@ def partial_triple(q, k, v, scale):
 
 
 # ----------------------------------------------------------------------------------
+# O5t: multi-stage summarisation ("A multi-stage summarization approach could
+#      achieve O(log n)"). The key chunks of a query chunk are summarised one
+#      after another (partial_triple = Figure 1 lines 12-19's summary) and
+#      combined like a binary counter: level l holds the summary of 2^l consecutive
+#      chunks; a new summary carries upward while its level is occupied, merging two
+#      summaries with Figure 1's rescale (lines 33-36, via merge2). The
+#      occupied levels are merged at the end and v*/s* returned (line 40).
+#      Returns (out, lse, max_alive): max_alive = most summaries alive at once.
+#      Reading (reading 18): the paper gives no algorithm for this stage, only
+#      the remark; the binary counter is the plainest schedule with O(log n) summaries.
+# ----------------------------------------------------------------------------------
+def merge2(a, b):
+    """Two summaries (m, s, v*) of the same rows over disjoint key ranges -> one."""
+    (ma, sa, va), (mb, sb, vb) = a, b
+    m = np.maximum(ma, mb)
+    wa = np.where(ma == -math.inf, 0.0, np.exp(ma - m))
+    wb = np.where(mb == -math.inf, 0.0, np.exp(mb - m))
+    return m, sa * wa + sb * wb, va * wa[:, None] + vb * wb[:, None]
+
+
+def tree_summarize(q, k, v, scale, key_chunk_size):
+    q, k, v = _check(q, k, v)
+    levels = []            # levels[l] = summary of 2^l chunks, or None
+    max_alive = 0
+    for c in range(0, k.shape[0], key_chunk_size):
+        cur = partial_triple(q, k[c:c + key_chunk_size], v[c:c + key_chunk_size], scale)
+        max_alive = max(max_alive, 1 + sum(x is not None for x in levels))
+        lvl = 0
+        while lvl < len(levels) and levels[lvl] is not None:
+            cur = merge2(levels[lvl], cur)
+            levels[lvl] = None
+            lvl += 1
+        if lvl == len(levels):
+            levels.append(None)
+        levels[lvl] = cur
+    acc = None
+    for x in levels:
+        if x is not None:
+            acc = x if acc is None else merge2(x, acc)
+    m, s_, vstar = acc
+    return vstar / s_[:, None], m + np.log(s_), max_alive
+
+
+# ----------------------------------------------------------------------------------
 # O6: analytic backward of out = softmax(scale q k^T) v. The paper delegates the
 #     derivative to jax.grad with checkpointing (P:254-261); the formulas are the
 #     standard softmax calculus (SPEC.md:122). The max carries no gradient

@@ -83,6 +83,41 @@ def mea_attention_fwd_workspace_size(B, H, n_q, n_k, d, in_dtype, q_chunk=0, k_c
 
 
 MEA_F32_SPLIT = 2
+MEA_CHUNK_SQRT_N = -1   # k_chunk: the paper's sqrt(n) key chunk
+
+
+def mea_attention_fwd_tree_workspace_size(B, H, n_q, n_k, d, in_dtype=MEA_BF16, q_chunk=0, k_chunk=MEA_CHUNK_SQRT_N):
+    n = ctypes.c_size_t(0)
+    _check(_lib.load().mea_attention_fwd_tree_workspace_size(B, H, n_q, n_k, d, in_dtype, q_chunk, k_chunk,
+                                                             ctypes.byref(n)))
+    return n.value
+
+
+def mea_attention_fwd_tree(q, k, v, scale=None, out=None, out_dtype=None, lse=None, want_lse=False,
+                           q_chunk=0, k_chunk=MEA_CHUNK_SQRT_N, workspace=None):
+    """The paper's chunked forward with multi-stage (tree) summarisation: key chunks
+    summarised one after another per query chunk and merged like a binary counter, so only
+    O(log(n_k / k_chunk)) summaries per query row are alive. bf16 inputs, d in {64, 128}."""
+    _cuda_contig(q, k, v, out, lse)
+    B, n_q, H, d = q.shape
+    n_k = k.shape[1]
+    if k.shape != (B, n_k, H, d) or v.shape != k.shape:
+        raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        raise TypeError("q, k, v must share a dtype")
+    dt = _dtype(q)
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    if out is None:
+        out = torch.empty((B, n_q, H, d), dtype=q.dtype if out_dtype is None else out_dtype, device=q.device)
+    if want_lse and lse is None:
+        lse = torch.empty((B, H, n_q), dtype=torch.float32, device=q.device)
+    if workspace is None:
+        workspace = _workspace(mea_attention_fwd_tree_workspace_size(B, H, n_q, n_k, d, dt, q_chunk, k_chunk),
+                               q.device)
+    _check(_lib.load().mea_attention_fwd_tree(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(out), B, H, n_q, n_k, d, dt, _dtype(out), scale, _ptr(lse),
+        q_chunk, k_chunk, _ptr(workspace), workspace.numel() if workspace is not None else 0, _stream(q.device)))
+    return (out, lse) if (want_lse or lse is not None) else out
 
 
 def mea_attention_fwd(q, k, v, scale=None, out=None, out_dtype=None, lse=None, want_lse=False,

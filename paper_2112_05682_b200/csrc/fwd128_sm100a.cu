@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kThreads128, 1)
   const int q0 = p.q_begin + qb * 128;
   const int q_end = min(p.n_q, p.q_begin + p.q_count);
   const int n_tiles = (p.n_k + kTileN - 1) / kTileN;
-  const int t_begin = split * p.tiles_per_split;
+  const int t_begin = (p.split_base + split) * p.tiles_per_split;  // split_base: tree schedule, one chunk per launch
   const int t_end = p.causal ? min(n_tiles, qb + 1) : min(n_tiles, t_begin + p.tiles_per_split);
   const int T = t_end - t_begin;
   const int diag = p.causal ? qb : -1;
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kThreads128, 1)
         p.tri_m[idx] = m_ref * 0.6931471805599453f;
         p.tri_s[idx] = lrow;
       }
-    } else if (row < q_end && p.num_splits > 1) {
+    } else if (row < q_end && p.part_o) {  // key-split / tree summaries
       const size_t prow = ((size_t)split * p.B * p.H + (size_t)b * p.H + h) * p.q_count + (row - p.q_begin);
       float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kD + half * 64);
 #pragma unroll

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int q0 = p.q_begin + qblk * kRowsPerCta;
   const int q_end = min(p.n_q, p.q_begin + p.q_count);
   const int n_tiles = (p.n_k + kTileN - 1) / kTileN;
-  const int t_begin = split * p.tiles_per_split;
+  const int t_begin = (p.split_base + split) * p.tiles_per_split;  // split_base: tree schedule, one chunk per launch
   // causal (n_q == n_k, no split): query tile qt of this block needs key tiles [0, 2 qblk + qt]
   // (the last one is its diagonal tile); the producer streams the union.
   const int t_end = p.causal ? min(n_tiles, 2 * qblk + 2) : min(n_tiles, t_begin + p.tiles_per_split);
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           p.tri_m[idx] = m_ref * 0.6931471805599453f;
           p.tri_s[idx] = lrow;
         }
-      } else if (p.num_splits > 1) {
+      } else if (p.part_o) {  // key-split / tree summaries
         const size_t prow = ((size_t)split * p.B * p.H + bh) * p.q_count + (row - p.q_begin);
         float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kHeadDim + half * 32);
 #pragma unroll
@@ -622,6 +622,32 @@ cudaError_t launch_merge_rows(const FwdParams& p, cudaStream_t s) {
   const int64_t rows = (int64_t)p.B * p.H * p.q_count;
   const int warps = 8;
   merge_rows_kernel<<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+// Two summaries of the same query rows over disjoint key ranges -> one (Figure 1 lines 33-36,
+// PAPER.md:140-144, for two chunks): M = max(m_a, m_b), w = 2^(m - M), s = s_a w_a + s_b w_b,
+// v* = v*_a w_a + v*_b w_b. Empty summaries (m = -inf) contribute nothing. Warp per row.
+__global__ void merge_pair_kernel(float* dst_o, float2* dst_ml, const float* src_o, const float2* src_ml,
+                                  int64_t rows, int d) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float2 a = dst_ml[r], b = src_ml[r];
+  const float M = fmaxf(a.x, b.x);
+  const float wa = M == -INFINITY ? 0.f : ex2_approx(a.x - M);
+  const float wb = M == -INFINITY ? 0.f : ex2_approx(b.x - M);
+  for (int i = lane; i < d; i += 32) dst_o[r * d + i] = dst_o[r * d + i] * wa + src_o[r * d + i] * wb;
+  __syncwarp();
+  if (lane == 0) dst_ml[r] = make_float2(M, a.y * wa + b.y * wb);
+}
+
+cudaError_t launch_merge_pair(float* dst_o, float2* dst_ml, const float* src_o, const float2* src_ml, int64_t rows,
+                              int d, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  const int warps = 8;
+  merge_pair_kernel<<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, s>>>(dst_o, dst_ml, src_o, src_ml,
+                                                                               rows, d);
   return cudaGetLastError();
 }
 

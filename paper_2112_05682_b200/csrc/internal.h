@@ -40,7 +40,9 @@ struct FwdParams {
   int num_q_blocks;        // ceil(q_count / 256)
   int num_splits;          // key splits (1 = online over all keys)
   int tiles_per_split;     // key tiles of 128 per split
-  float* part_o;           // [splits][B*H][q_count][64] unnormalised v*   (split mode)
+  int split_base;          // key chunk of blockIdx split 0 (tree schedule: one chunk per launch)
+  float* part_o;           // [splits][B*H][q_count][d] unnormalised v* (split / tree mode; non-null
+                           // selects the summary epilogue)
   float* part_ml;          // [splits][B*H][q_count][2]  (m* in log2 units, s*) (split mode)
   float* tri_m;            // partial mode (mea_attention_partial_fwd): [B,n_q,H] m* (natural log)
   float* tri_s;            //   [B,n_q,H] s*
@@ -74,6 +76,10 @@ cudaError_t make_bnhd_map(CUtensorMap* map, const void* base, CUtensorMapDataTyp
 cudaError_t launch_fwd_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                             const CUtensorMap& mv, cudaStream_t s);
 cudaError_t launch_merge_rows(const FwdParams& p, cudaStream_t s);
+// dst <- dst (+) src for `rows` summaries (v* [rows][d], (m* log2, s*) [rows]): the pairwise merge
+// of the tree schedule (PAPER.md:140-147 applied to two summaries).
+cudaError_t launch_merge_pair(float* dst_o, float2* dst_ml, const float* src_o, const float2* src_ml, int64_t rows,
+                              int d, cudaStream_t s);
 // d = 64 forward with double-buffered 96-key score tiles (fwd_db_sm100a.cu): online over all
 // keys (causal or not), no key split, no triple output; K/V maps with fwd_db_key_tile() rows.
 int fwd_db_key_tile();

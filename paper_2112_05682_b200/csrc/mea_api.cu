@@ -127,7 +127,17 @@ struct FwdPlan {
 // rows are processed in windows of q_chunk rows (rounded up to the 256-row CTA), one after the
 // other, as Figure 1's outer map over query chunks does, so the summaries of
 // only one query chunk are alive at a time: workspace = splits * B * H * q_window * (d + 2) f32.
+// k_chunk == MEA_CHUNK_SQRT_N (-1): the paper's sqrt(n) key chunk, ceil(sqrt(n_k)).
+int64_t resolve_k_chunk(int64_t k_chunk, int64_t n_k) {
+  if (k_chunk != MEA_CHUNK_SQRT_N) return k_chunk;
+  int64_t r = (int64_t)std::ceil(std::sqrt((double)n_k));
+  while (r > 1 && (r - 1) * (r - 1) >= n_k) --r;
+  while (r * r < n_k) ++r;
+  return std::max<int64_t>(r, 1);
+}
+
 FwdPlan plan_fwd(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t q_chunk, int64_t k_chunk, int64_t d) {
+  k_chunk = resolve_k_chunk(k_chunk, n_k);
   FwdPlan pl;
   const int64_t n_tiles = (n_k + kTileN - 1) / kTileN;
   pl.tiles_per_split = (int)n_tiles;
@@ -183,8 +193,9 @@ mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
                                               mea_dtype_t in_dtype, int64_t q_chunk, int64_t k_chunk, size_t* bytes) {
   if (!bytes) return fail(MEA_ERR_INVALID_VALUE, "bytes is NULL");
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
-  if (q_chunk < 0 || k_chunk < 0) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
+  if (q_chunk < 0 || (k_chunk < 0 && k_chunk != MEA_CHUNK_SQRT_N)) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
   if (!valid_dtype(in_dtype) && in_dtype != MEA_F32_SPLIT) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
+  k_chunk = resolve_k_chunk(k_chunk, n_k);
   if (in_dtype == MEA_F32_SPLIT)
     *bytes = (d == kHeadDim) ? f32tc_workspace(B, H, n_q, n_k) : 0;
   else if (in_dtype == MEA_F32)
@@ -204,7 +215,8 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
   if (causal && n_q != n_k) return fail(MEA_ERR_UNSUPPORTED, "causal attention needs n_q == n_k");
   if (causal && in_dtype != MEA_BF16) return fail(MEA_ERR_UNSUPPORTED, "causal attention: bf16 path only");
   if (causal) q_chunk = k_chunk = 0;  // causal runs the online schedule (no key split)
-  if (q_chunk < 0 || k_chunk < 0) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
+  if (q_chunk < 0 || (k_chunk < 0 && k_chunk != MEA_CHUNK_SQRT_N)) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
+  k_chunk = resolve_k_chunk(k_chunk, n_k);
   if ((!valid_dtype(in_dtype) && in_dtype != MEA_F32_SPLIT) || !valid_dtype(out_dtype))
     return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
   if (in_dtype == MEA_F32_SPLIT && (d != kHeadDim || out_dtype != MEA_F32 || causal || (k_chunk > 0 && k_chunk < n_k)))
@@ -336,7 +348,166 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
   return MEA_OK;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Multi-stage (tree) summarisation — PAPER.md:183: "A multi-stage summarization approach could
+// achieve O(log n)". Per query chunk, the key chunks are summarised one after another (one launch
+// of the split-mode forward kernel per chunk, split_base = chunk) and combined like a binary
+// counter: level l holds the summary of 2^l consecutive chunks; a new chunk summary merges upward
+// (merge_pair, Figure 1's rescale for two summaries) while its level is occupied. At most
+// floor(log2(chunks)) + 1 levels are occupied, plus the incoming summary, so the workspace holds
+// floor(log2(chunks)) + 2 summaries per query row instead of Figure 1's `chunks`. The remaining
+// levels are merged at the end and normalised (merge_rows over one summary: out = v*/s*, lse).
+struct TreePlan {
+  int64_t kc = 0;          // keys per chunk (a multiple of the 128-key tile)
+  int tiles_per_chunk = 0;
+  int chunks = 0;
+  int slots = 0;           // summaries alive at once
+  int64_t q_window = 0;    // query rows per pass
+  size_t ws = 0;
+};
+
+TreePlan plan_tree(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t q_chunk, int64_t k_chunk, int64_t d) {
+  TreePlan t;
+  const int64_t kc = resolve_k_chunk(k_chunk <= 0 ? MEA_CHUNK_SQRT_N : k_chunk, n_k);
+  const int64_t n_tiles = (n_k + kTileN - 1) / kTileN;
+  t.tiles_per_chunk = (int)std::min<int64_t>(n_tiles, (kc + kTileN - 1) / kTileN);
+  t.kc = (int64_t)t.tiles_per_chunk * kTileN;
+  t.chunks = (int)((n_tiles + t.tiles_per_chunk - 1) / t.tiles_per_chunk);
+  int lg = 0;
+  while ((2 << lg) <= t.chunks) ++lg;  // floor(log2(chunks))
+  t.slots = lg + 2;
+  const int rows_per_cta = d == 128 ? 128 : kRowsPerCta;
+  t.q_window = q_chunk > 0 ? std::min(n_q, (q_chunk + rows_per_cta - 1) / rows_per_cta * rows_per_cta) : n_q;
+  t.ws = (size_t)t.slots * B * H * t.q_window * (d + 2) * sizeof(float);
+  return t;
+}
+
+static mea_status_t fwd_tree_impl(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
+                                  int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t in_dtype, mea_dtype_t out_dtype,
+                                  float scale, float* lse, int64_t q_chunk, int64_t k_chunk, void* workspace,
+                                  size_t workspace_bytes, void* stream) {
+  if (mea_status_t s = check_common(B, H, n_q, n_k, d, scale)) return s;
+  if (q_chunk < 0 || (k_chunk < 0 && k_chunk != MEA_CHUNK_SQRT_N)) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
+  if (in_dtype != MEA_BF16 || !valid_dtype(out_dtype))
+    return fail(in_dtype == MEA_F32 || in_dtype == MEA_F32_SPLIT ? MEA_ERR_UNSUPPORTED : MEA_ERR_INVALID_VALUE,
+                "tree schedule: bf16 inputs, bf16 or f32 output");
+  if (d != kHeadDim && d != 128) return fail(MEA_ERR_UNSUPPORTED, "tree schedule supports d in {64, 128}");
+  if (n_q == 0) return MEA_OK;
+  if (n_k == 0) return fail(MEA_ERR_EMPTY_KEYS, "attention over an empty key list");
+  if (!q || !k || !v || !out) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out))
+    return fail(MEA_ERR_MISALIGNED, "q, k, v, out must be 16-byte aligned");
+  if (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)) return fail(MEA_ERR_MISALIGNED, "lse must be 4-byte aligned");
+  const TreePlan tp = plan_tree(B, H, n_q, n_k, q_chunk, k_chunk, d);
+  if (!workspace || workspace_bytes < tp.ws) return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "tree schedule needs workspace");
+  if (!aligned16(workspace)) return fail(MEA_ERR_MISALIGNED, "workspace must be 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int rows_per_cta = d == 128 ? 128 : kRowsPerCta;
+
+  CUtensorMap mq, mk, mv;
+  const char* why = "";
+  cudaError_t e;
+  if ((e = make_bnhd_map(&mq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_q, H, d, 64, kTileM,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+      (e = make_bnhd_map(&mk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+      (e = make_bnhd_map(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
+                         CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess)
+    return cuda_fail(e, why);
+
+  FwdParams p{};
+  p.B = (int)B;
+  p.H = (int)H;
+  p.n_q = (int)n_q;
+  p.n_k = (int)n_k;
+  p.scale = scale;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.out = out;
+  p.out_f32 = out_dtype == MEA_F32;
+  p.lse = lse;
+  p.d = (int)d;
+  p.num_splits = 1;  // one chunk per launch
+  p.tiles_per_split = tp.tiles_per_chunk;
+  const size_t slot_rows = (size_t)B * H * tp.q_window;
+  float* base_o = static_cast<float*>(workspace);
+  float2* base_ml = reinterpret_cast<float2*>(base_o + (size_t)tp.slots * slot_rows * d);
+  for (int64_t w0 = 0; w0 < n_q; w0 += tp.q_window) {
+    p.q_begin = (int)w0;
+    p.q_count = (int)std::min<int64_t>(tp.q_window, n_q - w0);
+    p.num_q_blocks = (p.q_count + rows_per_cta - 1) / rows_per_cta;
+    const int64_t rows = (int64_t)B * H * p.q_count;  // summaries of this pass, [B*H][q_count]
+    auto slot_o = [&](int sl) { return base_o + (size_t)sl * rows * d; };
+    auto slot_ml = [&](int sl) { return base_ml + (size_t)sl * rows; };
+    std::vector<int> free_slots, level_slot(tp.slots, -1);
+    for (int sl = tp.slots - 1; sl >= 0; --sl) free_slots.push_back(sl);
+    for (int c = 0; c < tp.chunks; ++c) {
+      int cur = free_slots.back();
+      free_slots.pop_back();
+      p.split_base = c;
+      p.part_o = slot_o(cur);
+      p.part_ml = reinterpret_cast<float*>(slot_ml(cur));
+      {
+        ProfScope ps(d == 128 ? "fwd128_bf16" : "fwd_bf16", st);
+        e = d == 128 ? launch_fwd128_bf16(p, mq, mk, mv, st) : launch_fwd_bf16(p, mq, mk, mv, st);
+        if (e != cudaSuccess) return cuda_fail(e, "tree chunk launch");
+      }
+      for (int l = 0;; ++l) {  // binary-counter carry
+        if (level_slot[l] < 0) {
+          level_slot[l] = cur;
+          break;
+        }
+        ProfScope ps("merge_pair", st);
+        if ((e = launch_merge_pair(slot_o(level_slot[l]), slot_ml(level_slot[l]), slot_o(cur), slot_ml(cur), rows,
+                                   (int)d, st)) != cudaSuccess)
+          return cuda_fail(e, "merge_pair launch");
+        free_slots.push_back(cur);
+        cur = level_slot[l];
+        level_slot[l] = -1;
+      }
+    }
+    // fold the occupied levels (low to high) into the highest one, then normalise
+    int acc = -1;
+    for (int l = 0; l < tp.slots; ++l) {
+      if (level_slot[l] < 0) continue;
+      if (acc >= 0) {
+        ProfScope ps("merge_pair", st);
+        if ((e = launch_merge_pair(slot_o(level_slot[l]), slot_ml(level_slot[l]), slot_o(acc), slot_ml(acc), rows,
+                                   (int)d, st)) != cudaSuccess)
+          return cuda_fail(e, "merge_pair launch");
+      }
+      acc = level_slot[l];
+    }
+    FwdParams pm = p;
+    pm.num_splits = 1;
+    pm.part_o = slot_o(acc);
+    pm.part_ml = reinterpret_cast<float*>(slot_ml(acc));
+    ProfScope ps("merge_rows", st);
+    if ((e = launch_merge_rows(pm, st)) != cudaSuccess) return cuda_fail(e, "merge_rows launch");
+  }
+  return MEA_OK;
+}
+
 extern "C" {
+
+mea_status_t mea_attention_fwd_tree(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
+                                    int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t in_dtype, mea_dtype_t out_dtype,
+                                    float scale, float* lse, int64_t q_chunk, int64_t k_chunk, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+  return fwd_tree_impl(q, k, v, out, B, H, n_q, n_k, d, in_dtype, out_dtype, scale, lse, q_chunk, k_chunk, workspace,
+                       workspace_bytes, stream);
+}
+
+mea_status_t mea_attention_fwd_tree_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                                                   mea_dtype_t in_dtype, int64_t q_chunk, int64_t k_chunk,
+                                                   size_t* bytes) {
+  if (!bytes) return fail(MEA_ERR_INVALID_VALUE, "bytes is NULL");
+  if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
+  if (q_chunk < 0 || (k_chunk < 0 && k_chunk != MEA_CHUNK_SQRT_N)) return fail(MEA_ERR_INVALID_VALUE, "negative chunk size");
+  if (in_dtype != MEA_BF16) return fail(MEA_ERR_UNSUPPORTED, "tree schedule: bf16 inputs");
+  if (d != kHeadDim && d != 128) return fail(MEA_ERR_UNSUPPORTED, "tree schedule supports d in {64, 128}");
+  *bytes = (n_q == 0 || n_k == 0) ? 0 : plan_tree(B, H, n_q, n_k, q_chunk, k_chunk, d).ws;
+  return MEA_OK;
+}
 
 mea_status_t mea_attention_fwd(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
                                int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t in_dtype, mea_dtype_t out_dtype,

@@ -119,3 +119,37 @@ def test_host_only_validation_of_the_newer_entry_points(lib):
     assert n.value == 2 * (2 * 384 * 4)
     assert lib.mea_attention_bwd_workspace_size(1, 2, 300, 300, 64, 1, 1, ctypes.byref(n)) == 0
     assert n.value > 300 * 2 * 64 * 4                       # d = 64 fused: + dq accumulator
+
+
+def test_tree_schedule_workspace_is_logarithmic(lib):
+    """mea_attention_fwd_tree_workspace_size: (floor(log2(chunks)) + 2) summaries per
+    query row, against the flat schedule's `chunks`; MEA_CHUNK_SQRT_N = ceil(sqrt(n_k)) keys
+    (rounded up to the 128-key tile) in both. Host-only argument checks."""
+    import math
+    p = ctypes.c_void_p(16)
+    B, H, d = 1, 2, 64
+    row = B * H * (d + 2) * 4
+    for n_k in (128, 1000, 16384, 1 << 20):
+        kc = math.ceil(math.sqrt(n_k))
+        chunks = -(-n_k // (-(-kc // 128) * 128))
+        t, f = ctypes.c_size_t(0), ctypes.c_size_t(0)
+        assert lib.mea_attention_fwd_tree_workspace_size(B, H, 512, n_k, d, 1, 256, -1, ctypes.byref(t)) == 0
+        assert t.value == (int(math.floor(math.log2(chunks))) + 2) * 256 * row
+        assert lib.mea_attention_fwd_workspace_size(B, H, 512, n_k, d, 1, 256, -1, ctypes.byref(f)) == 0
+        assert f.value == (chunks * 256 * row if chunks > 1 else 0)
+        if chunks >= 8:
+            assert t.value < f.value
+    # k_chunk 0 also means sqrt(n); explicit chunk, whole rows (q_chunk 0); d = 128 rows per pass
+    t = ctypes.c_size_t(0)
+    assert lib.mea_attention_fwd_tree_workspace_size(1, 1, 300, 16384, 64, 1, 0, 0, ctypes.byref(t)) == 0
+    assert t.value == (7 + 2) * 300 * 66 * 4
+    assert lib.mea_attention_fwd_tree_workspace_size(1, 1, 300, 16384, 64, 1, 0, 4096, ctypes.byref(t)) == 0
+    assert t.value == (2 + 2) * 300 * 66 * 4
+    assert lib.mea_attention_fwd_tree_workspace_size(1, 1, 300, 16384, 128, 1, 100, 4096, ctypes.byref(t)) == 0
+    assert t.value == (2 + 2) * 128 * 130 * 4
+    # invalid / unsupported: k_chunk -2, f32, d = 32, missing workspace (status 5)
+    assert lib.mea_attention_fwd_tree_workspace_size(1, 1, 8, 8, 64, 1, 0, -2, ctypes.byref(t)) == 1
+    assert lib.mea_attention_fwd_tree_workspace_size(1, 1, 8, 8, 64, 0, 0, 0, ctypes.byref(t)) == 3
+    assert lib.mea_attention_fwd_tree(p, p, p, p, 1, 1, 8, 8, 32, 1, 1, 1.0, None, 0, 0, None, 0, None) == 3
+    assert lib.mea_attention_fwd_tree(p, p, p, p, 1, 1, 8, 8, 64, 1, 1, 1.0, None, 0, 0, None, 0, None) == 5
+    assert lib.mea_attention_fwd_tree(p, p, p, p, 1, 1, 8, 0, 64, 1, 1, 1.0, None, 0, 0, None, 0, None) == 2

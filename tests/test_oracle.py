@@ -132,6 +132,31 @@ def test_merge_over_disjoint_key_ranges(rng):
     np.testing.assert_allclose(vst, v1, rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("n_k,kc", [(1, 1), (7, 1), (50, 7), (64, 1), (65, 8), (200, 13)])
+def test_tree_summarization_equals_definition_with_log_memory(rng, n_k, kc):
+    """O5t against the definition (O1): same out and lse; and the binary counter never
+    holds more than floor(log2(chunks)) + 2 summaries (the O(log n) claim), which a flat
+    Figure 1 merge (chunks summaries) exceeds as soon as chunks > 3."""
+    q, k, v = _rand(rng, 6, 5), _rand(rng, n_k, 5), _rand(rng, n_k, 3)
+    ref, ref_lse = O.naive(q, k, v, 0.7)
+    out, lse, alive = O.tree_summarize(q, k, v, 0.7, kc)
+    np.testing.assert_allclose(out, ref, atol=1e-12)
+    np.testing.assert_allclose(lse, ref_lse, atol=1e-12)
+    chunks = -(-n_k // kc)
+    assert alive <= int(math.floor(math.log2(chunks))) + 2
+    if chunks == 2 ** 6:   # all levels full just before the last carry: the bound is attained
+        assert alive == 7
+    # merge2 of a summary with an empty one is the identity; merge2 is the P = 2 case of O5
+    a = O.partial_triple(q, k, v, 0.7)
+    e = O.partial_triple(q, k[:0], v[:0], 0.7)
+    for x, y in zip(O.merge2(a, e), a):
+        np.testing.assert_allclose(x, y, atol=1e-15)
+    b1, b2 = O.partial_triple(q, k[: n_k // 2], v[: n_k // 2], 0.7), O.partial_triple(q, k[n_k // 2:], v[n_k // 2:], 0.7)
+    if n_k >= 2:
+        m, s_, vs = O.merge2(b1, b2)
+        np.testing.assert_allclose(vs / s_[:, None], O.merge(*(np.stack([b1[i], b2[i]]) for i in range(3))), atol=1e-12)
+
+
 # ---------------------------------------------------------------- P5 / P6 shift and stability
 def _shifted(q, k, c):
     """Append a feature so every score of every row gets +c exactly (scale 1)."""

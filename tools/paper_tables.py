@@ -4,7 +4,8 @@ paper's setting), n = 2^8 ... 2^20.
 
 Table 1 rows: forward time with the default (online) schedule and with the paper's chunk sizes
 (query chunk 1024 / key chunk 4096, run query chunk by query chunk, Figure 1), and the scratch
-each needs (torch peak-allocation delta with the outputs pre-allocated), beside the analytic
+each needs; with sqrt(n) key chunks, the workspace of Figure 1's flat merge vs the multi-stage
+(tree) merge of P:183 (and the tree schedule's time up to n = 2^16) (torch peak-allocation delta with the outputs pre-allocated), beside the analytic
 n^2 x 4 B score matrix of standard attention. Table 2 rows: forward + backward time with the
 paper's loss (sum of the results: dO = 1) and the backward's scratch. The paper's TPUv3 numbers
 are quoted as context (another machine; its differentiation timed jax.grad w.r.t. q only, DESIGN
@@ -79,11 +80,21 @@ def main():
             api.mea_attention_fwd(q, k, v, out=out_b, lse=lse)
             api.mea_attention_bwd(q, k, v, out_b, do, lse=lse, dq=dq, dk=dk, dv=dv)
 
+        # the paper's sqrt(n) key chunks: Figure 1's flat merge (O(sqrt n) summaries) and the
+        # multi-stage (tree) merge (O(log n) summaries), query chunks of 1024; workspace from
+        # the size functions, tree timed up to 2^16 (one launch per (query chunk, key chunk))
+        kc = api.MEA_CHUNK_SQRT_N
+        ws_flat = api.mea_attention_fwd_workspace_size(1, 1, n, n, 64, api.MEA_BF16, 1024, kc)
+        ws_tree = api.mea_attention_fwd_tree_workspace_size(1, 1, n, n, 64, api.MEA_BF16, 1024, kc)
+        tree = lambda: api.mea_attention_fwd_tree(q, k, v, out=out, lse=lse, q_chunk=1024, k_chunk=kc)  # noqa: E731
+        sqrt_cols = {"sqrt_n_flat_workspace_bytes": ws_flat, "sqrt_n_tree_workspace_bytes": ws_tree,
+                     "sqrt_n_tree_ms": timed(tree) if n <= (1 << 16) else None,
+                     "sqrt_n_tree_scratch_bytes": scratch(tree) if n <= (1 << 16) else None}
         r = {"n": n, "io_bytes": 3 * n * 64 * 2 + n * 64 * 4, "standard_scores_bytes": n * n * 4,
              "fwd_ms": timed(fwd), "fwd_scratch_bytes": scratch(fwd),
              "fwd_paper_chunks_ms": timed(fwd_paper), "fwd_paper_chunks_scratch_bytes": scratch(fwd_paper),
              "diff_ms": timed(step), "diff_scratch_bytes": scratch(step), "lse_residual_bytes": n * 4,
-             "paper_t1": PAPER_T1[n], "paper_t2": PAPER_T2[n]}
+             "paper_t1": PAPER_T1[n], "paper_t2": PAPER_T2[n], **sqrt_cols}
         rows.append(r)
         print(json.dumps(r), flush=True)
         del q, k, v, do, out, out_b, lse, dq, dk, dv
