@@ -152,6 +152,21 @@ MEA_API mea_status_t mea_attention_fwd_causal(const void* q, const void* k, cons
                                       float* lse, void* stream);
 
 /*
+ * Key padding (masking needed to drop the library into a Transformer over
+ * a padded batch; the paper disabled packing to avoid it): batch element b attends
+ * only keys j < kv_lens[b] (clamped to [0, n_k]); the masked keys get probability 0 (scores
+ * -inf in the definition). kv_lens [B] int32 is a DEVICE array (read by the
+ * kernels, never by the host; 4-byte aligned; MEA_ERR_INVALID_VALUE if NULL). A row with no
+ * keys (kv_lens[b] = 0) yields out = 0 and lse = -inf. Otherwise as mea_attention_fwd on the
+ * online schedule (no key chunks, no causal mask); bf16 inputs with d in {64, 128}
+ * (MEA_ERR_UNSUPPORTED otherwise). Padded query rows need no mask: rows are independent.
+ */
+MEA_API mea_status_t mea_attention_fwd_padded(const void* q, const void* k, const void* v, void* out,
+                                      int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                                      mea_dtype_t in_dtype, mea_dtype_t out_dtype, float scale,
+                                      float* lse, const int* kv_lens, void* stream);
+
+/*
  * Single-query attention per (b,h) — the paper's O(1)-memory algorithm (PAPER.md:59-63,
  * stabilised as in PAPER.md:85-90). q,out [B,H,d]; k,v [B,n_k,H,d]. Keys are split into
  * ranges processed in parallel (split-K); each range yields a triple (m*, s*, v*) in the
@@ -219,6 +234,17 @@ MEA_API mea_status_t mea_attention_bwd(const void* q, const void* k, const void*
                                int64_t H, int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t dtype,
                                float scale, const float* lse, void* workspace,
                                size_t workspace_bytes, void* stream);
+
+/*
+ * Backward of mea_attention_fwd_padded: as mea_attention_bwd (same workspace,
+ * mea_attention_bwd_workspace_size), with keys j >= kv_lens[b] masked (kv_lens as for the
+ * forward); their dk, dv rows are written as 0. lse NULL recomputes it with the same padding.
+ */
+MEA_API mea_status_t mea_attention_bwd_padded(const void* q, const void* k, const void* v, const void* out,
+                                      const void* dout, void* dq, void* dk, void* dv, int64_t B,
+                                      int64_t H, int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t dtype,
+                                      float scale, const float* lse, const int* kv_lens,
+                                      void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * Deterministic backward: same contract and results as mea_attention_bwd (within tolerance), but

@@ -9,5 +9,6 @@ from .api import (  # noqa: F401
     mea_attention_bwd_causal, mea_attention_fwd_causal, mea_attention_partial_fwd,
     mea_attention_fwd, mea_attention_fwd_workspace_size, mea_debug_umma_tile, mea_fill_synthetic,
     MEA_CHUNK_SQRT_N, mea_attention_fwd_tree, mea_attention_fwd_tree_workspace_size,
+    mea_attention_fwd_padded, mea_attention_bwd_padded,
     mea_merge_partials, mea_single_query_fwd, mea_single_query_partial, mea_single_query_workspace_size, version,
 )

@@ -20,6 +20,10 @@ SIGNATURES = {
     "mea_attention_fwd": (_st, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _st, _st, _f, _vp, _i64, _i64,
                                 _vp, _sz, _vp]),
     "mea_attention_fwd_workspace_size": (_st, [_i64, _i64, _i64, _i64, _i64, _st, _i64, _i64, _c.POINTER(_sz)]),
+    "mea_attention_fwd_padded": (_st, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _st, _st, _f, _vp, _vp,
+                                       _vp]),
+    "mea_attention_bwd_padded": (_st, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _st, _f,
+                                       _vp, _vp, _vp, _sz, _vp]),
     "mea_attention_fwd_tree": (_st, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _st, _st, _f, _vp, _i64,
                                      _i64, _vp, _sz, _vp]),
     "mea_attention_fwd_tree_workspace_size": (_st, [_i64, _i64, _i64, _i64, _i64, _st, _i64, _i64,

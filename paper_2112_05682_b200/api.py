@@ -288,6 +288,43 @@ def mea_attention_bwd_causal(q, k, v, out, dout, lse=None, scale=None, dq=None, 
     return _bwd(fn, mea_attention_bwd_workspace_size, q, k, v, out, dout, lse, scale, dq, dk, dv, workspace)
 
 
+def _kv_lens_dev(kv_lens, q):
+    if not (torch.is_tensor(kv_lens) and kv_lens.dtype == torch.int32 and kv_lens.is_cuda and kv_lens.is_contiguous()):
+        raise TypeError("kv_lens must be a contiguous int32 CUDA tensor [B]")
+    if kv_lens.shape != (q.shape[0],):
+        raise ValueError(f"kv_lens must have shape [B] = [{q.shape[0]}], got {tuple(kv_lens.shape)}")
+    return kv_lens
+
+
+def mea_attention_fwd_padded(q, k, v, kv_lens, scale=None, out=None, out_dtype=None, lse=None, want_lse=False):
+    """Attention with key padding: batch element b attends keys j < kv_lens[b] (int32 CUDA [B])."""
+    _cuda_contig(q, k, v, out, lse)
+    B, n_q, H, d = q.shape
+    n_k = k.shape[1]
+    if k.shape != (B, n_k, H, d) or v.shape != k.shape:
+        raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
+    kv_lens = _kv_lens_dev(kv_lens, q)
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    if out is None:
+        out = torch.empty((B, n_q, H, d), dtype=q.dtype if out_dtype is None else out_dtype, device=q.device)
+    if want_lse and lse is None:
+        lse = torch.empty((B, H, n_q), dtype=torch.float32, device=q.device)
+    _check(_lib.load().mea_attention_fwd_padded(_ptr(q), _ptr(k), _ptr(v), _ptr(out), B, H, n_q, n_k, d, _dtype(q),
+                                                _dtype(out), scale, _ptr(lse), _ptr(kv_lens), _stream(q.device)))
+    return (out, lse) if (want_lse or lse is not None) else out
+
+
+def mea_attention_bwd_padded(q, k, v, out, dout, kv_lens, lse=None, scale=None, dq=None, dk=None, dv=None,
+                             workspace=None):
+    """(dq, dk, dv) of out = mea_attention_fwd_padded(q, k, v, kv_lens) given dout."""
+    lib = _lib.load()
+    kv_lens = _kv_lens_dev(kv_lens, q)
+    fn = lambda q_, k_, v_, o_, do_, dq_, dk_, dv_, B, H, n_q, n_k, d, dt, sc, lse_, ws, nb, st: \
+        lib.mea_attention_bwd_padded(q_, k_, v_, o_, do_, dq_, dk_, dv_, B, H, n_q, n_k, d, dt, sc, lse_, _ptr(kv_lens),
+                                     ws, nb, st)
+    return _bwd(fn, mea_attention_bwd_workspace_size, q, k, v, out, dout, lse, scale, dq, dk, dv, workspace)
+
+
 def mea_attention_bwd_deterministic(q, k, v, out, dout, lse=None, scale=None, dq=None, dk=None, dv=None,
                                     workspace=None):
     """Same as mea_attention_bwd, bitwise reproducible (no cross-CTA reduction), ~2 MiB workspace."""

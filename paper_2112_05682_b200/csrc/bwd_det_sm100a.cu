@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const int g = (warp - 4) >> 2;           // query columns [NC g, NC g + NC)
     const int quarter = warp & 3;
     const int j = quarter * 32 + lane;       // key row within the tile (TMEM lane)
-    const bool key_ok = k0 + j < p.n_k;
+    const bool key_ok = k0 + j < keys_of(p.kv_lens, b, p.n_k);  // key padding: P = 0 -> dK = dV = 0
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     const float c = p.scale_log2;
     const float2 c2 = make_float2(c, c);
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
 #ifdef MEA_EXP_TIMING
       if (false) {
 #else
-      if (key_ok) {
+      if (k0 + j < p.n_k) {
 #endif
         const float sc = is_dv ? 1.f : p.scale;
         __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(is_dv ? p.dv : p.dk) +

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(kQThreads, 1)
   const int q0 = qblk * kTile;
   // causal (n_q == n_k): keys up to this block's last query row only
   const int T = p.causal ? min((p.n_k + KT - 1) / KT, (q0 + kTile + KT - 1) / KT) : (p.n_k + KT - 1) / KT;
+  const int nk = keys_of(p.kv_lens, b, p.n_k);  // key padding
   const int nq_pad = (p.n_q + kTile - 1) / kTile * kTile;
   const size_t bh = (size_t)b * p.H + h;
 
@@ -241,6 +242,11 @@ __global__ void __launch_bounds__(kQThreads, 1)
           const int key = t * KT + colhalf * (KT / 2) + (lane >> 4) * (KT / 4) + 2 * u;
           if (key > row) pr.x = 0.f;
           if (key + 1 > row) pr.y = 0.f;
+        }
+        if (p.kv_lens) {  // key padding: keys >= nk masked
+          const int key = t * KT + colhalf * (KT / 2) + (lane >> 4) * (KT / 4) + 2 * u;
+          if (key >= nk) pr.x = 0.f;
+          if (key + 1 >= nk) pr.y = 0.f;
         }
         const float2 ds = __fmul2_rn(pr, __fadd2_rn(d2, nd2));                 // P (dP - delta)
         pk[u] = pack_bf16x2(ds.x, ds.y);

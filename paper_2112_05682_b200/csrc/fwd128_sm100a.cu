@@ -64,12 +64,14 @@ __global__ void __launch_bounds__(kThreads128, 1)
   const int split = p.causal ? 0 : blockIdx.x / p.num_q_blocks;
   const int q0 = p.q_begin + qb * 128;
   const int q_end = min(p.n_q, p.q_begin + p.q_count);
-  const int n_tiles = (p.n_k + kTileN - 1) / kTileN;
+  // key padding (kv_lens, online schedule only): keys [0, nk), at least one tile (all masked if nk = 0)
+  const int nk = keys_of(p.kv_lens, b, p.n_k);
+  const int n_tiles = p.kv_lens ? max(1, (nk + kTileN - 1) / kTileN) : (p.n_k + kTileN - 1) / kTileN;
   const int t_begin = (p.split_base + split) * p.tiles_per_split;  // split_base: tree schedule, one chunk per launch
   const int t_end = p.causal ? min(n_tiles, qb + 1) : min(n_tiles, t_begin + p.tiles_per_split);
   const int T = t_end - t_begin;
   const int diag = p.causal ? qb : -1;
-  const int key_end = min(p.n_k, t_end * kTileN);
+  const int key_end = min(nk, t_end * kTileN);
 
   if (threadIdx.x == 0) {
     mbar_init(&sm.q_full, 1);

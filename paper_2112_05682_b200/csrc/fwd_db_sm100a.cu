@@ -86,8 +86,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int q_end = min(p.n_q, p.q_begin + p.q_count);
   // key tiles query tile qt needs (causal, n_q == n_k: keys below its last row + 1); the
   // producer streams the union (query tile 1's)
+  // key padding: this batch element's keys [0, nk); at least one tile runs (all masked if nk = 0)
+  const int nk = keys_of(p.kv_lens, b, p.n_k);
   auto tiles_for = [&](int qt) {
-    return ((p.causal ? min(p.n_k, q0 + (qt + 1) * kTileM) : p.n_k) + kN - 1) / kN;
+    return max(1, ((p.causal ? min(nk, q0 + (qt + 1) * kTileM) : nk) + kN - 1) / kN);
   };
   const int T = tiles_for(1);
 
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r0 = q0 + qt * kTileM;  // first row of this query tile
     const int row = r0 + rloc;
     const int Tq = tiles_for(qt);
-    const int key_lim = p.causal ? min(p.n_k, row + 1) : p.n_k;  // keys this row sees: [0, key_lim)
+    const int key_lim = p.causal ? min(nk, row + 1) : nk;  // keys this row sees: [0, key_lim)
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32 + sub * 16) << 16);
     const uint32_t colO = col_o(qt);
     const float c = p.scale_log2;
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int valid = (key_lim - t * kN) - half * 48;  // keys of this tile in my half (may be <= 0)
       uint32_t pk[24];
       // fast path: m* set, and every row of the query tile sees every key of this tile
-      bool fast = (t > 0) && (p.n_k - t * kN >= kN) && (!p.causal || (t + 1) * kN <= r0 + 1) && (c >= 0.f);
+      bool fast = (t > 0) && (nk - t * kN >= kN) && (!p.causal || (t + 1) * kN <= r0 + 1) && (c >= 0.f);
       if (fast) {
         const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
         float2 rs = make_float2(0.f, 0.f);
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_ld_wait();
     if (row < q_end) {
       const size_t bh = (size_t)b * p.H + h;
-      const float inv = 1.f / lrow;
+      const float inv = lrow > 0.f ? 1.f / lrow : 0.f;  // a row with no keys (padding): out = 0, lse = -inf
       const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + half * 32;
       if (p.out_f32) {
         float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);

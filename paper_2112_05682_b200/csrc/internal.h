@@ -49,6 +49,8 @@ struct FwdParams {
   float* tri_v;            //   [B,n_q,H,64] v* (unnormalised)
   int causal;              // query i sees keys j <= i (n_q == n_k, one window, no key split)
   int d;                   // head dimension (64: fwd_bf16, 128: fwd128_bf16); merge_rows reads it
+  const int* kv_lens;      // [B] keys per batch element (key padding: keys >= kv_lens[b] masked);
+                           // nullable; online schedule only (no causal mask, no key split)
 };
 
 struct BwdParams {
@@ -65,7 +67,13 @@ struct BwdParams {
   float* dq_acc;           // [B,n_q,H,64] f32 reduction target (fused path)
   int num_k_blocks;        // ceil(n_k / 128)
   int causal;              // query i sees keys j <= i (n_q == n_k): query tiles from the diagonal on
+  const int* kv_lens;      // [B] key padding (keys >= kv_lens[b] get P = 0 and zero dK, dV); nullable
 };
+
+// keys batch element b attends: min(n_k, max(0, kv_lens[b])) with key padding, else n_k
+__device__ __forceinline__ int keys_of(const int* kv_lens, int b, int n_k) {
+  return kv_lens ? min(n_k, max(0, __ldg(kv_lens + b))) : n_k;
+}
 
 // 4-D tensor map over a [B, n, H, d] tensor (d innermost), box {64, 1, box_rows, 1},
 // 128-byte swizzle. elem = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 or FLOAT32.

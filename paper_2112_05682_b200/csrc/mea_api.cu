@@ -210,7 +210,7 @@ mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
 static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
                              int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t in_dtype, mea_dtype_t out_dtype,
                              float scale, float* lse, int64_t q_chunk, int64_t k_chunk, void* workspace,
-                             size_t workspace_bytes, void* stream, bool causal) {
+                             size_t workspace_bytes, void* stream, bool causal, const int* kv_lens = nullptr) {
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, scale)) return s;
   if (causal && n_q != n_k) return fail(MEA_ERR_UNSUPPORTED, "causal attention needs n_q == n_k");
   if (causal && in_dtype != MEA_BF16) return fail(MEA_ERR_UNSUPPORTED, "causal attention: bf16 path only");
@@ -317,6 +317,7 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
   p.out_f32 = out_dtype == MEA_F32;
   p.lse = lse;
   p.causal = causal ? 1 : 0;
+  p.kv_lens = kv_lens;
   p.d = (int)d;
   p.num_splits = pl.splits;
   p.tiles_per_split = pl.tiles_per_split;
@@ -708,7 +709,8 @@ mea_status_t mea_attention_bwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
 static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const void* out, const void* dout, void* dq,
                              void* dk, void* dv, int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
                              mea_dtype_t dtype, float scale, const float* lse, void* workspace,
-                             size_t workspace_bytes, void* stream, bool fused, bool causal = false) {
+                             size_t workspace_bytes, void* stream, bool fused, bool causal = false,
+                             const int* kv_lens = nullptr) {
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, scale)) return s;
   if (causal && n_q != n_k) return fail(MEA_ERR_UNSUPPORTED, "causal attention needs n_q == n_k");
   if (causal && scale == 0.f) return fail(MEA_ERR_UNSUPPORTED, "causal backward needs scale != 0");
@@ -760,7 +762,7 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
     // B0: the statistics pass — rerun the forward for lse (its output goes to scratch).
     float* lse_tmp = reinterpret_cast<float*>(ws + L.lse_tmp);
     mea_status_t r = fwd_impl(q, k, v, ws + L.out_tmp, B, H, n_q, n_k, d, MEA_BF16, MEA_BF16, scale, lse_tmp, 0, 0,
-                              nullptr, 0, stream, causal);
+                              nullptr, 0, stream, causal, kv_lens);
     if (r != MEA_OK) return r;
     lse = lse_tmp;
   }
@@ -787,6 +789,7 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   p.dq_acc = dq_acc;
   p.num_k_blocks = (int)((n_k + kTileN - 1) / kTileN);
   p.causal = causal ? 1 : 0;
+  p.kv_lens = kv_lens;
   p.d = (int)d;
   if (fused) {
     {
@@ -839,6 +842,33 @@ mea_status_t mea_attention_bwd_causal(const void* q, const void* k, const void* 
                                       size_t workspace_bytes, void* stream) {
   return bwd_impl(q, k, v, out, dout, dq, dk, dv, B, H, n, n, d, dtype, scale, lse, workspace, workspace_bytes,
                   stream, true, true);
+}
+
+// Key padding: per batch element, keys >= kv_lens[b] are masked.
+static mea_status_t check_kv_lens(const int* kv_lens, mea_dtype_t dtype) {
+  if (!kv_lens) return fail(MEA_ERR_INVALID_VALUE, "kv_lens is NULL");
+  if (reinterpret_cast<uintptr_t>(kv_lens) & 3u) return fail(MEA_ERR_MISALIGNED, "kv_lens must be 4-byte aligned");
+  if (dtype != MEA_BF16) return fail(valid_dtype(dtype) ? MEA_ERR_UNSUPPORTED : MEA_ERR_INVALID_VALUE,
+                                     "key padding: bf16 path only");
+  return MEA_OK;
+}
+
+mea_status_t mea_attention_bwd_padded(const void* q, const void* k, const void* v, const void* out, const void* dout,
+                                      void* dq, void* dk, void* dv, int64_t B, int64_t H, int64_t n_q, int64_t n_k,
+                                      int64_t d, mea_dtype_t dtype, float scale, const float* lse,
+                                      const int* kv_lens, void* workspace, size_t workspace_bytes, void* stream) {
+  if (mea_status_t s = check_kv_lens(kv_lens, dtype)) return s;
+  return bwd_impl(q, k, v, out, dout, dq, dk, dv, B, H, n_q, n_k, d, dtype, scale, lse, workspace, workspace_bytes,
+                  stream, true, false, kv_lens);
+}
+
+mea_status_t mea_attention_fwd_padded(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
+                                      int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t in_dtype,
+                                      mea_dtype_t out_dtype, float scale, float* lse, const int* kv_lens,
+                                      void* stream) {
+  if (mea_status_t s = check_kv_lens(kv_lens, in_dtype)) return s;
+  return fwd_impl(q, k, v, out, B, H, n_q, n_k, d, in_dtype, out_dtype, scale, lse, 0, 0, nullptr, 0, stream, false,
+                  kv_lens);
 }
 
 mea_status_t mea_attention_bwd_deterministic_workspace_size(int64_t B, int64_t H, int64_t n_q, int64_t n_k,

@@ -153,3 +153,14 @@ def test_tree_schedule_workspace_is_logarithmic(lib):
     assert lib.mea_attention_fwd_tree(p, p, p, p, 1, 1, 8, 8, 32, 1, 1, 1.0, None, 0, 0, None, 0, None) == 3
     assert lib.mea_attention_fwd_tree(p, p, p, p, 1, 1, 8, 8, 64, 1, 1, 1.0, None, 0, 0, None, 0, None) == 5
     assert lib.mea_attention_fwd_tree(p, p, p, p, 1, 1, 8, 0, 64, 1, 1, 1.0, None, 0, 0, None, 0, None) == 2
+
+
+def test_padded_entry_points_validate_on_the_host(lib):
+    """Key padding: kv_lens NULL (1) / misaligned (4) / non-bf16 (3) rejected before any launch."""
+    p = ctypes.c_void_p(16)
+    assert lib.mea_attention_fwd_padded(p, p, p, p, 1, 1, 8, 8, 64, 1, 1, 1.0, None, None, None) == 1
+    assert lib.mea_attention_fwd_padded(p, p, p, p, 1, 1, 8, 8, 64, 1, 1, 1.0, None, ctypes.c_void_p(18), None) == 4
+    assert lib.mea_attention_fwd_padded(p, p, p, p, 1, 1, 8, 8, 64, 0, 0, 1.0, None, p, None) == 3
+    assert lib.mea_attention_bwd_padded(p, p, p, p, p, p, p, p, 1, 1, 8, 8, 64, 1, 1.0, None, None, None, 0, None) == 1
+    assert lib.mea_attention_bwd_padded(p, p, p, p, p, p, p, p, 1, 1, 8, 8, 64, 0, 1.0, None, p, None, 0, None) == 3
+    assert lib.mea_attention_bwd_padded(p, p, p, p, p, p, p, p, 1, 1, 8, 8, 64, 1, 1.0, None, p, p, 16, None) == 5
