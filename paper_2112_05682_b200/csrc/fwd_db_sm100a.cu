@@ -224,6 +224,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = r0 + rloc;
     const int Tq = tiles_for(qt);
     const int key_lim = p.causal ? min(nk, row + 1) : nk;  // keys this row sees: [0, key_lim)
+    // tiles [0, full) are complete for every row of the query tile (fast-path candidates)
+    const int full = (p.causal ? min(nk, r0 + 1) : nk) / kN;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32 + sub * 16) << 16);
     const uint32_t colO = col_o(qt);
     const float c = p.scale_log2;
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int valid = (key_lim - t * kN) - half * 48;  // keys of this tile in my half (may be <= 0)
       uint32_t pk[24];
       // fast path: m* set, and every row of the query tile sees every key of this tile
-      bool fast = (t > 0) && (nk - t * kN >= kN) && (!p.causal || (t + 1) * kN <= r0 + 1) && (c >= 0.f);
+      bool fast = (t > 0) && (t < full) && (c >= 0.f);
       if (fast) {
         const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
         float2 rs = make_float2(0.f, 0.f);
