@@ -291,6 +291,7 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
   }
   const int64_t nqb = (n_q + rows_per_cta - 1) / rows_per_cta;
   if (nqb * pl.splits > kMaxInt) return fail(MEA_ERR_UNSUPPORTED, "grid too large");
+  if (causal && nqb * B * H > kMaxInt) return fail(MEA_ERR_UNSUPPORTED, "causal grid (blocks x B x H) too large");
 
   // the plain d = 64 forward (online over all keys, no mask) runs the double-buffered kernel
   const bool use_db = MEA_FWD_DB && d == kHeadDim && pl.splits == 1;
@@ -735,6 +736,9 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(dout) || !aligned16(dq) ||
       !aligned16(dk) || !aligned16(dv))
     return fail(MEA_ERR_MISALIGNED, "tensors must be 16-byte aligned");
+  // causal grids are 1-D over (key or query blocks) x B x H
+  if (causal && ((std::max(n_q, n_k) + 63) / 64) * B * H > kMaxInt)
+    return fail(MEA_ERR_UNSUPPORTED, "causal grid (blocks x B x H) too large");
   const BwdLayout L = bwd_layout(B, H, n_q, d, lse != nullptr, fused);
   if (!workspace || workspace_bytes < L.total) return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "backward workspace");
   if (!aligned16(workspace)) return fail(MEA_ERR_MISALIGNED, "workspace must be 16-byte aligned");
