@@ -38,6 +38,8 @@
 // then applies Figure 1's global-max rescale (lines 33-40).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -83,6 +85,7 @@ struct FwdSmem {
   uint64_t p_full[2];
   uint64_t o_done[2];
   uint32_t tmem_base;
+  uint32_t merge_last;  // fused merge: this CTA is the last split of its query block
 };
 constexpr size_t kFwdSmemBytes = sizeof(FwdSmem) + 1024;
 
@@ -124,6 +127,9 @@ __device__ __forceinline__ constexpr bool poly_pair(int i) { return ((MEA_POLY_M
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_bf16_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                     const __grid_constant__ CUtensorMap mv, const FwdParams p) {
+  // PDL: the next kernel in the stream (the window's merge) may be scheduled now; it waits for
+  // this grid's results itself (griddepcontrol.wait)
+  asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ uint8_t smem_raw[];
   FwdSmem& sm = *reinterpret_cast<FwdSmem*>(align1024(smem_raw));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -425,6 +431,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t o[32];
     tmem_ld32_split<32>(lane_base + colO, o);
     tmem_ld_wait();
+    // PDL: the previous kernel (the last window's merge) reads the summaries this epilogue
+    // overwrites; everything above (all of Q/K/V's streaming) overlapped its drain
+    if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (row < q_end) {
       const size_t bh = (size_t)b * p.H + h;
       if (p.tri_v) {
@@ -473,6 +482,47 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       }
     }
+    if (p.merge_cnt) {
+      // Fused merge of the key-split summaries (Figure 1 lines 33-40): the last
+      // of the num_splits CTAs of this query block to finish merges its 256 rows, so no separate
+      // merge launch sits between two query windows (threadfence-reduction pattern).
+      __threadfence();
+      named_bar_sync(1, 512);  // the 16 softmax warps have written this CTA's summaries
+      if (sw == 0 && lane == 0) {
+        const size_t ci = ((size_t)b * p.H + h) * p.num_q_blocks + qblk;
+        const unsigned prev = atomicAdd(p.merge_cnt + ci, 1u);
+        sm.merge_last = prev == (unsigned)(p.num_splits - 1);
+        if (sm.merge_last) p.merge_cnt[ci] = 0u;  // every split has arrived: reset for the next window
+      }
+      named_bar_sync(1, 512);
+      if (sm.merge_last) {
+        __threadfence();
+        const size_t bh = (size_t)b * p.H + h, stride = (size_t)p.B * p.H * p.q_count;
+        const float2* ml = reinterpret_cast<const float2*>(p.part_ml);
+        for (int rr = sw; rr < kRowsPerCta; rr += 16) {  // warp sw: rows sw, sw + 16, ... of the block
+          const int grow = q0 + rr;
+          if (grow >= q_end) break;
+          const size_t r = bh * p.q_count + (grow - p.q_begin);
+          float M = -INFINITY;
+          for (int s = 0; s < p.num_splits; ++s) M = fmaxf(M, __ldcg(&ml[s * stride + r]).x);
+          float den = 0.f;
+          float2 acc = make_float2(0.f, 0.f);
+          for (int s = 0; s < p.num_splits; ++s) {
+            const float2 t = __ldcg(&ml[s * stride + r]);
+            const float w = ex2_approx(t.x - M);
+            den += w * t.y;
+            const float2 ov = __ldcg(reinterpret_cast<const float2*>(p.part_o + (s * stride + r) * kHeadDim) + lane);
+            acc.x += w * ov.x;
+            acc.y += w * ov.y;
+          }
+          const float inv = 1.f / den;
+          const size_t off = (((size_t)b * p.n_q + grow) * p.H + h) * kHeadDim + 2 * lane;
+          if (p.out_f32) reinterpret_cast<float2*>(static_cast<float*>(p.out) + off)[0] = make_float2(acc.x * inv, acc.y * inv);
+          else reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(p.out) + off)[0] = pack_bf16x2(acc.x * inv, acc.y * inv);
+          if (p.lse && lane == 0) p.lse[bh * p.n_q + grow] = (M + __log2f(den)) * 0.6931471805599453f;
+        }
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -485,37 +535,43 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Figure 1 lines 33-40 over the key-split partials of each query row:
 // M = max_c m_c; out = sum_c 2^(m_c - M) v*_c / sum_c 2^(m_c - M) s*_c. One warp per row.
 __global__ void merge_rows_kernel(const FwdParams p) {
+  // PDL trigger first: the grid is small enough to be resident at once, so the next window's
+  // forward may start on the SMs the current forward's last wave leaves idle (it waits for this
+  // merge itself before overwriting the summaries); then wait for this window's summaries
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t rows = (int64_t)p.B * p.H * p.q_count;  // rows of this query window
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
   const int64_t stride = rows;  // rows per split
   const int d = p.d, per = d / 32;  // 2 (d = 64) or 4 (d = 128) features per lane
   const float2* ml = reinterpret_cast<const float2*>(p.part_ml);
-  float M = -INFINITY;
-  for (int s = 0; s < p.num_splits; ++s) M = fmaxf(M, ml[s * stride + r].x);
-  float den = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int s = 0; s < p.num_splits; ++s) {
-    const float2 t = ml[s * stride + r];
-    const float w = ex2_approx(t.x - M);
-    den += w * t.y;
-    const float* o = p.part_o + (s * stride + r) * d + per * lane;
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; r < rows;
+       r += (int64_t)gridDim.x * (blockDim.x / 32)) {
+    float M = -INFINITY;
+    for (int s = 0; s < p.num_splits; ++s) M = fmaxf(M, ml[s * stride + r].x);
+    float den = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int s = 0; s < p.num_splits; ++s) {
+      const float2 t = ml[s * stride + r];
+      const float w = ex2_approx(t.x - M);
+      den += w * t.y;
+      const float* o = p.part_o + (s * stride + r) * d + per * lane;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i < per) acc[i] += w * o[i];
-  }
-  const int64_t bh = r / p.q_count, row = p.q_begin + r % p.q_count;
-  if (row >= p.n_q) return;
-  const int64_t b = bh / p.H, h = bh % p.H;
-  const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * d + per * lane;
-  const float inv = 1.f / den;
+      for (int i = 0; i < 4; ++i)
+        if (i < per) acc[i] += w * o[i];
+    }
+    const int64_t bh = r / p.q_count, row = p.q_begin + r % p.q_count;
+    if (row >= p.n_q) continue;
+    const int64_t b = bh / p.H, h = bh % p.H;
+    const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * d + per * lane;
+    const float inv = 1.f / den;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (i >= per) break;
-    if (p.out_f32) static_cast<float*>(p.out)[off + i] = acc[i] * inv;
-    else static_cast<__nv_bfloat16*>(p.out)[off + i] = __float2bfloat16_rn(acc[i] * inv);
+    for (int i = 0; i < 4; ++i) {
+      if (i >= per) break;
+      if (p.out_f32) static_cast<float*>(p.out)[off + i] = acc[i] * inv;
+      else static_cast<__nv_bfloat16*>(p.out)[off + i] = __float2bfloat16_rn(acc[i] * inv);
+    }
+    if (p.lse && lane == 0) p.lse[bh * p.n_q + row] = (M + __log2f(den)) * 0.6931471805599453f;
   }
-  if (p.lse && lane == 0) p.lse[bh * p.n_q + row] = (M + __log2f(den)) * 0.6931471805599453f;
 }
 
 // ---------------------------------------------------------------------------- debug probe
@@ -598,8 +654,21 @@ cudaError_t launch_fwd_bf16(const FwdParams& p, const CUtensorMap& mq, const CUt
   const cudaError_t attr = ensure_smem_attr<fwd_bf16_kernel>((int)kFwdSmemBytes);
   if (attr != cudaSuccess) return attr;
   const dim3 grid = p.causal ? dim3(p.num_q_blocks * p.H * p.B) : dim3(p.num_q_blocks * p.num_splits, p.H, p.B);
-  fwd_bf16_kernel<<<grid, kThreads, kFwdSmemBytes, s>>>(mq, mk, mv, p);
-  return cudaGetLastError();
+  if (!p.pdl) {
+    fwd_bf16_kernel<<<grid, kThreads, kFwdSmemBytes, s>>>(mq, mk, mv, p);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kFwdSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fwd_bf16_kernel, mq, mk, mv, p);
 }
 
 // The triple of an empty key range: (m*, s*, v*) = (-inf, 0, 0) (PAPER.md:89's initial state).
@@ -621,8 +690,17 @@ cudaError_t launch_empty_triples(float* m, float* s, float* vstar, int64_t rows,
 cudaError_t launch_merge_rows(const FwdParams& p, cudaStream_t s) {
   const int64_t rows = (int64_t)p.B * p.H * p.q_count;
   const int warps = 8;
-  merge_rows_kernel<<<(unsigned)((rows + warps - 1) / warps), warps * 32, 0, s>>>(p);
-  return cudaGetLastError();
+  // PDL: scheduled while the forward grid drains; waits for its summaries (griddepcontrol.wait)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)std::min<int64_t>((rows + warps - 1) / warps, 148 * 4));  // resident at once
+  cfg.blockDim = dim3(warps * 32);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, merge_rows_kernel, p);
 }
 
 // Two summaries of the same query rows over disjoint key ranges -> one (Figure 1 lines 33-36,

@@ -49,6 +49,11 @@ struct FwdParams {
   float* tri_v;            //   [B,n_q,H,64] v* (unnormalised)
   int causal;              // query i sees keys j <= i (n_q == n_k, one window, no key split)
   int d;                   // head dimension (64: fwd_bf16, 128: fwd128_bf16); merge_rows reads it
+  unsigned* merge_cnt;     // d = 64 key split: [B*H][num_q_blocks] arrival counters (zeroed, self-
+                           // resetting); the last split CTA of a query block merges its rows
+  int pdl;                 // programmatic dependent launch (key-split windows after the first): the
+                           // kernel may start while the previous window's merge drains; it waits
+                           // (griddepcontrol.wait) only before its first global write
   const int* kv_lens;      // [B] keys per batch element (key padding: keys >= kv_lens[b] masked);
                            // nullable; online schedule only (no causal mask, no key split)
 };

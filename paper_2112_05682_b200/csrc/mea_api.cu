@@ -120,6 +120,7 @@ struct FwdPlan {
   int splits = 1, tiles_per_split = 0;
   int64_t q_window = 0;  // query rows per launch (split mode): the paper's query chunk
   size_t ws = 0;
+  size_t cnt_off = 0;    // d = 64: byte offset of the fused merge's arrival counters
 };
 
 // Key split (k_chunk < n_k): Figure 1's summaries of key chunks of k_chunk keys (rounded up to
@@ -150,6 +151,10 @@ FwdPlan plan_fwd(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t q_chunk
       pl.tiles_per_split = (int)tps;
       if (q_chunk > 0) pl.q_window = std::min(n_q, (q_chunk + kRowsPerCta - 1) / kRowsPerCta * kRowsPerCta);
       pl.ws = (size_t)splits * B * H * pl.q_window * (d + 2) * sizeof(float);
+      if (d == kHeadDim) {  // + one arrival counter per (b, h, 256-row query block of a window)
+        pl.cnt_off = (pl.ws + 15) / 16 * 16;
+        pl.ws = pl.cnt_off + (size_t)B * H * ((pl.q_window + kRowsPerCta - 1) / kRowsPerCta) * sizeof(unsigned);
+      }
     }
   }
   return pl;
@@ -326,12 +331,21 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
     const size_t rows = (size_t)pl.splits * B * H * pl.q_window;
     p.part_o = static_cast<float*>(workspace);
     p.part_ml = p.part_o + rows * d;
+    if (d == kHeadDim) {  // fused merge (last split CTA per query block); counters start at 0
+      p.merge_cnt = reinterpret_cast<unsigned*>(static_cast<uint8_t*>(workspace) + pl.cnt_off);
+      if ((e = cudaMemsetAsync(p.merge_cnt, 0, pl.ws - pl.cnt_off, st)) != cudaSuccess)
+        return cuda_fail(e, "merge counter reset");
+    }
   }
   // one window (all rows) unless the key-split schedule runs query chunk by query chunk
   for (int64_t w0 = 0; w0 < n_q; w0 += pl.q_window) {
     p.q_begin = (int)w0;
     p.q_count = (int)std::min<int64_t>(pl.q_window, n_q - w0);
     p.num_q_blocks = (p.q_count + rows_per_cta - 1) / rows_per_cta;
+    // windows after the first follow our own forward (its fused merge does not touch q, k, v):
+    // the d = 64 split forward may start on the SMs its last wave leaves idle (PDL) and waits for
+    // it only before writing summaries
+    p.pdl = (w0 > 0 && p.merge_cnt) ? 1 : 0;
     if (d == 128) {
       ProfScope ps("fwd128_bf16", st);
       if ((e = launch_fwd128_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd128_bf16 launch");
@@ -342,7 +356,7 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
       ProfScope ps("fwd_bf16", st);
       if ((e = launch_fwd_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_bf16 launch");
     }
-    if (pl.splits > 1) {
+    if (pl.splits > 1 && !p.merge_cnt) {
       ProfScope ps("merge_rows", st);
       if ((e = launch_merge_rows(p, st)) != cudaSuccess) return cuda_fail(e, "merge_rows launch");
     }

@@ -53,11 +53,13 @@ def test_host_only_calls(lib):
     assert lib.mea_attention_fwd_workspace_size(1, 16, 16384, 16384, 64, 1, 0, 0, ctypes.byref(n)) == 0
     assert n.value == 0
     assert lib.mea_attention_fwd_workspace_size(1, 16, 16384, 16384, 64, 1, 1024, 4096, ctypes.byref(n)) == 0
-    assert n.value == 4 * 16 * 1024 * 66 * 4     # one query chunk of summaries alive
+    # one query chunk of summaries alive + the fused merge's arrival counters
+    # (one per (b, h, 256-row query block of the window), after 16-byte alignment)
+    assert n.value == 4 * 16 * 1024 * 66 * 4 + 16 * 4 * 4
     assert lib.mea_attention_fwd_workspace_size(1, 16, 16384, 16384, 64, 1, 0, 4096, ctypes.byref(n)) == 0
-    assert n.value == 4 * 16 * 16384 * 66 * 4    # q_chunk 0: all rows in one launch
+    assert n.value == 4 * 16 * 16384 * 66 * 4 + 16 * 64 * 4    # q_chunk 0: all rows in one launch
     assert lib.mea_attention_fwd_workspace_size(1, 16, 16384, 16384, 64, 1, 300, 4096, ctypes.byref(n)) == 0
-    assert n.value == 4 * 16 * 512 * 66 * 4      # q_chunk rounded up to the 256-row CTA
+    assert n.value == 4 * 16 * 512 * 66 * 4 + 16 * 2 * 4       # q_chunk rounded up to the 256-row CTA
     assert lib.mea_attention_fwd_workspace_size(1, 16, 16384, 16384, 64, 1, 1024, 16384, ctypes.byref(n)) == 0
     assert n.value == 0                          # k_chunk >= n_k: no key split, q_chunk has no effect
     # single-query workspace is independent of n_k once the split count saturates
@@ -136,7 +138,8 @@ def test_tree_schedule_workspace_is_logarithmic(lib):
         assert lib.mea_attention_fwd_tree_workspace_size(B, H, 512, n_k, d, 1, 256, -1, ctypes.byref(t)) == 0
         assert t.value == (int(math.floor(math.log2(chunks))) + 2) * 256 * row
         assert lib.mea_attention_fwd_workspace_size(B, H, 512, n_k, d, 1, 256, -1, ctypes.byref(f)) == 0
-        assert f.value == (chunks * 256 * row if chunks > 1 else 0)
+        flat = chunks * 256 * row
+        assert f.value == ((flat + 15) // 16 * 16 + B * H * 4 if chunks > 1 else 0)
         if chunks >= 8:
             assert t.value < f.value
     # k_chunk 0 also means sqrt(n); explicit chunk, whole rows (q_chunk 0); d = 128 rows per pass

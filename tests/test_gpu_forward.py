@@ -75,7 +75,9 @@ def test_bf16_query_chunk_windows():
     ref, ref_lse = O.mha_forward(q, k, v, 0.125)
     for qc in (1, 256, 300, 600, 1100, 5000):
         ws = api.mea_attention_fwd_workspace_size(2, 2, 1100, 700, 64, api.MEA_BF16, qc, 256)
-        assert ws == 3 * 2 * 2 * min(1100, -(-qc // 256) * 256) * 66 * 4
+        rows = min(1100, -(-qc // 256) * 256)
+        # summaries of one window (16-byte aligned) + one merge arrival counter per (b, h, block)
+        assert ws == -(-(3 * 2 * 2 * rows * 66 * 4) // 16) * 16 + 2 * 2 * (-(-rows // 256)) * 4
         b, lb = _run(q, k, v, scale=0.125, k_chunk=256, q_chunk=qc)
         Hh.assert_close_bf16(b, ref)
         assert np.abs(lb - ref_lse).max() < 1e-3

@@ -3,7 +3,7 @@ shape (B=1, H=16, n=16384, bf16): calls alternate build by build so every build 
 clock / power state, with a 512 MiB L2 read-flush before each call; results are compared with the
 first build's (experiments only; parity is tests/).
 
-    CASE=fwd|fwd_causal|bwd|bwd_causal|bwd_det|fwd128|bwd128 ITERS=30 python tools/ab.py A.so B.so ...
+    CASE=fwd|fwd_paper|fwd_causal|bwd|bwd_causal|bwd_det|fwd128|bwd128 ITERS=30 python tools/ab.py A.so B.so ...
 """
 import ctypes, os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -39,6 +39,8 @@ flops = (4 if case.startswith("fwd") else 10) * vis * d * H
 
 
 def call():
+    if case == "fwd_paper":   # configs[2]'s literal schedule: query chunk 1024, key chunk 4096
+        return (api.mea_attention_fwd(q, k, v, q_chunk=1024, k_chunk=4096),)
     if case.startswith("fwd"):
         return (fwd(q, k, v),)
     bwd = {"bwd": api.mea_attention_bwd, "bwd128": api.mea_attention_bwd, "bwd_det": api.mea_attention_bwd_deterministic,
