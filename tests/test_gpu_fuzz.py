@@ -1,0 +1,93 @@
+"""Seeded random sweep over the whole entry-point surface against the float64 oracle (O1, O5,
+O5t, O6 and their causal / truncated-key forms): shapes (ragged against every tile size: 96-key
+and 128-key tiles, 128- and 256-row query blocks), head dims 64 / 128, scales of either sign and
+zero, output dtypes, key chunks, query chunks, padding and causal masks. Each case is small enough
+for the oracle; the point is breadth — a schedule or mask combination that breaks shows up here
+even if no hand-written case hits it.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from tests import helpers as Hh
+
+pytestmark = pytest.mark.gpu
+
+N_CASES = 150
+
+
+def _case(i):
+    r = np.random.default_rng(1000 + i)
+    d = int(r.choice([64, 128]))
+    B, H = int(r.integers(1, 3)), int(r.integers(1, 3))
+    n_q, n_k = int(r.integers(1, 520)), int(r.integers(1, 700))
+    scale = float(r.choice([1 / math.sqrt(d), 0.5, -0.2, 0.0, 0.02]))
+    mode = str(r.choice(["plain", "chunks", "causal", "padded", "tree"]))
+    out_f32 = bool(r.integers(0, 2))
+    return dict(d=d, B=B, H=H, n_q=n_q, n_k=n_k, scale=scale, mode=mode, out_f32=out_f32,
+                q_chunk=int(r.choice([0, 1, 300, 1024])), k_chunk=int(r.choice([1, 128, 200, 4096, -1])),
+                lens=[int(x) for x in r.integers(0, n_k + 1, size=B)], seed=i)
+
+
+@pytest.mark.parametrize("i", range(N_CASES))
+def test_forward_and_backward_random_case(i):
+    from paper_2112_05682_b200 import api
+    c = _case(i)
+    d, B, H, n_q, n_k, scale = c["d"], c["B"], c["H"], c["n_q"], c["n_k"], c["scale"]
+    if c["mode"] == "causal":
+        n_k = n_q
+    q, k, v, do = Hh.host_inputs(B, n_q, n_k, H, d, seed=c["seed"], with_dout=True)
+    qd, kd, vd, dod = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v, do))
+    od = torch.float32 if c["out_f32"] else torch.bfloat16
+    mode = c["mode"]
+    lens = [min(L, n_k) for L in c["lens"]]
+    if mode == "plain":
+        out, lse = api.mea_attention_fwd(qd, kd, vd, scale=scale, out_dtype=od, want_lse=True)
+    elif mode == "chunks":
+        out, lse = api.mea_attention_fwd(qd, kd, vd, scale=scale, out_dtype=od, want_lse=True,
+                                         q_chunk=c["q_chunk"], k_chunk=c["k_chunk"])
+    elif mode == "tree":
+        out, lse = api.mea_attention_fwd_tree(qd, kd, vd, scale=scale, out_dtype=od, want_lse=True,
+                                              q_chunk=c["q_chunk"], k_chunk=c["k_chunk"])
+    elif mode == "causal":
+        out, lse = api.mea_attention_fwd_causal(qd, kd, vd, scale=scale, out_dtype=od, want_lse=True)
+    else:
+        kl = torch.tensor(lens, dtype=torch.int32, device="cuda")
+        out, lse = api.mea_attention_fwd_padded(qd, kd, vd, kl, scale=scale, out_dtype=od, want_lse=True)
+    torch.cuda.synchronize()
+    got, glse = out.double().cpu().numpy(), lse.double().cpu().numpy()
+    causal = mode == "causal"
+    for b in range(B):
+        L = lens[b] if mode == "padded" else n_k
+        if L == 0:   # padded element with no keys: out 0, lse -inf
+            assert (got[b] == 0).all() and np.isneginf(glse[b]).all()
+            continue
+        ref, ref_lse = O.mha_forward(q[b:b + 1], k[b:b + 1, :L], v[b:b + 1, :L], scale, causal=causal)
+        Hh.assert_close_bf16(got[b:b + 1], ref, what=f"case {i} {mode} out")
+        assert np.abs(glse[b:b + 1] - ref_lse).max() < 1e-3, f"case {i} {mode} lse"
+    # backward on the modes that have one (the padded / causal / plain forward's)
+    if mode in ("plain", "causal", "padded") and scale != 0.0 and all(L > 0 for L in lens):
+        ob = out if out.dtype == torch.bfloat16 else out.to(torch.bfloat16)
+        if mode == "plain":
+            dq, dk, dv = api.mea_attention_bwd(qd, kd, vd, ob, dod, lse=lse, scale=scale)
+        elif mode == "causal":
+            dq, dk, dv = api.mea_attention_bwd_causal(qd, kd, vd, ob, dod, lse=lse, scale=scale)
+        else:
+            dq, dk, dv = api.mea_attention_bwd_padded(qd, kd, vd, ob, dod, kl, lse=lse, scale=scale)
+        torch.cuda.synchronize()
+        dq, dk, dv = (x.double().cpu().numpy() for x in (dq, dk, dv))
+        # dq = scale dS K and dk = scale dS^T Q carry the bf16 rounding of dS (an MMA operand) times
+        # `scale`: the north star's 5e-2 is stated at the standard scale 1/sqrt(d), so the bar
+        # grows with |scale| sqrt(d) beyond it (reading 16)
+        gtol = Hh.TOL_BF16_GRAD * max(1.0, abs(scale) * math.sqrt(d))
+        for b in range(B):
+            L = lens[b] if mode == "padded" else n_k
+            rq, rk, rv = O.mha_backward(q[b:b + 1], k[b:b + 1, :L], v[b:b + 1, :L], do[b:b + 1], scale, causal=causal)
+            for g, r, nm in ((dq[b:b + 1], rq, "dq"), (dk[b:b + 1, :L], rk, "dk"), (dv[b:b + 1, :L], rv, "dv")):
+                Hh.assert_close_bf16(g, r, abs_tol=gtol if nm != "dv" else Hh.TOL_BF16_GRAD, rel_tol=Hh.REL_NORM_GRAD,
+                                     what=f"case {i} {nm}")
+            if L < n_k:
+                assert (dk[b, L:] == 0).all() and (dv[b, L:] == 0).all()
