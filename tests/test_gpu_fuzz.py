@@ -91,3 +91,68 @@ def test_forward_and_backward_random_case(i):
                                      what=f"case {i} {nm}")
             if L < n_k:
                 assert (dk[b, L:] == 0).all() and (dv[b, L:] == 0).all()
+
+
+@pytest.mark.parametrize("i", range(60))
+def test_other_entry_points_random_case(i):
+    """Single query (bf16 d 64/128, f32), key-range partials merged, the deterministic backward
+    and the fp32 forwards (exact SIMT and split-precision) on random shapes."""
+    from paper_2112_05682_b200 import api
+    r = np.random.default_rng(5000 + i)
+    kind = ["single_query", "partial_merge", "bwd_det", "f32"][i % 4]
+    d = int(r.choice([64, 128]))
+    B, H = int(r.integers(1, 3)), int(r.integers(1, 4))
+    n_q, n_k = int(r.integers(1, 400)), int(r.integers(1, 3000))
+    scale = float(r.choice([1 / math.sqrt(d), -0.1, 0.03]))
+    if kind == "single_query":
+        f32 = bool(r.integers(0, 2))
+        q, k, v = Hh.host_inputs(B, 1, n_k, H, d, seed=i, dtype="f32" if f32 else "bf16")
+        dt = torch.float32 if f32 else torch.bfloat16
+        out = api.mea_single_query_fwd(Hh.to_dev(q[:, 0], dt), Hh.to_dev(k, dt), Hh.to_dev(v, dt), scale=scale,
+                                       out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        got = out.double().cpu().numpy()
+        for b in range(B):
+            for h in range(H):
+                ref = O.naive(q[b, 0, h][None], k[b, :, h], v[b, :, h], scale)[0][0]
+                if f32:
+                    Hh.assert_close_f32(got[b, h], ref)
+                else:
+                    Hh.assert_close_bf16(got[b, h], ref)
+    elif kind == "partial_merge":
+        q, k, v = Hh.host_inputs(B, n_q, n_k, H, d, seed=i)
+        cuts = sorted({0, n_k, *[int(x) for x in r.integers(0, n_k + 1, size=int(r.integers(0, 4)))]})
+        qd = Hh.to_dev(q, torch.bfloat16)
+        parts = [api.mea_attention_partial_fwd(qd, Hh.to_dev(k[:, a:b_], torch.bfloat16),
+                                               Hh.to_dev(v[:, a:b_], torch.bfloat16), scale=scale)
+                 for a, b_ in zip(cuts[:-1], cuts[1:])]
+        out = api.mea_merge_partials(torch.stack([p_[0].reshape(-1) for p_ in parts]),
+                                     torch.stack([p_[1].reshape(-1) for p_ in parts]),
+                                     torch.stack([p_[2].reshape(-1, d) for p_ in parts]), B, n_q * H,
+                                     out_dtype=torch.float32).reshape(B, n_q, H, d)
+        torch.cuda.synchronize()
+        Hh.assert_close_bf16(out.double().cpu().numpy(), O.mha_forward(q, k, v, scale)[0])
+    elif kind == "bwd_det":
+        n_k = min(n_k, 800)
+        q, k, v, do = Hh.host_inputs(B, n_q, n_k, H, d, seed=i, with_dout=True)
+        qd, kd, vd, dod = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v, do))
+        out, lse = api.mea_attention_fwd(qd, kd, vd, scale=scale, want_lse=True)
+        g = api.mea_attention_bwd_deterministic(qd, kd, vd, out, dod, lse=lse if i % 8 else None, scale=scale)
+        torch.cuda.synchronize()
+        gtol = Hh.TOL_BF16_GRAD * max(1.0, abs(scale) * math.sqrt(d))
+        for x, ref, nm in zip(g, O.mha_backward(q, k, v, do, scale), ("dq", "dk", "dv")):
+            Hh.assert_close_bf16(x.double().cpu().numpy(), ref, abs_tol=gtol, rel_tol=Hh.REL_NORM_GRAD, what=nm)
+    else:
+        n_q, n_k = min(n_q, 200), min(n_k, 600)
+        split = d == 64 and bool(r.integers(0, 2))
+        q, k, v = Hh.host_inputs(B, n_q, n_k, H, d, seed=i, dtype="f32")
+        out, lse = api.mea_attention_fwd(Hh.to_dev(q, torch.float32), Hh.to_dev(k, torch.float32),
+                                         Hh.to_dev(v, torch.float32), scale=scale, want_lse=True, f32_split=split)
+        torch.cuda.synchronize()
+        ref, ref_lse = O.mha_forward(q, k, v, scale)
+        got = out.double().cpu().numpy()
+        if split:   # the split-precision bound (tests/test_gpu_forward.py): 1e-5 + 3 2^-18 max|v|
+            assert np.abs(got - ref).max() <= 1e-5 + 3 * 2.0 ** -18 * np.abs(v).max()
+        else:
+            Hh.assert_close_f32(got, ref)
+        assert np.abs(lse.double().cpu().numpy() - ref_lse).max() < 1e-5
