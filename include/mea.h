@@ -96,10 +96,10 @@ MEA_API const char* mea_last_error_detail(void);
  *     keys). With a key split, q_chunk > 0 processes the query rows in chunks of
  *     q_chunk rows (rounded up to 256), one after another, as Figure 1's outer map over
  *     query chunks does, so only one chunk's summaries are alive:
- *     workspace = splits * B * H * min(n_q, q_chunk') * (d + 2) * 4 bytes (at d = 64 rounded
- *     up to 16 bytes, + 4 bytes per (b, h, 256-row query block of a chunk): the arrival
- *     counters of the merge, which the last key-chunk CTA of each query block performs in the
- *     same launch). Without a key split q_chunk has no effect. Results do not depend on q_chunk.
+ *     workspace = splits * B * H * min(n_q, q_chunk') * (d + 2) * 4 bytes (at d = 64 with at
+ *     most 16 splits rounded up to 16 bytes, + 4 bytes per (b, h, 256-row query block of a
+ *     chunk): the arrival counters of the merge, which the last key-chunk CTA of each query
+ *     block then performs in the same launch). Without a key split q_chunk has no effect. Results do not depend on q_chunk.
  *   in_dtype MEA_BF16 requires d in {64, 128} and out_dtype in {BF16, F32};
  *   in_dtype MEA_F32 requires d <= 128, out_dtype F32 and k_chunk == 0.
  */

@@ -503,17 +503,33 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int grow = q0 + rr;
           if (grow >= q_end) break;
           const size_t r = bh * p.q_count + (grow - p.q_begin);
+          // two passes over the splits, 4 summaries in flight per step (few registers: this code
+          // shares the softmax warps' register budget)
           float M = -INFINITY;
-          for (int s = 0; s < p.num_splits; ++s) M = fmaxf(M, __ldcg(&ml[s * stride + r]).x);
+          for (int s0 = 0; s0 < p.num_splits; s0 += 4) {
+            float mm[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) mm[u] = s0 + u < p.num_splits ? __ldcg(&ml[(s0 + u) * stride + r]).x : -INFINITY;
+            M = fmaxf(M, fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])));
+          }
           float den = 0.f;
           float2 acc = make_float2(0.f, 0.f);
-          for (int s = 0; s < p.num_splits; ++s) {
-            const float2 t = __ldcg(&ml[s * stride + r]);
-            const float w = ex2_approx(t.x - M);
-            den += w * t.y;
-            const float2 ov = __ldcg(reinterpret_cast<const float2*>(p.part_o + (s * stride + r) * kHeadDim) + lane);
-            acc.x += w * ov.x;
-            acc.y += w * ov.y;
+          for (int s0 = 0; s0 < p.num_splits; s0 += 4) {
+            float2 t[4], ov[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const bool ok = s0 + u < p.num_splits;
+              const size_t sr = (size_t)(ok ? s0 + u : 0) * stride + r;
+              t[u] = ok ? __ldcg(&ml[sr]) : make_float2(-INFINITY, 0.f);
+              ov[u] = ok ? __ldcg(reinterpret_cast<const float2*>(p.part_o + sr * kHeadDim) + lane) : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float w = ex2_approx(t[u].x - M);
+              den += w * t[u].y;
+              acc.x += w * ov[u].x;
+              acc.y += w * ov[u].y;
+            }
           }
           const float inv = 1.f / den;
           const size_t off = (((size_t)b * p.n_q + grow) * p.H + h) * kHeadDim + 2 * lane;

@@ -29,6 +29,8 @@ constexpr int kTileM = 128;       // query rows per softmax warpgroup (UMMA M)
 constexpr int kTileN = 128;       // keys per tile (UMMA N of QK^T, K of PV)
 constexpr int kRowsPerCta = 256;  // two query tiles per CTA share each K/V tile
 
+constexpr int kFusedMergeMax = 16;  // key splits the in-kernel merge handles (more: merge_rows)
+
 struct FwdParams {
   int B, H, n_q, n_k;
   float scale_log2;        // scale * log2(e): exponent base change folded into one FFMA

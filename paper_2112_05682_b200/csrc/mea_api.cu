@@ -151,7 +151,7 @@ FwdPlan plan_fwd(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t q_chunk
       pl.tiles_per_split = (int)tps;
       if (q_chunk > 0) pl.q_window = std::min(n_q, (q_chunk + kRowsPerCta - 1) / kRowsPerCta * kRowsPerCta);
       pl.ws = (size_t)splits * B * H * pl.q_window * (d + 2) * sizeof(float);
-      if (d == kHeadDim) {  // + one arrival counter per (b, h, 256-row query block of a window)
+      if (d == kHeadDim && splits <= kFusedMergeMax) {  // + one arrival counter per (b, h, 256-row block)
         pl.cnt_off = (pl.ws + 15) / 16 * 16;
         pl.ws = pl.cnt_off + (size_t)B * H * ((pl.q_window + kRowsPerCta - 1) / kRowsPerCta) * sizeof(unsigned);
       }
@@ -331,7 +331,7 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
     const size_t rows = (size_t)pl.splits * B * H * pl.q_window;
     p.part_o = static_cast<float*>(workspace);
     p.part_ml = p.part_o + rows * d;
-    if (d == kHeadDim) {  // fused merge (last split CTA per query block); counters start at 0
+    if (pl.cnt_off > 0) {  // fused merge (last split CTA per query block); counters start at 0
       p.merge_cnt = reinterpret_cast<unsigned*>(static_cast<uint8_t*>(workspace) + pl.cnt_off);
       if ((e = cudaMemsetAsync(p.merge_cnt, 0, pl.ws - pl.cnt_off, st)) != cudaSuccess)
         return cuda_fail(e, "merge counter reset");

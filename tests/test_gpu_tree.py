@@ -61,7 +61,7 @@ def test_tree_equals_default_forward_and_workspace_is_small():
     ws_tree = api.mea_attention_fwd_tree_workspace_size(B, H, n, n, d, api.MEA_BF16, 1024, api.MEA_CHUNK_SQRT_N)
     ws_flat = api.mea_attention_fwd_workspace_size(B, H, n, n, d, api.MEA_BF16, 1024, api.MEA_CHUNK_SQRT_N)
     assert ws_tree == (7 + 2) * B * H * 1024 * (d + 2) * 4
-    assert ws_flat == 128 * B * H * 1024 * (d + 2) * 4 + B * H * 4 * 4   # + merge arrival counters
+    assert ws_flat == 128 * B * H * 1024 * (d + 2) * 4   # 128 splits: merged by merge_rows, no counters
     out = torch.empty_like(q)
     torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats()
