@@ -132,6 +132,19 @@ def oracle_sample(rows, n=N, d=D, seed=0, heads=1):
     return secs, 14 * rows * n * d * heads
 
 
+def arm_metric_config(workload, run_bwd, world, Bl, Hl, n):
+    """The metric string and config dict both arms report (the reference arm times the oracle
+    on a sample of this same workload)."""
+    wl = ("cfg3+cfg4: self-attention fwd+bwd (recompute from lse), B=1/GPU H=16 n=16384 d=64 bf16"
+          if workload == "cfg3" else "cfg5: self-attention fwd B=8 H=16 n=2^20 d=64 bf16, (b,h)-sharded")
+    metric = ("attention TFLOP/s (fwd 4*n^2*d + bwd 10*n^2*d per head)" if run_bwd
+              else "attention TFLOP/s (fwd 4*n^2*d per head)")
+    config = {"workload": wl, "B_per_gpu": Bl, "H": Hl, "n": n, "d": D, "global_batch": Bl * world,
+              "seq_len": n, "parallelism": f"dp{world} (batch x head sharding, no collective)",
+              "l2": "flushed before every timed step (512 MiB read, outside the events)"}
+    return metric, config
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -154,11 +167,13 @@ def run_reference(a):
     val = flops / (ms * 1e-3) / 1e12
     sample = (f"float64 oracle (naive fwd O1 + analytic bwd O6): 1 of {H} heads, {rows} of {N} query rows "
               f"vs all {N} keys, d={D}, per step")
-    line = {"impl": "reference", "metric": "attention TFLOP/s (fwd+bwd, 14*n^2*d per head)", "value": val,
-            "unit": "TFLOP/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+    world = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
+    metric, config = arm_metric_config("cfg3", True, world, 1, H, N)   # the mea arm's metric and config
+    line = {"impl": "reference", "metric": metric, "value": val,
+            "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (counter-based Irwin-Hall(12), N(0,1)-like, PAPER.md:231)",
-            "config": {"workload": "cfg3+cfg4 sample: self-attention fwd+bwd H=16 n=16384 d=64", "sample": sample},
+            "config": config,
             "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cpu_cores(), "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -510,17 +525,13 @@ def main():
                "seconds": secs}
 
     if rank == 0:
-        wl = ("cfg3+cfg4: self-attention fwd+bwd (recompute from lse), B=1/GPU H=16 n=16384 d=64 bf16"
-              if a.workload == "cfg3" else "cfg5: self-attention fwd B=8 H=16 n=2^20 d=64 bf16, (b,h)-sharded")
+        metric, config = arm_metric_config(a.workload, run_bwd, world, Bl, Hl, n)
         line = {
-            "metric": "attention TFLOP/s (fwd 4*n^2*d + bwd 10*n^2*d per head)" if run_bwd
-            else "attention TFLOP/s (fwd 4*n^2*d per head)",
+            "metric": metric,
             "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (counter-based Irwin-Hall(12), N(0,1)-like, PAPER.md:231)",
-            "config": {"workload": wl, "B_per_gpu": Bl, "H": Hl, "n": n, "d": D, "global_batch": Bl * world,
-                       "seq_len": n, "parallelism": f"dp{world} (batch x head sharding, no collective)",
-                       "l2": "flushed before every timed step (512 MiB read, outside the events)"},
+            "config": config,
             "clocks": clk, "gpu_launches": gpu_launches, "roofline": roofline, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "scratch": scratch, **extras,
             "paper_context": {"tpu_v3_fwd_ms_n16384_h1": 11.3, "tpu_v3_diff_ms_n16384_h1": 21.0,
