@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--fwd-only", action="store_true", help="time the forward pass alone as the step")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="only the headline step (e.g. for an ncu launch list whose shares match the step)")
     return ap.parse_args()
 
 
@@ -308,127 +310,128 @@ def main():
                 "per_launch_flops": dom_flops}
 
     extras = {}
-    # ---------------- forward alone, backward alone
-    fwd_ms = statistics.mean(timed(lambda: api.mea_attention_fwd(q, k, v, out=out, lse=lse), max(3, a.steps // 2), 1))
-    extras["fwd"] = {"ms": fwd_ms, "tflops": flop_fwd / (fwd_ms * 1e-3) / 1e12,
-                     "frac": flop_fwd / (fwd_ms * 1e-3) / 1e12 / pk["tflops"]}
-    if run_bwd:
-        bwd_ms = statistics.mean(timed(lambda: api.mea_attention_bwd(q, k, v, out, do, lse=lse, dq=dq, dk=dk, dv=dv,
-                                                                     workspace=bwd_ws), max(3, a.steps // 2), 1))
-        extras["bwd"] = {"ms": bwd_ms, "tflops": flop_bwd / (bwd_ms * 1e-3) / 1e12,
-                         "frac": flop_bwd / (bwd_ms * 1e-3) / 1e12 / pk["tflops"]}
-    # ---------------- causal masking: flops of the visible (i, j <= i) pairs only
-    if a.workload == "cfg3" and not a.fwd_only:
-        vis = n * (n + 1) / 2 * D * Hl * Bl
-        cf_ms = statistics.mean(timed(lambda: api.mea_attention_fwd_causal(q, k, v, out=out, lse=lse),
-                                      max(3, a.steps // 2), 1))
-        cb_ms = statistics.mean(timed(lambda: api.mea_attention_bwd_causal(q, k, v, out, do, lse=lse, dq=dq, dk=dk,
-                                                                           dv=dv, workspace=bwd_ws),
-                                      max(3, a.steps // 2), 1))
-        extras["causal"] = {"fwd_ms": cf_ms, "fwd_tflops": 4 * vis / (cf_ms * 1e-3) / 1e12,
-                            "bwd_ms": cb_ms, "bwd_tflops": 10 * vis / (cb_ms * 1e-3) / 1e12,
-                            "flops": "visible pairs only: 4 (fwd) / 10 (bwd) x n(n+1)/2 x d x H"}
-    # ---------------- head dimension 128: forward, configs[2]'s B, H, n
-    if a.workload == "cfg3":
-        q128 = torch.empty((Bl, n, Hl, 128), dtype=torch.bfloat16, device=dev)
-        k128, v128 = torch.empty_like(q128), torch.empty_like(q128)
-        for t, tid in ((q128, gen.TENSOR_Q), (k128, gen.TENSOR_K), (v128, gen.TENSOR_V)):
-            api.mea_fill_synthetic(t, a.seed, tid, offset=rank * q128.numel())
-        o128 = torch.empty_like(q128)
-        l128 = torch.empty((Bl, Hl, n), dtype=torch.float32, device=dev)
-        f128_ms = statistics.mean(timed(lambda: api.mea_attention_fwd(q128, k128, v128, out=o128, lse=l128),
-                                        max(3, a.steps // 2), 1))
-        fl128 = 4 * n * n * 128 * Hl * Bl
-        extras["fwd_d128"] = {"ms": f128_ms, "tflops": fl128 / (f128_ms * 1e-3) / 1e12,
-                              "frac": fl128 / (f128_ms * 1e-3) / 1e12 / pk["tflops"], "kernel": "fwd128_bf16"}
-        if not a.fwd_only:
-            do128 = torch.empty_like(q128)
-            api.mea_fill_synthetic(do128, a.seed, gen.TENSOR_DO, offset=rank * do128.numel())
-            g128 = [torch.empty_like(q128) for _ in range(3)]
-            ws128 = torch.empty(api.mea_attention_bwd_workspace_size(Bl, Hl, n, n, 128, api.MEA_BF16, True),
-                                dtype=torch.uint8, device=dev)
-            b128_ms = statistics.mean(timed(lambda: api.mea_attention_bwd(
-                q128, k128, v128, o128, do128, lse=l128, dq=g128[0], dk=g128[1], dv=g128[2], workspace=ws128),
-                max(3, a.steps // 2), 1))
-            extras["bwd_d128"] = {"ms": b128_ms, "tflops": 2.5 * fl128 / (b128_ms * 1e-3) / 1e12,
-                                  "frac": 2.5 * fl128 / (b128_ms * 1e-3) / 1e12 / pk["tflops"],
-                                  "kernels": "bwd_dkdv<128> (64-query tiles) + bwd_dq<128>"}
-            del do128, g128, ws128
-        del q128, k128, v128, o128, l128
-    # ---------------- the paper's literal schedule (query chunk 1024 / key chunk 4096)
-    if a.workload == "cfg3":
-        ws_kc = api.mea_attention_fwd_workspace_size(Bl, Hl, n, n, D, api.MEA_BF16, 1024, 4096)
-        wsb = torch.empty(ws_kc, dtype=torch.uint8, device=dev)
-        kc_ms = statistics.mean(timed(lambda: api.mea_attention_fwd(q, k, v, out=out, lse=lse, q_chunk=1024,
-                                                                    k_chunk=4096, workspace=wsb), 3, 1))
-        extras["fwd_paper_chunks_qc1024_kc4096"] = {"ms": kc_ms, "tflops": flop_fwd / (kc_ms * 1e-3) / 1e12,
-                                                    "scratch_bytes": ws_kc}
-        del wsb
-    # ---------------- single query (configs[1]): HBM-bound split-K + merge
-    if a.workload == "cfg3":
-        sq_q = torch.empty((1, 1, D), dtype=torch.bfloat16, device=dev)
-        sq_k = torch.empty((1, SQ_NK, 1, D), dtype=torch.bfloat16, device=dev)
-        sq_v = torch.empty_like(sq_k)
-        for t, tid in ((sq_q, gen.TENSOR_Q), (sq_k, gen.TENSOR_K), (sq_v, gen.TENSOR_V)):
-            api.mea_fill_synthetic(t, a.seed, tid)
-        sq_o = torch.empty((1, 1, D), dtype=torch.bfloat16, device=dev)
-        sq_ws = torch.empty(api.mea_single_query_workspace_size(1, 1, SQ_NK, D, api.MEA_BF16), dtype=torch.uint8,
-                            device=dev)
-        sq_ts = timed(lambda: api.mea_single_query_fwd(sq_q, sq_k, sq_v, out=sq_o, workspace=sq_ws), a.steps, 2)
-        call_ms = statistics.median(sq_ts)       # both kernels (the merge overlaps via PDL)
-        api.profile_enable(True)
-        api.profile_read()
-        timed(lambda: api.mea_single_query_fwd(sq_q, sq_k, sq_v, out=sq_o, workspace=sq_ws), a.steps, 2)
-        sp = api.profile_read()
-        api.profile_enable(False)
-        part_ms = sp["sq_partial"][1] / sp["sq_partial"][0]
-        sq_bytes = 2 * SQ_NK * D * 2 + D * 2 * 2
-        extras["single_query_cfg2"] = {
-            "n_k": SQ_NK, "call_us": call_ms * 1e3, "partial_us": part_ms * 1e3,
-            "gbs_call": sq_bytes / (call_ms * 1e-3) / 1e9, "gbs_partial": sq_bytes / (part_ms * 1e-3) / 1e9,
-            "frac_hbm_call": sq_bytes / (call_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
-            "frac_hbm_partial": sq_bytes / (part_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
-            "peak_gbs": pk["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json copy (read + write)",
-            "scratch_bytes": sq_ws.numel()}
-        del sq_k, sq_v
-    # ---------------- key-range sharded single query across ranks (NCCL all-gather + merge)
-    if distributed and a.workload == "cfg3":
-        from paper_2112_05682_b200 import dist as mdist
-        Bq, Hq = 1, 16          # a decode-shaped batch of 16 heads, 2^20 keys per rank (weak)
-        n_local = SQ_NK
-        sq_q = torch.empty((Bq, Hq, D), dtype=torch.bfloat16, device=dev)
-        sq_k = torch.empty((Bq, n_local, Hq, D), dtype=torch.bfloat16, device=dev)
-        sq_v = torch.empty_like(sq_k)
-        api.mea_fill_synthetic(sq_q, a.seed, gen.TENSOR_Q)
-        api.mea_fill_synthetic(sq_k, a.seed, gen.TENSOR_K, offset=rank * sq_k.numel())
-        api.mea_fill_synthetic(sq_v, a.seed, gen.TENSOR_V, offset=rank * sq_v.numel())
-        run = lambda: mdist.sharded_single_query(sq_q, sq_k, sq_v)
-        t = timed(run, max(5, a.steps // 3), 2)
-        sh_ms = max_over_ranks(statistics.mean(t))
-        gb = world * 2 * n_local * Hq * D * 2 / 1e9
-        extras["single_query_key_sharded"] = {
-            "keys_total": n_local * world, "heads": Hq, "ms": sh_ms, "gbs_total": gb / (sh_ms * 1e-3),
-            "collective": "one all_gather of (m*, s*, v*) per (b,h), NCCL"}
-        del sq_k, sq_v
-        # key-range sharded self-attention (long context beyond one GPU): every rank holds all
-        # query rows and n/world of the keys of configs[2]'s shape; row triples, one all-gather,
-        # merge on every rank (strong scaling in the keys)
-        lo, hi = mdist.shard_range(n, world, rank)
-        q_all = torch.empty_like(q)                 # the same query rows on every rank (batch element 0)
-        api.mea_fill_synthetic(q_all, a.seed, gen.TENSOR_Q)
-        k_loc = torch.empty((Bl, hi - lo, Hl, D), dtype=torch.bfloat16, device=dev)
-        v_loc = torch.empty_like(k_loc)             # this rank's key range of batch element 0
-        api.mea_fill_synthetic(k_loc, a.seed, gen.TENSOR_K, offset=lo * Hl * D)
-        api.mea_fill_synthetic(v_loc, a.seed, gen.TENSOR_V, offset=lo * Hl * D)
-        run = lambda: mdist.sharded_self_attention(q_all, k_loc, v_loc)
-        t = timed(run, max(3, a.steps // 3), 1)
-        sa_ms = max_over_ranks(statistics.mean(t))
-        extras["self_attention_key_sharded"] = {
-            "n": n, "heads": Hl, "keys_per_rank": hi - lo, "ms": sa_ms,
-            "tflops_total": flop_fwd / (sa_ms * 1e-3) / 1e12,
-            "exchange_bytes_per_rank": Bl * n * Hl * (D + 2) * 4,
-            "collective": "one all_gather of the per-row (m*, s*, v*) triples, NCCL; merge on every rank"}
-        del q_all, k_loc, v_loc
+    if not a.no_extras:
+        # ---------------- forward alone, backward alone
+        fwd_ms = statistics.mean(timed(lambda: api.mea_attention_fwd(q, k, v, out=out, lse=lse), max(3, a.steps // 2), 1))
+        extras["fwd"] = {"ms": fwd_ms, "tflops": flop_fwd / (fwd_ms * 1e-3) / 1e12,
+                         "frac": flop_fwd / (fwd_ms * 1e-3) / 1e12 / pk["tflops"]}
+        if run_bwd:
+            bwd_ms = statistics.mean(timed(lambda: api.mea_attention_bwd(q, k, v, out, do, lse=lse, dq=dq, dk=dk, dv=dv,
+                                                                         workspace=bwd_ws), max(3, a.steps // 2), 1))
+            extras["bwd"] = {"ms": bwd_ms, "tflops": flop_bwd / (bwd_ms * 1e-3) / 1e12,
+                             "frac": flop_bwd / (bwd_ms * 1e-3) / 1e12 / pk["tflops"]}
+        # ---------------- causal masking: flops of the visible (i, j <= i) pairs only
+        if a.workload == "cfg3" and not a.fwd_only:
+            vis = n * (n + 1) / 2 * D * Hl * Bl
+            cf_ms = statistics.mean(timed(lambda: api.mea_attention_fwd_causal(q, k, v, out=out, lse=lse),
+                                          max(3, a.steps // 2), 1))
+            cb_ms = statistics.mean(timed(lambda: api.mea_attention_bwd_causal(q, k, v, out, do, lse=lse, dq=dq, dk=dk,
+                                                                               dv=dv, workspace=bwd_ws),
+                                          max(3, a.steps // 2), 1))
+            extras["causal"] = {"fwd_ms": cf_ms, "fwd_tflops": 4 * vis / (cf_ms * 1e-3) / 1e12,
+                                "bwd_ms": cb_ms, "bwd_tflops": 10 * vis / (cb_ms * 1e-3) / 1e12,
+                                "flops": "visible pairs only: 4 (fwd) / 10 (bwd) x n(n+1)/2 x d x H"}
+        # ---------------- head dimension 128: forward, configs[2]'s B, H, n
+        if a.workload == "cfg3":
+            q128 = torch.empty((Bl, n, Hl, 128), dtype=torch.bfloat16, device=dev)
+            k128, v128 = torch.empty_like(q128), torch.empty_like(q128)
+            for t, tid in ((q128, gen.TENSOR_Q), (k128, gen.TENSOR_K), (v128, gen.TENSOR_V)):
+                api.mea_fill_synthetic(t, a.seed, tid, offset=rank * q128.numel())
+            o128 = torch.empty_like(q128)
+            l128 = torch.empty((Bl, Hl, n), dtype=torch.float32, device=dev)
+            f128_ms = statistics.mean(timed(lambda: api.mea_attention_fwd(q128, k128, v128, out=o128, lse=l128),
+                                            max(3, a.steps // 2), 1))
+            fl128 = 4 * n * n * 128 * Hl * Bl
+            extras["fwd_d128"] = {"ms": f128_ms, "tflops": fl128 / (f128_ms * 1e-3) / 1e12,
+                                  "frac": fl128 / (f128_ms * 1e-3) / 1e12 / pk["tflops"], "kernel": "fwd128_bf16"}
+            if not a.fwd_only:
+                do128 = torch.empty_like(q128)
+                api.mea_fill_synthetic(do128, a.seed, gen.TENSOR_DO, offset=rank * do128.numel())
+                g128 = [torch.empty_like(q128) for _ in range(3)]
+                ws128 = torch.empty(api.mea_attention_bwd_workspace_size(Bl, Hl, n, n, 128, api.MEA_BF16, True),
+                                    dtype=torch.uint8, device=dev)
+                b128_ms = statistics.mean(timed(lambda: api.mea_attention_bwd(
+                    q128, k128, v128, o128, do128, lse=l128, dq=g128[0], dk=g128[1], dv=g128[2], workspace=ws128),
+                    max(3, a.steps // 2), 1))
+                extras["bwd_d128"] = {"ms": b128_ms, "tflops": 2.5 * fl128 / (b128_ms * 1e-3) / 1e12,
+                                      "frac": 2.5 * fl128 / (b128_ms * 1e-3) / 1e12 / pk["tflops"],
+                                      "kernels": "bwd_dkdv<128> (64-query tiles) + bwd_dq<128>"}
+                del do128, g128, ws128
+            del q128, k128, v128, o128, l128
+        # ---------------- the paper's literal schedule (query chunk 1024 / key chunk 4096)
+        if a.workload == "cfg3":
+            ws_kc = api.mea_attention_fwd_workspace_size(Bl, Hl, n, n, D, api.MEA_BF16, 1024, 4096)
+            wsb = torch.empty(ws_kc, dtype=torch.uint8, device=dev)
+            kc_ms = statistics.mean(timed(lambda: api.mea_attention_fwd(q, k, v, out=out, lse=lse, q_chunk=1024,
+                                                                        k_chunk=4096, workspace=wsb), 3, 1))
+            extras["fwd_paper_chunks_qc1024_kc4096"] = {"ms": kc_ms, "tflops": flop_fwd / (kc_ms * 1e-3) / 1e12,
+                                                        "scratch_bytes": ws_kc}
+            del wsb
+        # ---------------- single query (configs[1]): HBM-bound split-K + merge
+        if a.workload == "cfg3":
+            sq_q = torch.empty((1, 1, D), dtype=torch.bfloat16, device=dev)
+            sq_k = torch.empty((1, SQ_NK, 1, D), dtype=torch.bfloat16, device=dev)
+            sq_v = torch.empty_like(sq_k)
+            for t, tid in ((sq_q, gen.TENSOR_Q), (sq_k, gen.TENSOR_K), (sq_v, gen.TENSOR_V)):
+                api.mea_fill_synthetic(t, a.seed, tid)
+            sq_o = torch.empty((1, 1, D), dtype=torch.bfloat16, device=dev)
+            sq_ws = torch.empty(api.mea_single_query_workspace_size(1, 1, SQ_NK, D, api.MEA_BF16), dtype=torch.uint8,
+                                device=dev)
+            sq_ts = timed(lambda: api.mea_single_query_fwd(sq_q, sq_k, sq_v, out=sq_o, workspace=sq_ws), a.steps, 2)
+            call_ms = statistics.median(sq_ts)       # both kernels (the merge overlaps via PDL)
+            api.profile_enable(True)
+            api.profile_read()
+            timed(lambda: api.mea_single_query_fwd(sq_q, sq_k, sq_v, out=sq_o, workspace=sq_ws), a.steps, 2)
+            sp = api.profile_read()
+            api.profile_enable(False)
+            part_ms = sp["sq_partial"][1] / sp["sq_partial"][0]
+            sq_bytes = 2 * SQ_NK * D * 2 + D * 2 * 2
+            extras["single_query_cfg2"] = {
+                "n_k": SQ_NK, "call_us": call_ms * 1e3, "partial_us": part_ms * 1e3,
+                "gbs_call": sq_bytes / (call_ms * 1e-3) / 1e9, "gbs_partial": sq_bytes / (part_ms * 1e-3) / 1e9,
+                "frac_hbm_call": sq_bytes / (call_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                "frac_hbm_partial": sq_bytes / (part_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                "peak_gbs": pk["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json copy (read + write)",
+                "scratch_bytes": sq_ws.numel()}
+            del sq_k, sq_v
+        # ---------------- key-range sharded single query across ranks (NCCL all-gather + merge)
+        if distributed and a.workload == "cfg3":
+            from paper_2112_05682_b200 import dist as mdist
+            Bq, Hq = 1, 16          # a decode-shaped batch of 16 heads, 2^20 keys per rank (weak)
+            n_local = SQ_NK
+            sq_q = torch.empty((Bq, Hq, D), dtype=torch.bfloat16, device=dev)
+            sq_k = torch.empty((Bq, n_local, Hq, D), dtype=torch.bfloat16, device=dev)
+            sq_v = torch.empty_like(sq_k)
+            api.mea_fill_synthetic(sq_q, a.seed, gen.TENSOR_Q)
+            api.mea_fill_synthetic(sq_k, a.seed, gen.TENSOR_K, offset=rank * sq_k.numel())
+            api.mea_fill_synthetic(sq_v, a.seed, gen.TENSOR_V, offset=rank * sq_v.numel())
+            run = lambda: mdist.sharded_single_query(sq_q, sq_k, sq_v)
+            t = timed(run, max(5, a.steps // 3), 2)
+            sh_ms = max_over_ranks(statistics.mean(t))
+            gb = world * 2 * n_local * Hq * D * 2 / 1e9
+            extras["single_query_key_sharded"] = {
+                "keys_total": n_local * world, "heads": Hq, "ms": sh_ms, "gbs_total": gb / (sh_ms * 1e-3),
+                "collective": "one all_gather of (m*, s*, v*) per (b,h), NCCL"}
+            del sq_k, sq_v
+            # key-range sharded self-attention (long context beyond one GPU): every rank holds all
+            # query rows and n/world of the keys of configs[2]'s shape; row triples, one all-gather,
+            # merge on every rank (strong scaling in the keys)
+            lo, hi = mdist.shard_range(n, world, rank)
+            q_all = torch.empty_like(q)                 # the same query rows on every rank (batch element 0)
+            api.mea_fill_synthetic(q_all, a.seed, gen.TENSOR_Q)
+            k_loc = torch.empty((Bl, hi - lo, Hl, D), dtype=torch.bfloat16, device=dev)
+            v_loc = torch.empty_like(k_loc)             # this rank's key range of batch element 0
+            api.mea_fill_synthetic(k_loc, a.seed, gen.TENSOR_K, offset=lo * Hl * D)
+            api.mea_fill_synthetic(v_loc, a.seed, gen.TENSOR_V, offset=lo * Hl * D)
+            run = lambda: mdist.sharded_self_attention(q_all, k_loc, v_loc)
+            t = timed(run, max(3, a.steps // 3), 1)
+            sa_ms = max_over_ranks(statistics.mean(t))
+            extras["self_attention_key_sharded"] = {
+                "n": n, "heads": Hl, "keys_per_rank": hi - lo, "ms": sa_ms,
+                "tflops_total": flop_fwd / (sa_ms * 1e-3) / 1e12,
+                "exchange_bytes_per_rank": Bl * n * Hl * (D + 2) * 4,
+                "collective": "one all_gather of the per-row (m*, s*, v*) triples, NCCL; merge on every rank"}
+            del q_all, k_loc, v_loc
     # ---------------- scratch bytes vs the paper's accounting (standard attention: n^2*4 B/head)
     scratch = {"fwd_workspace_bytes": 0, "fwd_lse_residual_bytes": lse.numel() * 4,
                "bwd_workspace_bytes": bwd_ws.numel() if bwd_ws is not None else None,

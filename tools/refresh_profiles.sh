@@ -8,6 +8,7 @@ timeout 600 python bench.py > gpurun_out/bench_r01.json 2> gpurun_out/bench_r01.
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 1 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_torchrun.json 2> gpurun_out/bench_torchrun.err; echo "torchrun $?"
 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/plain_launch.log 2>&1; echo "plain $?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_r01.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1; echo "ncu launch $?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_step_r01.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-extras > gpurun_out/ncu_step.log 2>&1; echo "ncu step $?"
 for w in fwd bwd sq fwd128; do
   timeout 300 python tools/prof_kernel.py $w > gpurun_out/plain_$w.log 2>&1; echo "plain $w $?"
 done
