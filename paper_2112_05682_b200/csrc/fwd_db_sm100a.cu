@@ -177,10 +177,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #else
 #define IPROBE(k)
 #endif
-      // The issuer's waits poll (mbarrier.test_wait) instead of suspending: it resumes as soon as
-      // the last softmax warp has stored P_t (-2 % kernel time vs try_wait, measured).
+      // The issuer's waits poll (mbarrier.test_wait) up to 32 times before suspending: it resumes
+      // as soon as the last softmax warp has stored P_t, without burning issue slots and power on
+      // long waits (vs try_wait: -2 % at full clocks; vs pure polling: -0.7 % at full clocks and
+      // -1 % under the sustained power cap, measured).
       for (int t = 0; t < Tq; ++t) {
-        mbar_spin(&sm.p_full[qt], t & 1);
+        mbar_poll_wait<32>(&sm.p_full[qt], t & 1);
         IPROBE(0)
         tc_fence_after();
         if (elect_one()) {
@@ -193,8 +195,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         IPROBE(1)
         if (t + 2 < Tq) {
           // S_{t+2} goes into the buffer P_t occupies: wait until PV_t has read it
-          mbar_spin(&sm.kv_full[(t + 2) % kStages], ((t + 2) / kStages) & 1);
-          mbar_spin(&sm.pv_done[qt], t & 1);
+          mbar_poll_wait<32>(&sm.kv_full[(t + 2) % kStages], ((t + 2) / kStages) & 1);
+          mbar_poll_wait<32>(&sm.pv_done[qt], t & 1);
           IPROBE(2)
           tc_fence_after();
           if (elect_one()) qk(t + 2);

@@ -57,6 +57,16 @@ __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
   while (!mbar_test_wait(bar, parity)) {
   }
 }
+// Poll a bounded number of times (resume at once if the phase completes soon), then suspend in
+// try_wait (no issue slots or power burnt on a long wait).
+template <int kPolls>
+__device__ __forceinline__ void mbar_poll_wait(uint64_t* bar, uint32_t parity) {
+#pragma unroll  // an unrolled poll sequence (a rolled loop measured +2.6 % in fwd_db)
+  for (int i = 0; i < kPolls; ++i)
+    if (mbar_test_wait(bar, parity)) return;
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
 #ifdef MEA_DEBUG_HANG
 // Diagnostic build only: a wait that never completes is counted (by barrier smem offset)
 // and abandoned, so a deadlock shows up as counts instead of a hung GPU.
