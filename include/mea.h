@@ -187,9 +187,12 @@ MEA_API mea_status_t mea_single_query_workspace_size(int64_t B, int64_t H, int64
  * Multi-GPU building blocks for attention sharded over key ranges (MNNFast-style KV
  * sharding; merge = PAPER.md:140-147).
  * mea_single_query_partial writes, per (b,h), the stream state over this call's keys:
- *   m [B*H]      : reference max (natural-log units of the scaled score; any value
- *                  >= the true max minus 8*ln2 — all terms are relative to it),
- *   s [B*H]      : s* = sum_j e^{s_j - m},
+ *   m [B*H]      : reference max (natural-log units of the scaled score), an observed
+ *                  score, so m <= the true max; the lazily updated reference of the
+ *                  tensor-core kernels may lag it by up to 64*ln2 (every term e^{s_j - m}
+ *                  is certified < 2^64, reading 9; the single-query kernel
+ *                  keeps the exact blocked max). All terms are relative to m,
+ *   s [B*H]      : s* = sum_j e^{s_j - m}  (so 1 <= s* < n_k * 2^64 for n_k >= 1),
  *   vstar [B*H*d]: v* = sum_j v_j e^{s_j - m}   (all float32).
  * n_k == 0 is allowed here and yields the empty triple (-inf, 0, 0).
  * mea_merge_partials combines P stacked triples m [P,B*H], s [P,B*H], vstar [P,B*H,d]

@@ -64,6 +64,24 @@ def _cuda_contig(*ts):
             raise ValueError("tensors must be contiguous")
 
 
+def _expect(t, shape, dtype, name):
+    """Caller-supplied tensors are read by the kernels with the dtype / shape the call implies:
+    reject anything else instead of reinterpreting bytes or writing out of bounds."""
+    if t is None:
+        return
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+
+
+def _expect_out(out, shape):
+    if out is not None:
+        if out.dtype not in (torch.bfloat16, torch.float32):
+            raise TypeError(f"out must be bfloat16 or float32, got {out.dtype}")
+        _expect(out, shape, None, "out")
+
+
 def _workspace(nbytes, device):
     if nbytes == 0:
         return None
@@ -106,6 +124,8 @@ def mea_attention_fwd_tree(q, k, v, scale=None, out=None, out_dtype=None, lse=No
     if k.dtype != q.dtype or v.dtype != q.dtype:
         raise TypeError("q, k, v must share a dtype")
     dt = _dtype(q)
+    _expect_out(out, (B, n_q, H, d))
+    _expect(lse, (B, H, n_q), torch.float32, "lse")
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     if out is None:
         out = torch.empty((B, n_q, H, d), dtype=q.dtype if out_dtype is None else out_dtype, device=q.device)
@@ -136,6 +156,8 @@ def mea_attention_fwd(q, k, v, scale=None, out=None, out_dtype=None, lse=None, w
         dt = MEA_F32_SPLIT
     if k.dtype != q.dtype or v.dtype != q.dtype:
         raise TypeError("q, k, v must share a dtype")
+    _expect_out(out, (B, n_q, H, d))
+    _expect(lse, (B, H, n_q), torch.float32, "lse")
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     if out is None:
         od = q.dtype if out_dtype is None else out_dtype
@@ -156,6 +178,10 @@ def mea_attention_fwd_causal(q, k, v, scale=None, out=None, out_dtype=None, lse=
     B, n, H, d = q.shape
     if k.shape != q.shape or v.shape != q.shape:
         raise ValueError(f"causal attention needs q, k, v of one shape, got {tuple(q.shape)} {tuple(k.shape)}")
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        raise TypeError("q, k, v must share a dtype")
+    _expect_out(out, (B, n, H, d))
+    _expect(lse, (B, H, n), torch.float32, "lse")
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     if out is None:
         out = torch.empty((B, n, H, d), dtype=q.dtype if out_dtype is None else out_dtype, device=q.device)
@@ -175,6 +201,8 @@ def mea_attention_partial_fwd(q, k, v, scale=None):
     n_k = k.shape[1]
     if k.shape != (B, n_k, H, d) or v.shape != k.shape:
         raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        raise TypeError("q, k, v must share a dtype")
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     m = torch.empty((B, n_q, H), dtype=torch.float32, device=q.device)
     s = torch.empty((B, n_q, H), dtype=torch.float32, device=q.device)
@@ -197,8 +225,11 @@ def mea_single_query_fwd(q, k, v, scale=None, out=None, out_dtype=None, workspac
     B, H, d = q.shape
     n_k = k.shape[1]
     if k.shape != (B, n_k, H, d) or v.shape != k.shape:
-        raise ValueError("shape mismatch")
+        raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        raise TypeError("q, k, v must share a dtype")
     dt = _dtype(q)
+    _expect_out(out, (B, H, d))
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     if out is None:
         out = torch.empty((B, H, d), dtype=q.dtype if out_dtype is None else out_dtype, device=q.device)
@@ -215,6 +246,10 @@ def mea_single_query_partial(q, k, v, scale=None, workspace=None):
     _cuda_contig(q, k, v)
     B, H, d = q.shape
     n_k = k.shape[1]
+    if k.shape != (B, n_k, H, d) or v.shape != k.shape:
+        raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        raise TypeError("q, k, v must share a dtype")
     dt = _dtype(q)
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     m = torch.empty(B * H, dtype=torch.float32, device=q.device)
@@ -233,6 +268,10 @@ def mea_merge_partials(m, s, vstar, B, H, out_dtype=torch.bfloat16, out=None):
     _cuda_contig(m, s, vstar, out)
     P = m.shape[0]
     d = vstar.shape[-1]
+    _expect(m, (P, B * H), torch.float32, "m")
+    _expect(s, (P, B * H), torch.float32, "s")
+    _expect(vstar, (P, B * H, d), torch.float32, "vstar")
+    _expect_out(out, (B, H, d))
     if out is None:
         out = torch.empty((B, H, d), dtype=out_dtype, device=m.device)
     _check(_lib.load().mea_merge_partials(_ptr(m), _ptr(s), _ptr(vstar), P, B, H, d, _ptr(out), _dtype(out),
@@ -260,6 +299,13 @@ def _bwd(fn, ws_fn, q, k, v, out, dout, lse, scale, dq, dk, dv, workspace):
     B, n_q, H, d = q.shape
     n_k = k.shape[1]
     dt = _dtype(q)
+    # every tensor is read / written as q's dtype and the shapes below (an fp32 `out` from the
+    # paper's fp32-output forward must be cast by the caller, it is not reinterpreted)
+    for t, shape, nm in ((k, (B, n_k, H, d), "k"), (v, (B, n_k, H, d), "v"), (out, (B, n_q, H, d), "out"),
+                         (dout, (B, n_q, H, d), "dout"), (dq, (B, n_q, H, d), "dq"), (dk, (B, n_k, H, d), "dk"),
+                         (dv, (B, n_k, H, d), "dv")):
+        _expect(t, shape, q.dtype, nm)
+    _expect(lse, (B, H, n_q), torch.float32, "lse")
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     dq = torch.empty_like(q) if dq is None else dq
     dk = torch.empty_like(k) if dk is None else dk
@@ -304,6 +350,10 @@ def mea_attention_fwd_padded(q, k, v, kv_lens, scale=None, out=None, out_dtype=N
     if k.shape != (B, n_k, H, d) or v.shape != k.shape:
         raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
     kv_lens = _kv_lens_dev(kv_lens, q)
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        raise TypeError("q, k, v must share a dtype")
+    _expect_out(out, (B, n_q, H, d))
+    _expect(lse, (B, H, n_q), torch.float32, "lse")
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     if out is None:
         out = torch.empty((B, n_q, H, d), dtype=q.dtype if out_dtype is None else out_dtype, device=q.device)

@@ -300,6 +300,9 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
 
   // the plain d = 64 forward (online over all keys, no mask) runs the double-buffered kernel
   const bool use_db = MEA_FWD_DB && d == kHeadDim && pl.splits == 1;
+  // key padding is implemented by fwd_db (d = 64) and fwd128 only: never silently drop the mask
+  if (kv_lens && d == kHeadDim && !use_db)
+    return fail(MEA_ERR_UNSUPPORTED, "key padding needs the online d = 64 forward (no key split; MEA_FWD_DB build)");
   const int key_box = use_db ? fwd_db_key_tile() : kTileN;
   CUtensorMap mq, mk, mv;
   const char* why = "";

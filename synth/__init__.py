@@ -3,7 +3,7 @@
 This package holds NO attention arithmetic. It only produces input tensors from
 (seed, tensor_id, flat index) with a counter-based generator (see ``gen.py``).
 The CUDA library implements the same generator independently
-(``paper_2112_05682_b200/csrc/gen_inputs.cu``); ``tests/test_gpu_generator.py``
+(``paper_2112_05682_b200/csrc/gen_inputs.cu``); ``tests/test_gpu_probe.py::test_device_generator_bit_identical``
 checks the two are bit-identical.
 """
 from .gen import (  # noqa: F401

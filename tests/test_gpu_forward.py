@@ -108,9 +108,16 @@ def test_bf16_identical_keys_and_single_key():
     q, k, v = Hh.host_inputs(1, 130, 300, 1, 64, seed=6)
     k[:] = k[:, :1]
     got, _ = _run(q, k, v)
-    Hh.assert_close_bf16(got, np.broadcast_to(v.mean(axis=1, keepdims=True), got.shape))
-    got1, _ = _run(q, k[:, :1], v[:, :1])
-    assert np.abs(got1 - np.broadcast_to(v[:, :1], got1.shape)).max() < 1e-2
+    mean = np.broadcast_to(v.mean(axis=1, keepdims=True), got.shape)
+    Hh.assert_close_bf16(got, mean)
+    # every weight is exactly 1 (P rounds to 1.0 in bf16), so with an fp32 output the only error
+    # is the fp32 sum of 300 values and one division: far below the bf16 bar
+    got32, _ = _run(q, k, v, out_dtype=torch.float32)
+    assert np.abs(got32 - mean).max() <= 1e-5 + 1e-5 * np.abs(mean).max()
+    # n_k = 1: the weight is exactly 1, so out = v_1 bit for bit, in either output dtype
+    for od in (torch.bfloat16, torch.float32):
+        got1, _ = _run(q, k[:, :1], v[:, :1], out_dtype=od)
+        np.testing.assert_array_equal(got1, np.broadcast_to(v[:, :1], got1.shape))
 
 
 def test_f32_config1_parity():

@@ -88,6 +88,7 @@ def test_forward_and_backward_random_case(i):
             rq, rk, rv = O.mha_backward(q[b:b + 1], k[b:b + 1, :L], v[b:b + 1, :L], do[b:b + 1], scale, causal=causal)
             for g, r, nm in ((dq[b:b + 1], rq, "dq"), (dk[b:b + 1, :L], rk, "dk"), (dv[b:b + 1, :L], rv, "dv")):
                 Hh.assert_close_bf16(g, r, abs_tol=gtol if nm != "dv" else Hh.TOL_BF16_GRAD, rel_tol=Hh.REL_NORM_GRAD,
+                                     strict=nm == "dv" or gtol == Hh.TOL_BF16_GRAD,
                                      what=f"case {i} {nm}")
             if L < n_k:
                 assert (dk[b, L:] == 0).all() and (dv[b, L:] == 0).all()
@@ -141,7 +142,8 @@ def test_other_entry_points_random_case(i):
         torch.cuda.synchronize()
         gtol = Hh.TOL_BF16_GRAD * max(1.0, abs(scale) * math.sqrt(d))
         for x, ref, nm in zip(g, O.mha_backward(q, k, v, do, scale), ("dq", "dk", "dv")):
-            Hh.assert_close_bf16(x.double().cpu().numpy(), ref, abs_tol=gtol, rel_tol=Hh.REL_NORM_GRAD, what=nm)
+            Hh.assert_close_bf16(x.double().cpu().numpy(), ref, abs_tol=gtol, rel_tol=Hh.REL_NORM_GRAD, what=nm,
+                                 strict=nm == "dv" or gtol == Hh.TOL_BF16_GRAD)
     else:
         n_q, n_k = min(n_q, 200), min(n_k, 600)
         split = d == 64 and bool(r.integers(0, 2))

@@ -107,4 +107,31 @@ def test_config2_single_query_full():
     kh = gen.normal_tensor((1, n_k, 1, 64), 0, gen.TENSOR_K, "bf16").astype(np.float64)
     vh = gen.normal_tensor((1, n_k, 1, 64), 0, gen.TENSOR_V, "bf16").astype(np.float64)
     ref = O.naive(qh[0], kh[0, :, 0], vh[0, :, 0], 0.125)[0]
-    Hh.assert_close_bf16(out[0].double().cpu().numpy(), ref, abs_tol=2e-2, rel_tol=2e-2)
+    got = out[0].double().cpu().numpy()
+    # bf16 inputs are exact in both; the path accumulates in fp32 and writes fp32, so the bar is
+    # fp32-appropriate (output std ~1.6e-3 at 2^20 keys: an absolute 2e-2 would be ~12 sigma)
+    err = np.abs(got - ref)
+    assert (err <= 1e-3 * np.abs(ref) + 1e-6).all(), f"max abs err {err.max():.3e}"
+    assert Hh.rel_norm(got, ref) <= 1e-4
+
+
+@pytest.mark.parametrize("n_k", [1, 3, 1000, 70001])
+def test_single_query_exact_cases(n_k):
+    """n_k = 1 returns v_1 bit for bit; identical keys return the mean of the values
+     to fp32 summation accuracy."""
+    from paper_2112_05682_b200 import api
+    B, H, d = 2, 3, 64
+    q, k, v = _sq_inputs(B, H, n_k, d, seed=7)
+    k[:] = k[:, :1]
+    qd, kd, vd = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v))
+    for od in (torch.float32, torch.bfloat16):
+        out = api.mea_single_query_fwd(qd, kd, vd, out_dtype=od)
+        torch.cuda.synchronize()
+        got = out.double().cpu().numpy()
+        mean = v.mean(axis=1)
+        if n_k == 1:
+            np.testing.assert_array_equal(got, mean)
+        elif od == torch.float32:
+            assert np.abs(got - mean).max() <= 1e-6 + 1e-5 * np.abs(mean).max()
+        else:
+            Hh.assert_close_bf16(got, mean)

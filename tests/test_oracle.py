@@ -326,3 +326,51 @@ def test_causal_backward_matches_fd_and_autograd(rng):
     np.testing.assert_allclose(sq, an[0][qr], atol=1e-12)
     np.testing.assert_allclose(sk, an[1][kr], atol=1e-12)
     np.testing.assert_allclose(sv, an[2][kr], atol=1e-12)
+
+
+# ---------------------------------------------------------------- P8 on the library layout
+def _autograd_mha(q, k, v, do, scale, causal):
+    """torch float64 autograd of softmax attention on [B, n, H, d] (an independent library path:
+    einsum over the head axis, no per-(b,h) slicing)."""
+    tq, tk, tv = (torch.tensor(x, requires_grad=True) for x in (q, k, v))
+    s = scale * torch.einsum("bqhd,bkhd->bhqk", tq, tk)
+    if causal:
+        n_q, n_k = q.shape[1], k.shape[1]
+        s = s.masked_fill(torch.triu(torch.ones(n_q, n_k, dtype=torch.bool), 1), float("-inf"))
+    out = torch.einsum("bhqk,bkhd->bqhd", torch.softmax(s, dim=-1), tv)
+    out.backward(torch.from_numpy(do))
+    return out.detach().numpy(), tq.grad.numpy(), tk.grad.numpy(), tv.grad.numpy()
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("n_q,n_k", [(7, 11), (9, 9)])
+def test_mha_backward_matches_autograd_on_library_layout(rng, causal, n_q, n_k):
+    """mha_backward (the reference of every GPU backward parity test) on [B, n, H, d] with B, H > 1
+    against torch autograd: a swapped dk/dv, a wrong [b, :, h] slice or a
+    transposed head/batch index fails here."""
+    if causal and n_q != n_k:
+        pytest.skip("causal needs n_q == n_k")
+    B, H, d = 2, 3, 5
+    q, k, v = _rand(rng, B, n_q, H, d), _rand(rng, B, n_k, H, d), _rand(rng, B, n_k, H, d)
+    do = _rand(rng, B, n_q, H, d)
+    v = v * np.arange(1, d + 1)          # dv and dk differ in scale: a dk <-> dv swap cannot pass
+    out_ref, gq, gk, gv = _autograd_mha(q, k, v, do, 0.7, causal)
+    out, _ = O.mha_forward(q, k, v, 0.7, causal=causal)
+    np.testing.assert_allclose(out, out_ref, atol=1e-12, rtol=0)
+    dq, dk, dv = O.mha_backward(q, k, v, do, 0.7, causal=causal)
+    for got, ref, nm in ((dq, gq, "dq"), (dk, gk, "dk"), (dv, gv, "dv")):
+        assert got.shape == ref.shape, nm
+        np.testing.assert_allclose(got, ref, atol=1e-12, rtol=0, err_msg=nm)
+
+
+def test_mha_backward_equals_per_head_backward(rng):
+    """Each (b, h) slice of mha_backward is O6 on that slice alone, and different heads differ."""
+    B, n_q, n_k, H, d = 2, 6, 4, 3, 4
+    q, k, v, do = (_rand(rng, B, n, H, d) for n in (n_q, n_k, n_k, n_q))
+    dq, dk, dv = O.mha_backward(q, k, v, do, 0.5)
+    for b in range(B):
+        for h in range(H):
+            r = O.backward(q[b, :, h], k[b, :, h], v[b, :, h], do[b, :, h], 0.5)
+            for got, ref in zip((dq[b, :, h], dk[b, :, h], dv[b, :, h]), r):
+                np.testing.assert_array_equal(got, ref)
+    assert np.abs(dq[0, :, 0] - dq[0, :, 1]).max() > 1e-3 and np.abs(dq[0] - dq[1]).max() > 1e-3
