@@ -172,8 +172,11 @@ MEA_API mea_status_t mea_attention_fwd_padded(const void* q, const void* k, cons
  * Single-query attention per (b,h) — the paper's O(1)-memory algorithm (PAPER.md:59-63,
  * stabilised as in PAPER.md:85-90). q,out [B,H,d]; k,v [B,n_k,H,d]. Keys are split into
  * ranges processed in parallel (split-K); each range yields a triple (m*, s*, v*) in the
- * workspace and a merge pass combines them with Figure 1's global-max rescale
- * (PAPER.md:140-147). Workspace is independent of n_k (bounded by the split count).
+ * workspace and the last CTA of each (b, head block) merges them with Figure 1's
+ * global-max rescale in the same launch. Workspace (>= 8-byte aligned,
+ * mea_single_query_workspace_size bytes) is independent of n_k (bounded by the split count);
+ * its contents need no initialisation and are scratch between calls (the CTAs' completion
+ * flags carry a per-call tag). Calls sharing one workspace must be stream-ordered.
  */
 MEA_API mea_status_t mea_single_query_fwd(const void* q, const void* k, const void* v, void* out,
                                   int64_t B, int64_t H, int64_t n_k, int64_t d,
@@ -222,6 +225,26 @@ MEA_API mea_status_t mea_single_query_partial(const void* q, const void* k, cons
 MEA_API mea_status_t mea_merge_partials(const float* m, const float* s, const float* vstar, int64_t P,
                                 int64_t B, int64_t H, int64_t d, void* out, mea_dtype_t out_dtype,
                                 void* stream);
+
+/*
+ * Packed triples, for a collective that moves one buffer (torch all_gather_into_tensor):
+ * record r = { v*[0..d), m, s, 0-pad, 0-pad }: MEA_TRIPLE_FLOATS(d) = d + 4 floats (16-byte
+ * aligned rows), same meanings as above (m natural log). The partial calls write
+ * [B*H] (single query) or [B*n_q*H] (self-attention, row (b, i, h)) records; the pad floats
+ * are not written. mea_merge_triples merges P stacked record arrays [P][rows] into out
+ * [rows, d] (out_dtype): the layout an all-gather of every rank's records produces.
+ * triples must be 16-byte aligned. Errors as the unpacked calls.
+ */
+#define MEA_TRIPLE_FLOATS(d) ((d) + 4)
+MEA_API mea_status_t mea_single_query_partial_packed(const void* q, const void* k, const void* v, float* triples,
+                                             int64_t B, int64_t H, int64_t n_k, int64_t d,
+                                             mea_dtype_t in_dtype, float scale, void* workspace,
+                                             size_t workspace_bytes, void* stream);
+MEA_API mea_status_t mea_attention_partial_fwd_packed(const void* q, const void* k, const void* v, float* triples,
+                                              int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                                              mea_dtype_t in_dtype, float scale, void* stream);
+MEA_API mea_status_t mea_merge_triples(const float* triples, int64_t P, int64_t rows, int64_t d, void* out,
+                               mea_dtype_t out_dtype, void* stream);
 
 /*
  * Backward of out = attention(q, k, v) (the VJP the paper obtains with jax.grad through

@@ -26,6 +26,19 @@ extern "C" {
 MEA_API void mea_profile_enable(int on);
 MEA_API mea_status_t mea_profile_read(char* buf, size_t cap);
 
+/*
+ * Experiment knobs (A/B measurements without a rebuild; defaults are the shipped design):
+ *   "sq_heads_per_cta" (0 = auto), "sq_ctas_per_sm" (0 = auto), "sq_l2_256" (1 = L2::256B hint).
+ */
+MEA_API mea_status_t mea_debug_set_option(const char* name, int value);
+
+/*
+ * Read-only HBM probe: streams `bytes` (multiple of 16) from device pointer p with 16-byte
+ * non-caching loads on `ctas` CTAs of 512 threads (<= 0: 2 per SM); sink is a device float
+ * that is (almost) never written. Gives the read roofline for the single-query kernel.
+ */
+MEA_API mea_status_t mea_debug_read_probe(const void* p, size_t bytes, int ctas, float* sink, void* stream);
+
 MEA_API mea_status_t mea_debug_umma_tile(const void* a, const void* b, const void* v, float* s_out,
                                  float* o_out, void* stream);
 

@@ -38,6 +38,11 @@ SIGNATURES = {
     "mea_single_query_partial": (_st, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _st, _f, _vp, _sz,
                                        _vp]),
     "mea_merge_partials": (_st, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _st, _vp]),
+    "mea_single_query_partial_packed": (_st, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _st, _f, _vp, _sz, _vp]),
+    "mea_attention_partial_fwd_packed": (_st, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _st, _f, _vp]),
+    "mea_merge_triples": (_st, [_vp, _i64, _i64, _i64, _vp, _st, _vp]),
+    "mea_debug_set_option": (_st, [_c.c_char_p, _c.c_int]),
+    "mea_debug_read_probe": (_st, [_vp, _sz, _c.c_int, _vp, _vp]),
     "mea_attention_bwd": (_st, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _st, _f, _vp,
                                 _vp, _sz, _vp]),
     "mea_attention_bwd_workspace_size": (_st, [_i64, _i64, _i64, _i64, _i64, _st, _c.c_int, _c.POINTER(_sz)]),

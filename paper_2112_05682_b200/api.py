@@ -279,6 +279,67 @@ def mea_merge_partials(m, s, vstar, B, H, out_dtype=torch.bfloat16, out=None):
     return out
 
 
+def triple_floats(d):
+    """Floats per packed triple record {v*[d], m, s, pad, pad} (MEA_TRIPLE_FLOATS, mea.h)."""
+    return d + 4
+
+
+def mea_single_query_partial_packed(q, k, v, scale=None, triples=None, workspace=None):
+    """Per-(b,h) stream triple over these keys as packed records [B*H, d+4] (v*, m, s; m natural
+    log) — the buffer a rank hands to all_gather_into_tensor unchanged."""
+    _cuda_contig(q, k, v, triples)
+    B, H, d = q.shape
+    n_k = k.shape[1]
+    if k.shape != (B, n_k, H, d) or v.shape != k.shape:
+        raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        raise TypeError("q, k, v must share a dtype")
+    dt = _dtype(q)
+    _expect(triples, (B * H, triple_floats(d)), torch.float32, "triples")
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    if triples is None:
+        triples = torch.empty((B * H, triple_floats(d)), dtype=torch.float32, device=q.device)
+    if workspace is None:
+        workspace = _workspace(mea_single_query_workspace_size(B, H, n_k, d, dt), q.device)
+    _check(_lib.load().mea_single_query_partial_packed(
+        _ptr(q), _ptr(k), _ptr(v), _ptr(triples), B, H, n_k, d, dt, scale, _ptr(workspace),
+        workspace.numel() if workspace is not None else 0, _stream(q.device)))
+    return triples
+
+
+def mea_attention_partial_fwd_packed(q, k, v, scale=None, triples=None):
+    """Every query row's stream triple over these keys as packed records [B*n_q*H, d+4]
+    (row (b, i, h)); bf16, d in {64, 128}."""
+    _cuda_contig(q, k, v, triples)
+    B, n_q, H, d = q.shape
+    n_k = k.shape[1]
+    if k.shape != (B, n_k, H, d) or v.shape != k.shape:
+        raise ValueError(f"shape mismatch q{tuple(q.shape)} k{tuple(k.shape)} v{tuple(v.shape)}")
+    if k.dtype != q.dtype or v.dtype != q.dtype:
+        raise TypeError("q, k, v must share a dtype")
+    _expect(triples, (B * n_q * H, triple_floats(d)), torch.float32, "triples")
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    if triples is None:
+        triples = torch.empty((B * n_q * H, triple_floats(d)), dtype=torch.float32, device=q.device)
+    _check(_lib.load().mea_attention_partial_fwd_packed(_ptr(q), _ptr(k), _ptr(v), _ptr(triples), B, H, n_q, n_k, d,
+                                                        _dtype(q), scale, _stream(q.device)))
+    return triples
+
+
+def mea_merge_triples(triples, out_dtype=torch.bfloat16, out=None):
+    """Merge stacked packed records triples [P, rows, d+4] -> out [rows, d]."""
+    _cuda_contig(triples, out)
+    if triples.dim() != 3 or triples.dtype != torch.float32:
+        raise ValueError("triples must be float32 [P, rows, d + 4]")
+    P, rows, w = triples.shape
+    d = w - 4
+    _expect_out(out, (rows, d))
+    if out is None:
+        out = torch.empty((rows, d), dtype=out_dtype, device=triples.device)
+    _check(_lib.load().mea_merge_triples(_ptr(triples), P, rows, d, _ptr(out), _dtype(out), _stream(triples.device)))
+    return out
+
+
 # ------------------------------------------------------------------------ backward
 def mea_attention_bwd_workspace_size(B, H, n_q, n_k, d, dtype, lse_given=True):
     n = ctypes.c_size_t(0)
@@ -397,6 +458,21 @@ def mea_debug_umma_tile(a, b, v):
     o = torch.empty((128, 64), dtype=torch.float32, device=a.device)
     _check(_lib.load().mea_debug_umma_tile(_ptr(a), _ptr(b), _ptr(v), _ptr(s), _ptr(o), _stream(a.device)))
     return s, o
+
+
+def debug_set_option(name, value):
+    """Experiment knobs of the library (mea_debug.h); defaults are the shipped design."""
+    _check(_lib.load().mea_debug_set_option(name.encode(), int(value)))
+
+
+def debug_read_probe(buf, ctas=0, sink=None):
+    """Stream the bytes of a CUDA tensor with the read-only HBM probe (mea_debug.h)."""
+    _cuda_contig(buf)
+    if sink is None:
+        sink = torch.empty(1, dtype=torch.float32, device=buf.device)
+    nbytes = buf.numel() * buf.element_size()
+    _check(_lib.load().mea_debug_read_probe(_ptr(buf), nbytes - nbytes % 16, ctas, _ptr(sink), _stream(buf.device)))
+    return sink
 
 
 # ------------------------------------------------------------------------ launch profiling

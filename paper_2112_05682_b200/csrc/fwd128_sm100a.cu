@@ -305,14 +305,14 @@ __global__ void __launch_bounds__(kThreads128, 1)
     if (row < q_end && p.tri_v) {
       // this call's (m*, s*, v*) per row, for a merge across key ranges
       const size_t idx = ((size_t)b * p.n_q + row) * p.H + h;
-      float4* dst = reinterpret_cast<float4*>(p.tri_v + idx * kD + half * 64);
+      float4* dst = reinterpret_cast<float4*>(p.tri_v + idx * p.tri_vs + half * 64);
 #pragma unroll
       for (int i = 0; i < 16; ++i)
         dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]), __uint_as_float(o[4 * i + 2]),
                              __uint_as_float(o[4 * i + 3]));
       if (half == 0) {
-        p.tri_m[idx] = m_ref * 0.6931471805599453f;
-        p.tri_s[idx] = lrow;
+        p.tri_m[idx * p.tri_ms] = m_ref * 0.6931471805599453f;
+        p.tri_s[idx * p.tri_ms] = lrow;
       }
     } else if (row < q_end && p.part_o) {  // key-split / tree summaries
       const size_t prow = ((size_t)split * p.B * p.H + (size_t)b * p.H + h) * p.q_count + (row - p.q_begin);

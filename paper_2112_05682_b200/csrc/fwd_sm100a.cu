@@ -439,14 +439,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.tri_v) {
         // this call's (m*, s*, v*) per row, for a merge across key ranges
         const size_t idx = ((size_t)b * p.n_q + row) * p.H + h;
-        float4* dst = reinterpret_cast<float4*>(p.tri_v + idx * kHeadDim + half * 32);
+        float4* dst = reinterpret_cast<float4*>(p.tri_v + idx * p.tri_vs + half * 32);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
                                __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
         if (half == 0) {
-          p.tri_m[idx] = m_ref * 0.6931471805599453f;
-          p.tri_s[idx] = lrow;
+          p.tri_m[idx * p.tri_ms] = m_ref * 0.6931471805599453f;
+          p.tri_s[idx * p.tri_ms] = lrow;
         }
       } else if (p.part_o) {  // key-split / tree summaries
         const size_t prow = ((size_t)split * p.B * p.H + bh) * p.q_count + (row - p.q_begin);
@@ -688,18 +688,19 @@ cudaError_t launch_fwd_bf16(const FwdParams& p, const CUtensorMap& mq, const CUt
 }
 
 // The triple of an empty key range: (m*, s*, v*) = (-inf, 0, 0) (PAPER.md:89's initial state).
-__global__ void empty_triples_kernel(float* m, float* s, float* vstar, int64_t rows, int d) {
+__global__ void empty_triples_kernel(float* m, float* s, float* vstar, int64_t ms, int64_t vs, int64_t rows, int d) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < rows) {
-    m[i] = -INFINITY;
-    s[i] = 0.f;
+    m[i * ms] = -INFINITY;
+    s[i * ms] = 0.f;
   }
-  if (i < rows * d) vstar[i] = 0.f;
+  if (i < rows * d) vstar[(i / d) * vs + i % d] = 0.f;
 }
 
-cudaError_t launch_empty_triples(float* m, float* s, float* vstar, int64_t rows, int d, cudaStream_t st) {
+cudaError_t launch_empty_triples(float* m, float* s, float* vstar, int64_t ms, int64_t vs, int64_t rows, int d,
+                                 cudaStream_t st) {
   const int64_t n = rows * d;
-  empty_triples_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(m, s, vstar, rows, d);
+  empty_triples_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(m, s, vstar, ms, vs, rows, d);
   return cudaGetLastError();
 }
 

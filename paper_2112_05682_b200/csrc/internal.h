@@ -49,6 +49,8 @@ struct FwdParams {
   float* tri_m;            // partial mode (mea_attention_partial_fwd): [B,n_q,H] m* (natural log)
   float* tri_s;            //   [B,n_q,H] s*
   float* tri_v;            //   [B,n_q,H,64] v* (unnormalised)
+  int tri_vs, tri_ms;      //   floats between rows of tri_v (d) and of tri_m / tri_s (1); packed
+                           //   records {v*[d], m, s, pad, pad}: both d + 4
   int causal;              // query i sees keys j <= i (n_q == n_k, one window, no key split)
   int d;                   // head dimension (64: fwd_bf16, 128: fwd128_bf16); merge_rows reads it
   unsigned* merge_cnt;     // d = 64 key split: [B*H][num_q_blocks] arrival counters (zeroed, self-
@@ -104,19 +106,38 @@ cudaError_t launch_fwd128_bf16(const FwdParams& p, const CUtensorMap& mq, const 
                                const CUtensorMap& mv, cudaStream_t s);
 cudaError_t launch_split_f32(const float* x, void* const* parts, int nparts, int64_t n, cudaStream_t s);
 cudaError_t launch_fwd_f32tc(const FwdParams& p, const CUtensorMap (&maps)[8], cudaStream_t s);
-cudaError_t launch_empty_triples(float* m, float* s, float* vstar, int64_t rows, int d, cudaStream_t st);
+cudaError_t launch_empty_triples(float* m, float* s, float* vstar, int64_t ms, int64_t vs, int64_t rows, int d,
+                                 cudaStream_t st);
 cudaError_t launch_fwd_f32(const float* q, const float* k, const float* v, float* out, float* lse, int B,
                            int H, int n_q, int n_k, int d, float scale, cudaStream_t s);
 
-// single query
-int sq_num_splits(int64_t BH, int64_t n_k);
-cudaError_t launch_sq_partial(const void* q, const void* k, const void* v, int bf16, int B, int H, int n_k,
-                              int d, float scale, int splits, float* ws, cudaStream_t s);
-// mode 0: write out (dtype) ; mode 1: write triple (m natural, s, v*)
-cudaError_t launch_sq_merge(const float* ws, int splits, int BH, int d, int mode, void* out, int out_f32,
-                            float* m, float* sum, float* vstar, cudaStream_t s);
-cudaError_t launch_merge_partials(const float* m, const float* s, const float* vstar, int P, int64_t rows, int d,
-                                  void* out, int out_f32, cudaStream_t st);
+// single query (single_query.cu): one kernel per call, the last CTA of each group merges
+struct SqParams {
+  const void *q, *k, *v;   // q [B,H,d]; k, v [B,n_k,H,d]
+  int B, H, n_k, d;
+  float c;                 // scale * log2(e)
+  int splits;              // key ranges per (b, head block)
+  float* rec;              // workspace: partial records [B*H][splits][d+2], then the flags
+  unsigned long long* tickets;  // [groups][splits] per-CTA "records written" flags (= tag)
+  unsigned long long tag;  // unique per call (set by launch_sq)
+  int mode;                // 0: out = attention; 1: the merged triple (m natural log, s, v*)
+  void* out;               // mode 0: [B,H,d] bf16 or f32
+  int out_f32;
+  float *tri_m, *tri_s, *tri_v;  // mode 1: row bh at tri_m[bh*ms], tri_s[bh*ms], tri_v[bh*vs + f]
+  int64_t tri_ms_stride, tri_v_stride;
+};
+struct SqPlan {
+  int hc, splits;
+  int64_t groups;
+  size_t rec_bytes, bytes;
+};
+SqPlan sq_plan(int64_t B, int64_t H, int64_t n_k, int64_t d, int bf16);
+cudaError_t launch_sq(SqParams p, const SqPlan& pl, int bf16, cudaStream_t s);
+extern int g_sq_heads_per_cta, g_sq_ctas_per_sm, g_sq_l2_256;
+// m at m[(i*rows + r)*ms], s likewise, v* at vstar[(i*rows + r)*vs + f]
+cudaError_t launch_merge_partials(const float* m, const float* s, const float* vstar, int64_t ms, int64_t vs, int P,
+                                  int64_t rows, int d, void* out, int out_f32, cudaStream_t st);
+cudaError_t launch_read_probe(const void* p, size_t bytes, int ctas, float* sink, cudaStream_t s);
 
 // backward
 // dq_acc nullable: zeroed when given (fused path)

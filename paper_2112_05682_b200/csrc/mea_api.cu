@@ -543,9 +543,9 @@ mea_status_t mea_attention_fwd_causal(const void* q, const void* k, const void* 
 }
 
 // ------------------------------------------------------------------ partial self-attention
-mea_status_t mea_attention_partial_fwd(const void* q, const void* k, const void* v, float* m, float* s, float* vstar,
-                                       int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
-                                       mea_dtype_t in_dtype, float scale, void* stream) {
+static mea_status_t partial_fwd_impl(const void* q, const void* k, const void* v, float* m, float* s, float* vstar,
+                                     int64_t ms, int64_t vs, int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                                     mea_dtype_t in_dtype, float scale, void* stream) {
   if (mea_status_t r = check_common(B, H, n_q, n_k, d, scale)) return r;
   if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
   if (in_dtype != MEA_BF16 || (d != kHeadDim && d != 128))
@@ -559,7 +559,7 @@ mea_status_t mea_attention_partial_fwd(const void* q, const void* k, const void*
   cudaError_t e;
   if (n_k == 0) {  // empty key range: the initial stream state
     ProfScope ps("empty_triples", st);
-    e = launch_empty_triples(m, s, vstar, B * n_q * H, (int)d, st);
+    e = launch_empty_triples(m, s, vstar, ms, vs, B * n_q * H, (int)d, st);
     return e == cudaSuccess ? MEA_OK : cuda_fail(e, "empty_triples launch");
   }
   if (!k || !v) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
@@ -589,6 +589,8 @@ mea_status_t mea_attention_partial_fwd(const void* q, const void* k, const void*
   p.tri_m = m;
   p.tri_s = s;
   p.tri_v = vstar;
+  p.tri_vs = (int)vs;
+  p.tri_ms = (int)ms;
   if (d == 128) {
     ProfScope ps("fwd128_bf16", st);
     if ((e = launch_fwd128_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd128_bf16 launch");
@@ -599,20 +601,33 @@ mea_status_t mea_attention_partial_fwd(const void* q, const void* k, const void*
   return MEA_OK;
 }
 
+mea_status_t mea_attention_partial_fwd(const void* q, const void* k, const void* v, float* m, float* s, float* vstar,
+                                       int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d,
+                                       mea_dtype_t in_dtype, float scale, void* stream) {
+  return partial_fwd_impl(q, k, v, m, s, vstar, 1, d, B, H, n_q, n_k, d, in_dtype, scale, stream);
+}
+
+mea_status_t mea_attention_partial_fwd_packed(const void* q, const void* k, const void* v, float* triples, int64_t B,
+                                              int64_t H, int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t in_dtype,
+                                              float scale, void* stream) {
+  if (!triples && n_q > 0) return fail(MEA_ERR_INVALID_VALUE, "NULL triples");
+  return partial_fwd_impl(q, k, v, triples + d, triples + d + 1, triples, d + 4, d + 4, B, H, n_q, n_k, d, in_dtype,
+                          scale, stream);
+}
+
 // ------------------------------------------------------------------ single query
 mea_status_t mea_single_query_workspace_size(int64_t B, int64_t H, int64_t n_k, int64_t d, mea_dtype_t in_dtype,
                                              size_t* bytes) {
   if (!bytes) return fail(MEA_ERR_INVALID_VALUE, "bytes is NULL");
   if (mea_status_t s = check_common(B, H, 1, n_k, d, 1.f)) return s;
   if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  const int splits = sq_num_splits(B * H, n_k);
-  *bytes = (size_t)B * H * splits * (d + 2) * sizeof(float);
+  *bytes = sq_plan(B, H, n_k, d, in_dtype == MEA_BF16).bytes;
   return MEA_OK;
 }
 
 static mea_status_t sq_common(const void* q, const void* k, const void* v, int64_t B, int64_t H, int64_t n_k,
                               int64_t d, mea_dtype_t in_dtype, float scale, void* workspace, size_t workspace_bytes,
-                              int* splits_out) {
+                              SqPlan* plan) {
   if (mea_status_t s = check_common(B, H, 1, n_k, d, scale)) return s;
   if (!valid_dtype(in_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
   if (in_dtype == MEA_BF16 && d != kHeadDim && d != 128)
@@ -621,11 +636,26 @@ static mea_status_t sq_common(const void* q, const void* k, const void* v, int64
   if (B * H > 65535) return fail(MEA_ERR_UNSUPPORTED, "B*H > 65535");
   if (!q || (n_k > 0 && (!k || !v))) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
   if (!aligned16(q) || !aligned16(k) || !aligned16(v)) return fail(MEA_ERR_MISALIGNED, "q, k, v must be 16-byte aligned");
-  const int splits = sq_num_splits(B * H, n_k);
-  const size_t need = (size_t)B * H * splits * (d + 2) * sizeof(float);
-  if (!workspace || workspace_bytes < need) return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "single query needs workspace");
-  *splits_out = splits;
+  *plan = sq_plan(B, H, n_k, d, in_dtype == MEA_BF16);
+  if (!workspace || workspace_bytes < plan->bytes)
+    return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "single query needs mea_single_query_workspace_size bytes");
+  if (reinterpret_cast<uintptr_t>(workspace) & 7u) return fail(MEA_ERR_MISALIGNED, "workspace must be 8-byte aligned");
   return MEA_OK;
+}
+
+static SqParams sq_params(const void* q, const void* k, const void* v, int64_t B, int64_t H, int64_t n_k, int64_t d,
+                          float scale, void* workspace) {
+  SqParams p{};
+  p.q = q;
+  p.k = k;
+  p.v = v;
+  p.B = (int)B;
+  p.H = (int)H;
+  p.n_k = (int)n_k;
+  p.d = (int)d;
+  p.c = scale * 1.4426950408889634f;
+  p.rec = static_cast<float*>(workspace);
+  return p;
 }
 
 mea_status_t mea_single_query_fwd(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
@@ -633,58 +663,79 @@ mea_status_t mea_single_query_fwd(const void* q, const void* k, const void* v, v
                                   void* workspace, size_t workspace_bytes, void* stream) {
   if (n_k == 0 && B >= 1 && H >= 1 && d >= 1) return fail(MEA_ERR_EMPTY_KEYS, "attention over an empty key list");
   if (!valid_dtype(out_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  int splits = 0;
-  if (mea_status_t s = sq_common(q, k, v, B, H, n_k, d, in_dtype, scale, workspace, workspace_bytes, &splits)) return s;
+  SqPlan pl{};
+  if (mea_status_t s = sq_common(q, k, v, B, H, n_k, d, in_dtype, scale, workspace, workspace_bytes, &pl)) return s;
   if (!out || !aligned16(out)) return fail(out ? MEA_ERR_MISALIGNED : MEA_ERR_INVALID_VALUE, "bad out pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  float* ws = static_cast<float*>(workspace);
-  cudaError_t e;
-  {
-    ProfScope ps("sq_partial", st);
-    e = launch_sq_partial(q, k, v, in_dtype == MEA_BF16, (int)B, (int)H, (int)n_k, (int)d, scale, splits, ws, st);
-  }
-  if (e != cudaSuccess) return cuda_fail(e, "sq_partial launch");
-  {
-    ProfScope ps("sq_merge", st);
-    e = launch_sq_merge(ws, splits, (int)(B * H), (int)d, 0, out, out_dtype == MEA_F32, nullptr, nullptr, nullptr, st);
-  }
-  return e == cudaSuccess ? MEA_OK : cuda_fail(e, "sq_merge launch");
+  SqParams p = sq_params(q, k, v, B, H, n_k, d, scale, workspace);
+  p.mode = 0;
+  p.out = out;
+  p.out_f32 = out_dtype == MEA_F32;
+  ProfScope ps("sq_fused", st);
+  const cudaError_t e = launch_sq(p, pl, in_dtype == MEA_BF16, st);
+  return e == cudaSuccess ? MEA_OK : cuda_fail(e, "single query launch");
+}
+
+static mea_status_t sq_partial_impl(const void* q, const void* k, const void* v, float* m, float* s, float* vstar,
+                                    int64_t ms, int64_t vs, int64_t B, int64_t H, int64_t n_k, int64_t d,
+                                    mea_dtype_t in_dtype, float scale, void* workspace, size_t workspace_bytes,
+                                    void* stream) {
+  SqPlan pl{};
+  if (mea_status_t r = sq_common(q, k, v, B, H, n_k, d, in_dtype, scale, workspace, workspace_bytes, &pl)) return r;
+  if (!m || !s || !vstar) return fail(MEA_ERR_INVALID_VALUE, "NULL triple pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SqParams p = sq_params(q, k, v, B, H, n_k, d, scale, workspace);
+  p.mode = 1;
+  p.tri_m = m;
+  p.tri_s = s;
+  p.tri_v = vstar;
+  p.tri_ms_stride = ms;
+  p.tri_v_stride = vs;
+  ProfScope ps("sq_fused_triple", st);
+  const cudaError_t e = launch_sq(p, pl, in_dtype == MEA_BF16, st);
+  return e == cudaSuccess ? MEA_OK : cuda_fail(e, "single query launch");
 }
 
 mea_status_t mea_single_query_partial(const void* q, const void* k, const void* v, float* m, float* s, float* vstar,
                                       int64_t B, int64_t H, int64_t n_k, int64_t d, mea_dtype_t in_dtype, float scale,
                                       void* workspace, size_t workspace_bytes, void* stream) {
-  int splits = 0;
-  if (mea_status_t r = sq_common(q, k, v, B, H, n_k, d, in_dtype, scale, workspace, workspace_bytes, &splits)) return r;
-  if (!m || !s || !vstar) return fail(MEA_ERR_INVALID_VALUE, "NULL triple pointer");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  float* ws = static_cast<float*>(workspace);
-  cudaError_t e;
-  {
-    ProfScope ps("sq_partial", st);
-    e = launch_sq_partial(q, k, v, in_dtype == MEA_BF16, (int)B, (int)H, (int)n_k, (int)d, scale, splits, ws, st);
-  }
-  if (e != cudaSuccess) return cuda_fail(e, "sq_partial launch");
-  {
-    ProfScope ps("sq_merge_triple", st);
-    e = launch_sq_merge(ws, splits, (int)(B * H), (int)d, 1, nullptr, 0, m, s, vstar, st);
-  }
-  return e == cudaSuccess ? MEA_OK : cuda_fail(e, "sq_merge launch");
+  return sq_partial_impl(q, k, v, m, s, vstar, 1, d, B, H, n_k, d, in_dtype, scale, workspace, workspace_bytes, stream);
 }
 
-mea_status_t mea_merge_partials(const float* m, const float* s, const float* vstar, int64_t P, int64_t B, int64_t H,
-                                int64_t d, void* out, mea_dtype_t out_dtype, void* stream) {
-  if (P < 0 || B < 1 || H < 1 || d < 1) return fail(MEA_ERR_INVALID_VALUE, "bad sizes");
+mea_status_t mea_single_query_partial_packed(const void* q, const void* k, const void* v, float* triples, int64_t B,
+                                             int64_t H, int64_t n_k, int64_t d, mea_dtype_t in_dtype, float scale,
+                                             void* workspace, size_t workspace_bytes, void* stream) {
+  if (!triples) return fail(MEA_ERR_INVALID_VALUE, "NULL triples");
+  if (!aligned16(triples)) return fail(MEA_ERR_MISALIGNED, "triples must be 16-byte aligned");
+  return sq_partial_impl(q, k, v, triples + d, triples + d + 1, triples, d + 4, d + 4, B, H, n_k, d, in_dtype, scale,
+                         workspace, workspace_bytes, stream);
+}
+
+static mea_status_t merge_impl(const float* m, const float* s, const float* vstar, int64_t ms, int64_t vs, int64_t P,
+                               int64_t rows, int64_t d, void* out, mea_dtype_t out_dtype, void* stream) {
+  if (P < 0 || rows < 1 || d < 1) return fail(MEA_ERR_INVALID_VALUE, "bad sizes");
   if (P == 0) return fail(MEA_ERR_EMPTY_KEYS, "no partials to merge");
   if (d > 128) return fail(MEA_ERR_UNSUPPORTED, "d <= 128");
   if (P > kMaxInt) return fail(MEA_ERR_UNSUPPORTED, "P too large");
   if (!valid_dtype(out_dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
   if (!m || !s || !vstar || !out) return fail(MEA_ERR_INVALID_VALUE, "NULL pointer");
-  if ((B * H + 7) / 8 > kMaxInt) return fail(MEA_ERR_UNSUPPORTED, "too many rows");
+  if ((rows + 7) / 8 > kMaxInt) return fail(MEA_ERR_UNSUPPORTED, "too many rows");
   ProfScope ps("merge_partials", static_cast<cudaStream_t>(stream));
-  cudaError_t e = launch_merge_partials(m, s, vstar, (int)P, B * H, (int)d, out, out_dtype == MEA_F32,
+  cudaError_t e = launch_merge_partials(m, s, vstar, ms, vs, (int)P, rows, (int)d, out, out_dtype == MEA_F32,
                                         static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? MEA_OK : cuda_fail(e, "merge_partials launch");
+}
+
+mea_status_t mea_merge_partials(const float* m, const float* s, const float* vstar, int64_t P, int64_t B, int64_t H,
+                                int64_t d, void* out, mea_dtype_t out_dtype, void* stream) {
+  if (B < 1 || H < 1) return fail(MEA_ERR_INVALID_VALUE, "bad sizes");
+  return merge_impl(m, s, vstar, 1, d, P, B * H, d, out, out_dtype, stream);
+}
+
+mea_status_t mea_merge_triples(const float* triples, int64_t P, int64_t rows, int64_t d, void* out,
+                               mea_dtype_t out_dtype, void* stream) {
+  if (!triples) return fail(MEA_ERR_INVALID_VALUE, "NULL triples");
+  return merge_impl(triples + d, triples + d + 1, triples, d + 4, d + 4, P, rows, d, out, out_dtype, stream);
 }
 
 // ------------------------------------------------------------------ backward
@@ -959,6 +1010,22 @@ mea_status_t mea_profile_read(char* buf, size_t cap) {
     buf[n] = 0;
   }
   return err == cudaSuccess ? MEA_OK : cuda_fail(err, "profile events");
+}
+
+mea_status_t mea_debug_set_option(const char* name, int value) {
+  if (!name) return fail(MEA_ERR_INVALID_VALUE, "NULL name");
+  const std::string n(name);
+  if (n == "sq_heads_per_cta") mea::g_sq_heads_per_cta = value;
+  else if (n == "sq_ctas_per_sm") mea::g_sq_ctas_per_sm = value;
+  else if (n == "sq_l2_256") mea::g_sq_l2_256 = value;
+  else return fail(MEA_ERR_INVALID_VALUE, "unknown option");
+  return MEA_OK;
+}
+
+mea_status_t mea_debug_read_probe(const void* p, size_t bytes, int ctas, float* sink, void* stream) {
+  if (!p || !sink || !aligned16(p) || (bytes & 15u)) return fail(MEA_ERR_INVALID_VALUE, "bad read probe arguments");
+  const cudaError_t e = mea::launch_read_probe(p, bytes, ctas, sink, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? MEA_OK : cuda_fail(e, "read probe launch");
 }
 
 mea_status_t mea_debug_umma_tile(const void* a, const void* b, const void* v, float* s_out, float* o_out,

@@ -1,52 +1,55 @@
 // single_query.cu — the paper's O(1)-memory single-query attention (made
-// stable by the running max of PAPER.md:85-90), split over key ranges (split-K), plus the
-// merge of the per-range states with Figure 1's global-max rescale.
+// stable by the running max of PAPER.md:85-90), split over key ranges (split-K), with the
+// merge of the per-range states by Figure 1's global-max rescale done in
+// the SAME launch by the last split CTA of each group (decoupled look-back), one kernel per call.
 //
 // HBM-bound: every key costs 4*d bytes (k and v rows, bf16) and 4*d flops, 1 flop/byte.
-// bf16 d=64 kernel: a warp reads 16 keys per step; 8 lanes share one 128-byte key row
-// (16 B = 8 bf16 each, coalesced 128-bit loads), the dot product finishes with 3 xor-shuffles
-// inside the 8-lane group, and each group runs its own stream state (m*, s*, v*[8 dims per
-// lane]) with one rescale per 4 keys (block max first). Groups, warps and CTAs are then
-// merged with the same rescale rule. Two steps are unrolled so 8 K and 8 V loads (256 B)
-// per lane are in flight.
+// bf16 kernel: 8 (d = 64) or 16 (d = 128) lanes share one key row (16 B = 8 bf16 each,
+// 128-bit streaming loads), the dot product finishes with xor-shuffles inside the lane group,
+// and each group runs its own stream state (m*, s*, v*[8 dims per lane]) with one rescale per
+// 4 keys (block max first). A CTA covers one key range of HC heads of one batch element: the
+// HC rows of a key are adjacent in [B, n_k, H, d], so a warp-load of HC >= 2 heads is one
+// contiguous 256-byte (or longer) run instead of head-strided 128-byte rows. Groups, warps and
+// splits are merged with the same rescale rule.
 //
-// Partial layout (workspace, float32): part[(bh * splits + split) * (d + 2) + {0: m*, 1: s*,
-// 2..: v*}], with m* in log2 units of the scaled score (p = 2^(s*c - m*), c = scale*log2 e).
+// Partial records (workspace, float32): rec[(bh * splits + split) * (d + 2) + {0: m*, 1: s*,
+// 2..: v*}], m* in log2 units of the scaled score (p = 2^(s*c - m*), c = scale*log2 e). After
+// the records: one 64-bit flag per CTA, set to the call's tag (unique per call: a host counter
+// started from the clock) once the CTA's records are written; the last split of each group
+// waits for its group's flags and merges (decoupled look-back). A flag left by an earlier call,
+// or uninitialised workspace, never matches: no memset, no reset, no atomics.
 #include <cuda_bf16.h>
 
+#include <atomic>
+#include <chrono>
 #include <cmath>
 
 #include "internal.h"
 #include "ptx.cuh"
 
 namespace mea {
+
+// experiment knobs (mea_debug_set_option), defaults = the shipped configuration
+int g_sq_heads_per_cta = 0;   // 0 = automatic
+int g_sq_ctas_per_sm = 0;     // 0 = automatic
+int g_sq_l2_256 = 1;          // L2::256B prefetch hint on the K/V loads
+
 namespace {
 
-#ifndef MEA_SQ_THREADS
-#define MEA_SQ_THREADS 512
-#endif
-#ifndef MEA_SQ_UNROLL
-#define MEA_SQ_UNROLL 2
-#endif
-#ifndef MEA_SQ_CTAS
-#define MEA_SQ_CTAS 148
-#endif
-constexpr int kSqThreads = MEA_SQ_THREADS;  // one CTA per SM: 16 warps x 256 B x 2 steps in flight
+constexpr int kSqThreads = 512;
 constexpr int kSqWarps = kSqThreads / 32;
-// D = 64: 8 lanes per 128-byte key row, 4 key groups per warp; D = 128: 16 lanes per 256-byte
-// row, 2 groups. Every lane holds 8 dims of its group's state.
 template <int D> struct SqCfg {
-  static constexpr int LPR = D / 8;                  // lanes per key row
-  static constexpr int G = 32 / LPR;                 // key groups per warp
-  static constexpr int kKeysPerWarpStep = 4 * G;     // 4 keys per group per step
+  static constexpr int LPR = D / 8;     // lanes per key row
+  static constexpr int G = 32 / LPR;    // key groups per warp
+  static constexpr int NG = kSqWarps * G;
 };
-constexpr int kUnroll = MEA_SQ_UNROLL;  // warp steps in flight
+constexpr int kUnroll = 2;  // warp steps in flight
 
 struct State {
   float m, l, a[8];
 };
 
-// Merge state o into s (both relative to their own reference max).
+// Merge state o into s (both relative to their own reference max, log2 units).
 __device__ __forceinline__ void merge_state(State& s, const State& o) {
   const float M = fmaxf(s.m, o.m);
   if (M == -INFINITY) return;
@@ -66,37 +69,142 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float (&f)[8]) {
   }
 }
 
+template <bool kL2Hint>
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+  if (kL2Hint)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
   return r;
 }
 
-template <int D>
-__global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_bfloat16* __restrict__ q,
-                                                                     const __nv_bfloat16* __restrict__ k,
-                                                                     const __nv_bfloat16* __restrict__ v, int H,
-                                                                     int n_k, float scale_log2, int splits,
-                                                                     float* __restrict__ part) {
-  asm volatile("griddepcontrol.launch_dependents;");
+// Final merge of one CTA group (HC heads x `splits` records each), run by the last CTA:
+//   M = max_s m_s;  out = sum_s 2^(m_s - M) v*_s / sum_s 2^(m_s - M) s*_s
+// Threads own (head, feature) outputs; with fewer outputs than threads the splits are divided
+// among T thread subsets, each folding its splits with the online rule, then combined in smem.
+template <int NT>
+__device__ void merge_group(const SqParams& p, const float* __restrict__ rec, int bh0, int HC, int d, float* smem) {
+  const int O = HC * d;
+  const int T = O >= NT ? 1 : NT / O;
+  const int splits = p.splits;
+  float* sm_m = smem;                 // [T][O]
+  float* sm_l = sm_m + T * O;
+  float* sm_a = sm_l + T * O;
+  for (int t = threadIdx.x; t < O * T; t += NT) {
+    const int o = t % O, j = t / O;
+    const int hl = o / d, f = o % d;
+    const float* base = rec + (size_t)(bh0 + hl) * splits * (d + 2);
+    float m = -INFINITY, l = 0.f, a = 0.f;
+    for (int s0 = j; s0 < splits; s0 += 8 * T) {
+      float ms[8], ls[8], as[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int s = s0 + u * T;
+        const bool ok = s < splits;
+        const float* r = base + (size_t)(ok ? s : 0) * (d + 2);
+        ms[u] = ok ? __ldcg(r) : -INFINITY;
+        ls[u] = ok ? __ldcg(r + 1) : 0.f;
+        as[u] = ok ? __ldcg(r + 2 + f) : 0.f;
+      }
+      float M = m;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) M = fmaxf(M, ms[u]);
+      if (M == -INFINITY) continue;
+      const float w0 = ex2_approx(m - M);
+      l *= w0;
+      a *= w0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float w = ex2_approx(ms[u] - M);
+        l = fmaf(w, ls[u], l);
+        a = fmaf(w, as[u], a);
+      }
+      m = M;
+    }
+    sm_m[j * O + o] = m;
+    sm_l[j * O + o] = l;
+    sm_a[j * O + o] = a;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < O; o += NT) {
+    float M = -INFINITY;
+    for (int j = 0; j < T; ++j) M = fmaxf(M, sm_m[j * O + o]);
+    float L = 0.f, A = 0.f;
+    if (M != -INFINITY)
+      for (int j = 0; j < T; ++j) {
+        const float w = ex2_approx(sm_m[j * O + o] - M);
+        L = fmaf(w, sm_l[j * O + o], L);
+        A = fmaf(w, sm_a[j * O + o], A);
+      }
+    const int hl = o / d, f = o % d;
+    const size_t bh = (size_t)(bh0 + hl);
+    if (p.mode == 0) {
+      const float r = A / L;
+      if (p.out_f32) static_cast<float*>(p.out)[bh * d + f] = r;
+      else static_cast<__nv_bfloat16*>(p.out)[bh * d + f] = __float2bfloat16_rn(r);
+    } else {  // the merged triple, m in natural-log units, for the cross-GPU merge
+      if (f == 0) {
+        p.tri_m[bh * p.tri_ms_stride] = M * 0.6931471805599453f;
+        p.tri_s[bh * p.tri_ms_stride] = L;
+      }
+      p.tri_v[bh * p.tri_v_stride + f] = A;
+    }
+  }
+}
+
+// Publishes this CTA's records (written before the call) by storing the call's tag in its
+// flag; the LAST split of the group (dispatched after the others, so they are resident or done:
+// the forward-progress assumption of a decoupled look-back) waits for every flag of its group to
+// carry the tag, then merges. A flag left by an earlier call, or uninitialised workspace, holds
+// another value: no memset, no counter reset, no atomics.
+template <int NT>
+__device__ __forceinline__ void finish_cta(const SqParams& p, int group, int split, int bh0, int HC, int d,
+                                           float* smem) {
+  unsigned long long* flags = p.tickets + (size_t)group * p.splits;
+  __threadfence();  // this thread's record writes are visible device-wide before the flag
+  __syncthreads();
+  if (split != p.splits - 1) {
+    if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned long long*>(flags + split) = p.tag;
+    return;
+  }
+  for (int s = threadIdx.x; s < p.splits - 1; s += NT)
+    while (*reinterpret_cast<volatile unsigned long long*>(flags + s) != p.tag) {
+    }
+  __syncthreads();
+  __threadfence();
+  merge_group<NT>(p, p.rec, bh0, HC, d, smem);
+}
+
+template <int D, int HC, bool kL2Hint>
+__global__ void __launch_bounds__(kSqThreads) sq_bf16_kernel(const SqParams p) {
   using C = SqCfg<D>;
-  constexpr int LPR = C::LPR, kKeysPerWarpStep = C::kKeysPerWarpStep;
-  const int split = blockIdx.x, bh = blockIdx.y;
-  const int b = bh / H, h = bh % H;
+  constexpr int LPR = C::LPR, G = C::G, NG = C::NG;
+  constexpr int KS = NG / HC;                 // key slots per CTA step (groups per head)
+  constexpr int kStep = 4 * KS;               // keys per CTA step (4 per group)
+  const int split = blockIdx.x, group = blockIdx.y;
+  const int hb = p.H / HC;                    // head blocks per batch element
+  const int b = group / hb, h0 = (group % hb) * HC;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane / LPR, cidx = lane % LPR;  // key group in the warp, 16-byte chunk of the row
-  const int per = (n_k + splits - 1) / splits;
+  const int g = lane / LPR, cidx = lane % LPR;
+  const int gid = warp * G + g;               // group in the CTA
+  const int hl = gid % HC, ks = gid / HC;     // its head (of the block) and key slot
+  const int n_k = p.n_k;
+  const int per = (n_k + p.splits - 1) / p.splits;
   const int k_lo = split * per, k_hi = min(n_k, k_lo + per);
-  const size_t row_stride = (size_t)H * D;  // elements between consecutive keys
-  const __nv_bfloat16* kb = k + ((size_t)b * n_k * H + h) * D + cidx * 8;
-  const __nv_bfloat16* vb = v + ((size_t)b * n_k * H + h) * D + cidx * 8;
+  const size_t row_stride = (size_t)p.H * D;  // elements between consecutive keys
+  const __nv_bfloat16* kb = static_cast<const __nv_bfloat16*>(p.k) + ((size_t)b * n_k * p.H + h0 + hl) * D + cidx * 8;
+  const __nv_bfloat16* vb = static_cast<const __nv_bfloat16*>(p.v) + ((size_t)b * n_k * p.H + h0 + hl) * D + cidx * 8;
+  const int bh = b * p.H + h0 + hl;
 
   float qf[8];
-  bf16x8_to_f32(*reinterpret_cast<const uint4*>(q + (size_t)bh * D + cidx * 8), qf);
+  bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.q) + (size_t)bh * D + cidx * 8), qf);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) qf[i] *= scale_log2;
+  for (int i = 0; i < 8; ++i) qf[i] *= p.c;
 
   State st;
   st.m = -INFINITY;
@@ -104,17 +212,20 @@ __global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_
 #pragma unroll
   for (int i = 0; i < 8; ++i) st.a[i] = 0.f;
 
-  constexpr int kStep = kSqWarps * kKeysPerWarpStep;  // keys per CTA step
-  for (int base = k_lo + warp * kKeysPerWarpStep; base < k_hi; base += kStep * kUnroll) {
+  // the trip count must be warp-uniform (the shuffles below take the full mask): the loop runs
+  // while the warp's first key slot has keys left; other slots mask their keys individually
+  const int ks_warp = (warp * G) / HC;
+  for (int base0 = k_lo; base0 + ks_warp < k_hi; base0 += kStep * kUnroll) {
+    const int base = base0 + ks;
     uint4 kr[kUnroll][4], vr[kUnroll][4];
 #pragma unroll
     for (int s = 0; s < kUnroll; ++s)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int key = base + s * kStep + u * C::G + g;
+        const int key = base + s * kStep + u * KS;
         if (key < k_hi) {
-          kr[s][u] = ld_stream(kb + (size_t)key * row_stride);
-          vr[s][u] = ld_stream(vb + (size_t)key * row_stride);
+          kr[s][u] = ld_stream<kL2Hint>(kb + (size_t)key * row_stride);
+          vr[s][u] = ld_stream<kL2Hint>(vb + (size_t)key * row_stride);
         } else {
           kr[s][u] = make_uint4(0, 0, 0, 0);
           vr[s][u] = make_uint4(0, 0, 0, 0);
@@ -132,7 +243,7 @@ __global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_
         for (int i = 0; i < 8; ++i) dot = fmaf(qf[i], kf[i], dot);
 #pragma unroll
         for (int o = 1; o < LPR; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        const int key = base + s * kStep + u * C::G + g;
+        const int key = base + s * kStep + u * KS;
         sc[u] = key < k_hi ? dot : -INFINITY;
       }
       const float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
@@ -154,9 +265,10 @@ __global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_
       st.m = m_new;
     }
   }
-  // merge the key groups of the warp (lanes with equal cidx hold the same 8 dims)
+  // merge the groups of the warp that share a head (group ids equal mod HC)
 #pragma unroll
-  for (int off = LPR; off <= 16; off <<= 1) {
+  for (int gx = HC; gx < G; gx <<= 1) {
+    const int off = gx * LPR;
     State o;
     o.m = __shfl_xor_sync(0xffffffffu, st.m, off);
     o.l = __shfl_xor_sync(0xffffffffu, st.l, off);
@@ -164,45 +276,60 @@ __global__ void __launch_bounds__(kSqThreads) sq_partial_bf16_kernel(const __nv_
     for (int i = 0; i < 8; ++i) o.a[i] = __shfl_xor_sync(0xffffffffu, st.a[i], off);
     merge_state(st, o);
   }
-  __shared__ float sm_m[kSqWarps], sm_l[kSqWarps], sm_a[kSqWarps][D];
-  if (lane < LPR) {
-    if (lane == 0) {
-      sm_m[warp] = st.m;
-      sm_l[warp] = st.l;
+  // groups g < min(G, HC) of each warp now hold distinct (warp, head) states
+  constexpr int GV = G < HC ? G : HC;
+  __shared__ float sm_m[NG], sm_l[NG];
+  __shared__ __align__(16) float sm_a[NG][D];
+  if (g < GV) {
+    if (cidx == 0) {
+      sm_m[gid] = st.m;
+      sm_l[gid] = st.l;
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) sm_a[warp][cidx * 8 + i] = st.a[i];
+    for (int i = 0; i < 8; ++i) sm_a[gid][cidx * 8 + i] = st.a[i];
   }
   __syncthreads();
-  if (threadIdx.x < D) {
-    const int f = threadIdx.x;
+  // CTA record per head: fold the states of head hl2 = entries gid = hl2 + j*HC with gid%G < GV
+  for (int t = threadIdx.x; t < HC * D; t += kSqThreads) {
+    const int hl2 = t / D, f = t % D;
     float M = -INFINITY;
-    for (int w = 0; w < kSqWarps; ++w) M = fmaxf(M, sm_m[w]);
-    float l = 0.f, a = 0.f;
-    if (M != -INFINITY) {
-      for (int w = 0; w < kSqWarps; ++w) {
-        const float wt = ex2_approx(sm_m[w] - M);
-        l += wt * sm_l[w];
-        a += wt * sm_a[w][f];
-      }
+    for (int j = 0; j < KS; ++j) {
+      const int e = hl2 + j * HC;
+      if (e % G < GV) M = fmaxf(M, sm_m[e]);
     }
-    float* dst = part + ((size_t)bh * splits + split) * (D + 2);
+    float l = 0.f, a = 0.f;
+    if (M != -INFINITY)
+      for (int j = 0; j < KS; ++j) {
+        const int e = hl2 + j * HC;
+        if (e % G >= GV) continue;
+        const float w = ex2_approx(sm_m[e] - M);
+        l = fmaf(w, sm_l[e], l);
+        a = fmaf(w, sm_a[e][f], a);
+      }
+    float* dst = p.rec + ((size_t)(b * p.H + h0 + hl2) * p.splits + split) * (D + 2);
     if (f == 0) {
       dst[0] = M;
       dst[1] = l;
     }
     dst[2 + f] = a;
   }
+  // the final merge reuses the state arrays as scratch: (3 T O floats, T O <= max(512, HC D))
+  static_assert(3 * (kSqThreads > HC * D ? kSqThreads : HC * D) <= NG * D, "merge scratch");
+  __syncthreads();
+  finish_cta<kSqThreads>(p, group, split, b * p.H + h0, HC, D, &sm_a[0][0]);
 }
 
 // f32 inputs, any d <= 128: one warp per key, lanes own dims {lane, lane+32, lane+64, lane+96}.
-__global__ void __launch_bounds__(128) sq_partial_f32_kernel(const float* __restrict__ q, const float* __restrict__ k,
-                                                            const float* __restrict__ v, int H, int n_k, int d,
-                                                            float scale_log2, int splits, float* __restrict__ part) {
+constexpr int kF32Threads = 128;
+__global__ void __launch_bounds__(kF32Threads) sq_f32_kernel(const SqParams p) {
   const int split = blockIdx.x, bh = blockIdx.y;
+  const int H = p.H, d = p.d, n_k = p.n_k;
   const int b = bh / H, h = bh % H;
+  const float* q = static_cast<const float*>(p.q);
+  const float* k = static_cast<const float*>(p.k);
+  const float* v = static_cast<const float*>(p.v);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int per = (n_k + splits - 1) / splits;
+  const int per = (n_k + p.splits - 1) / p.splits;
   const int k_lo = split * per, k_hi = min(n_k, k_lo + per);
   float qf[4], a[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -216,22 +343,23 @@ __global__ void __launch_bounds__(128) sq_partial_f32_kernel(const float* __rest
       if (lane + 32 * i < d) dot = fmaf(qf[i], k[off + lane + 32 * i], dot);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    const float s = dot * scale_log2;
+    const float s = dot * p.c;
     const float m_new = fmaxf(m, s);
     const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - m_new);
-    const float p = exp2f(s - m_new);
-    l = l * alpha + p;
+    const float pr = exp2f(s - m_new);
+    l = l * alpha + pr;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = a[i] * alpha + ((lane + 32 * i < d) ? p * v[off + lane + 32 * i] : 0.f);
+    for (int i = 0; i < 4; ++i) a[i] = a[i] * alpha + ((lane + 32 * i < d) ? pr * v[off + lane + 32 * i] : 0.f);
     m = m_new;
   }
-  __shared__ float sm_m[4], sm_l[4], sm_a[4][128];
+  __shared__ float sm_m[4], sm_l[4];
+  __shared__ __align__(16) float sm_a[4 * 128];   // warp states, then the merge scratch (3 x 128)
   if (lane == 0) {
     sm_m[warp] = m;
     sm_l[warp] = l;
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) sm_a[warp][lane + 32 * i] = a[i];
+  for (int i = 0; i < 4; ++i) sm_a[warp * 128 + lane + 32 * i] = a[i];
   __syncthreads();
   if (threadIdx.x < d) {
     const int f = threadIdx.x;
@@ -242,108 +370,37 @@ __global__ void __launch_bounds__(128) sq_partial_f32_kernel(const float* __rest
       for (int w = 0; w < 4; ++w) {
         const float wt = exp2f(sm_m[w] - M);
         ls += wt * sm_l[w];
-        as += wt * sm_a[w][f];
+        as += wt * sm_a[w * 128 + f];
       }
-    float* dst = part + ((size_t)bh * splits + split) * (d + 2);
+    float* dst = p.rec + ((size_t)bh * p.splits + split) * (d + 2);
     if (f == 0) {
       dst[0] = M;
       dst[1] = ls;
     }
     dst[2 + f] = as;
   }
-}
-
-// Merge `splits` partial states per (b,h) (Figure 1 lines 33-40):
-//   M = max m_s;  out = sum_s 2^(m_s - M) v*_s / sum_s 2^(m_s - M) s*_s.
-// One CTA of 8 warps per (b,h): the max by a block reduction, then warp w folds splits
-// w, w+8, ... (lanes own dims lane + 32 i, 4 independent loads in flight per lane), then
-// the 8 warp results are combined. mode 0: out (dtype); mode 1: the merged triple with m in
-// natural-log units (m_nat = m ln 2) for the cross-GPU merge.
-constexpr int kMergeWarps = 8;
-__global__ void __launch_bounds__(kMergeWarps * 32) sq_merge_kernel(const float* __restrict__ part, int splits,
-                                                                    int d, int mode, void* out, int out_f32,
-                                                                    float* m_out, float* s_out, float* v_out) {
-  // PDL: everything above this point may overlap the tail of the partial kernel.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int bh = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const float* base = part + (size_t)bh * splits * (d + 2);
-  __shared__ float sm_red[kMergeWarps], sm_l[kMergeWarps], sm_a[kMergeWarps][128];
-  float M = -INFINITY;
-  for (int s = threadIdx.x; s < splits; s += blockDim.x) M = fmaxf(M, base[(size_t)s * (d + 2)]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  if (lane == 0) sm_red[warp] = M;
   __syncthreads();
-  M = sm_red[0];
-#pragma unroll
-  for (int w = 1; w < kMergeWarps; ++w) M = fmaxf(M, sm_red[w]);
-  float l = 0.f, a[4] = {0.f, 0.f, 0.f, 0.f};
-  if (M != -INFINITY) {
-    // 16 splits per warp per round, all loads issued before any use (latency-bound otherwise)
-    for (int s0 = warp; s0 < splits; s0 += 16 * kMergeWarps) {
-      float mw[16], lw[16], vw[16][4];
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int s = s0 + u * kMergeWarps;
-        const bool ok = s < splits;
-        const float* ps = base + (size_t)(ok ? s : 0) * (d + 2);
-        mw[u] = ok ? ps[0] : -INFINITY;
-        lw[u] = ok ? ps[1] : 0.f;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) vw[u][i] = (ok && lane + 32 * i < d) ? ps[2 + lane + 32 * i] : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const float w = exp2f(mw[u] - M);
-        l = fmaf(w, lw[u], l);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = fmaf(w, vw[u][i], a[i]);
-      }
-    }
-  }
-  if (lane == 0) sm_l[warp] = l;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (lane + 32 * i < d) sm_a[warp][lane + 32 * i] = a[i];
-  __syncthreads();
-  for (int f = threadIdx.x; f < d; f += blockDim.x) {
-    float L = 0.f, A = 0.f;
-#pragma unroll
-    for (int w = 0; w < kMergeWarps; ++w) {
-      L += sm_l[w];
-      A += sm_a[w][f];
-    }
-    if (mode == 0) {
-      const float r = A / L;
-      if (out_f32) static_cast<float*>(out)[(size_t)bh * d + f] = r;
-      else static_cast<__nv_bfloat16*>(out)[(size_t)bh * d + f] = __float2bfloat16_rn(r);
-    } else {
-      if (f == 0) {
-        m_out[bh] = M * 0.6931471805599453f;
-        s_out[bh] = L;
-      }
-      v_out[(size_t)bh * d + f] = A;
-    }
-  }
+  finish_cta<kF32Threads>(p, bh, split, bh, 1, d, sm_a);
 }
 
 // Cross-rank merge: P triples with natural-log m. One warp per row (a (b,h)
 // of a single query, or a (b, query, h) row of self-attention), lanes over the d features.
+// Triple i of row r: m at m[(i*rows + r) * ms], s at s[...], v* at vstar[(i*rows + r) * vs + f]
+// (separate arrays: ms = 1, vs = d; packed records {v*[d], m, s, pad, pad}: ms = vs = d + 4).
 __global__ void merge_partials_kernel(const float* __restrict__ m, const float* __restrict__ s,
-                                      const float* __restrict__ vstar, int P, int64_t rows, int d, void* out,
-                                      int out_f32) {
+                                      const float* __restrict__ vstar, int64_t ms, int64_t vs, int P, int64_t rows,
+                                      int d, void* out, int out_f32) {
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
   float M = -INFINITY;
-  for (int i = 0; i < P; ++i) M = fmaxf(M, m[(size_t)i * rows + r]);
+  for (int i = 0; i < P; ++i) M = fmaxf(M, m[((size_t)i * rows + r) * ms]);
   float L = 0.f, A[4] = {0.f, 0.f, 0.f, 0.f};
   for (int i = 0; i < P; ++i) {
-    const float mi = m[(size_t)i * rows + r];
+    const float mi = m[((size_t)i * rows + r) * ms];
     const float w = (mi == -INFINITY) ? 0.f : expf(mi - M);
-    L += w * s[(size_t)i * rows + r];
-    const float* vi = vstar + ((size_t)i * rows + r) * d;
+    L += w * s[((size_t)i * rows + r) * ms];
+    const float* vi = vstar + ((size_t)i * rows + r) * vs;
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if (lane + 32 * j < d) A[j] += w * vi[lane + 32 * j];
@@ -358,58 +415,88 @@ __global__ void merge_partials_kernel(const float* __restrict__ m, const float* 
   }
 }
 
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+std::atomic<unsigned long long> g_tag{0};
+
 }  // namespace
 
-// Splits: one 512-thread CTA per SM streaming (HBM needs ~35 KB in flight per SM; a CTA has
-// 256 KB in flight), at least ~1024 keys per split, so the merge stays small.
-int sq_num_splits(int64_t BH, int64_t n_k) {
-  const int64_t target_ctas = MEA_SQ_CTAS;
-  int64_t splits = (target_ctas + BH - 1) / BH;
+// Plan: heads per CTA (HC) and key splits. HC = the largest power of two <= 16 dividing H (a
+// CTA then streams HC adjacent rows per key); splits so that the grid fills the SMs (one
+// 512-thread CTA per SM keeps ~128 KB of loads in flight, HBM needs ~50 KB per SM), with at
+// least ~1024 keys per split.
+SqPlan sq_plan(int64_t B, int64_t H, int64_t n_k, int64_t d, int bf16) {
+  SqPlan pl{};
+  int hc = 1;
+  if (bf16) {
+    const int lim = d == 128 ? 8 : 16;   // the merge scratch bounds HC * d (sq_bf16_kernel)
+    const int cap = g_sq_heads_per_cta > 0 ? (g_sq_heads_per_cta < lim ? g_sq_heads_per_cta : lim) : lim;
+    while (hc * 2 <= cap && H % (hc * 2) == 0) hc *= 2;
+  }
+  pl.hc = hc;
+  const int64_t groups = B * H / hc;
+  const int64_t per_sm = g_sq_ctas_per_sm > 0 ? g_sq_ctas_per_sm : 1;
+  const int64_t target = (bf16 ? per_sm * num_sms() : 4 * num_sms());
+  int64_t splits = (target + groups - 1) / groups;
   const int64_t max_by_keys = (n_k + 1023) / 1024;
   if (splits > max_by_keys) splits = max_by_keys;
   if (splits < 1) splits = 1;
   if (splits > 4096) splits = 4096;
-  return (int)splits;
+  pl.splits = (int)splits;
+  pl.groups = groups;
+  pl.rec_bytes = ((size_t)B * H * splits * (d + 2) * sizeof(float) + 255) & ~(size_t)255;
+  pl.bytes = pl.rec_bytes + (size_t)groups * splits * sizeof(unsigned long long);
+  return pl;
 }
 
-cudaError_t launch_sq_partial(const void* q, const void* k, const void* v, int bf16, int B, int H, int n_k, int d,
-                              float scale, int splits, float* ws, cudaStream_t s) {
-  const float c = scale * 1.4426950408889634f;
-  dim3 grid(splits, B * H);
-  if (bf16 && d == 128) {
-    sq_partial_bf16_kernel<128><<<grid, kSqThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(q),
-                                                           static_cast<const __nv_bfloat16*>(k),
-                                                           static_cast<const __nv_bfloat16*>(v), H, n_k, c, splits, ws);
-  } else if (bf16) {
-    sq_partial_bf16_kernel<64><<<grid, kSqThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(q),
-                                                          static_cast<const __nv_bfloat16*>(k),
-                                                          static_cast<const __nv_bfloat16*>(v), H, n_k, c, splits, ws);
-  } else {
-    sq_partial_f32_kernel<<<grid, 128, 0, s>>>(static_cast<const float*>(q), static_cast<const float*>(k),
-                                               static_cast<const float*>(v), H, n_k, d, c, splits, ws);
+cudaError_t launch_sq(SqParams p, const SqPlan& pl, int bf16, cudaStream_t s) {
+  // a tag unique to this call: a per-process counter started from a hashed clock, so a workspace
+  // reused from another process (same address) cannot carry a matching stale flag
+  static const unsigned long long base =
+      (unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count() * 0x9E3779B97F4A7C15ull;
+  p.tag = base + g_tag.fetch_add(1, std::memory_order_relaxed);
+  p.splits = pl.splits;
+  p.tickets = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(p.rec) + pl.rec_bytes);
+  if (!bf16) {
+    sq_f32_kernel<<<dim3(pl.splits, (unsigned)(p.B * p.H)), kF32Threads, 0, s>>>(p);
+    return cudaGetLastError();
   }
+  const dim3 grid(pl.splits, (unsigned)pl.groups);
+#define MEA_SQ_LAUNCH(D, HC)                                                         \
+  do {                                                                               \
+    if (g_sq_l2_256) sq_bf16_kernel<D, HC, true><<<grid, kSqThreads, 0, s>>>(p);     \
+    else sq_bf16_kernel<D, HC, false><<<grid, kSqThreads, 0, s>>>(p);                \
+  } while (0)
+  if (p.d == 64) {
+    switch (pl.hc) {
+      case 1: MEA_SQ_LAUNCH(64, 1); break;
+      case 2: MEA_SQ_LAUNCH(64, 2); break;
+      case 4: MEA_SQ_LAUNCH(64, 4); break;
+      case 8: MEA_SQ_LAUNCH(64, 8); break;
+      default: MEA_SQ_LAUNCH(64, 16); break;
+    }
+  } else {
+    switch (pl.hc) {
+      case 1: MEA_SQ_LAUNCH(128, 1); break;
+      case 2: MEA_SQ_LAUNCH(128, 2); break;
+      case 4: MEA_SQ_LAUNCH(128, 4); break;
+      default: MEA_SQ_LAUNCH(128, 8); break;
+    }
+  }
+#undef MEA_SQ_LAUNCH
   return cudaGetLastError();
 }
 
-cudaError_t launch_sq_merge(const float* ws, int splits, int BH, int d, int mode, void* out, int out_f32, float* m,
-                            float* sum, float* vstar, cudaStream_t s) {
-  // Programmatic dependent launch: the merge grid is scheduled while the partial kernel
-  // drains and waits (griddepcontrol.wait) for its results, hiding the launch gap.
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(BH);
-  cfg.blockDim = dim3(kMergeWarps * 32);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, sq_merge_kernel, ws, splits, d, mode, out, out_f32, m, sum, vstar);
-}
-
-cudaError_t launch_merge_partials(const float* m, const float* s, const float* vstar, int P, int64_t rows, int d,
-                                  void* out, int out_f32, cudaStream_t st) {
-  merge_partials_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(m, s, vstar, P, rows, d, out, out_f32);
+cudaError_t launch_merge_partials(const float* m, const float* s, const float* vstar, int64_t ms, int64_t vs, int P,
+                                  int64_t rows, int d, void* out, int out_f32, cudaStream_t st) {
+  merge_partials_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(m, s, vstar, ms, vs, P, rows, d, out, out_f32);
   return cudaGetLastError();
 }
 

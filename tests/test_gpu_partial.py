@@ -116,3 +116,40 @@ def test_partial_large_rows_sampled():
         qr = gen.rows_of((B, n, H, d), 0, gen.TENSOR_Q, 0, rows, h)
         ref, _ = O.naive(qr, kk[0, :, h], vv[0, :, h], 1 / math.sqrt(d))
         Hh.assert_close_bf16(out[0, rows, h].double().cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_packed_partials_merge_to_full_attention(d):
+    """Packed records {v*, m, s} (the all-gather layout): self-attention over ragged key ranges,
+    one empty, and single-query ranges, merged by mea_merge_triples == the oracle."""
+    from paper_2112_05682_b200 import api
+    B, n_q, n_k, H = 2, 150, 900, 2
+    q, k, v = Hh.host_inputs(B, n_q, n_k, H, d, seed=25)
+    scale = 1 / math.sqrt(d)
+    ref, _ = O.mha_forward(q, k, v, scale)
+    qd = Hh.to_dev(q, torch.bfloat16)
+    cuts = [0, 300, 300, n_k]
+    recs = torch.stack([api.mea_attention_partial_fwd_packed(qd, Hh.to_dev(k[:, a:b], torch.bfloat16),
+                                                             Hh.to_dev(v[:, a:b], torch.bfloat16), scale=scale)
+                        for a, b in zip(cuts[:-1], cuts[1:])])
+    assert recs.shape == (3, B * n_q * H, d + 4)
+    assert torch.isinf(recs[1, :, d]).all() and (recs[1, :, d + 1] == 0).all() and (recs[1, :, :d] == 0).all()
+    out = api.mea_merge_triples(recs, out_dtype=torch.float32).reshape(B, n_q, H, d)
+    torch.cuda.synchronize()
+    Hh.assert_close_bf16(out.double().cpu().numpy(), ref)
+    # the unpacked triple of one range carries the same numbers
+    m, s, vs = api.mea_attention_partial_fwd(qd, Hh.to_dev(k[:, 300:], torch.bfloat16),
+                                             Hh.to_dev(v[:, 300:], torch.bfloat16), scale=scale)
+    torch.cuda.synchronize()
+    assert torch.equal(recs[2, :, d], m.reshape(-1)) and torch.equal(recs[2, :, d + 1], s.reshape(-1))
+    assert torch.equal(recs[2, :, :d], vs.reshape(-1, d))
+    # single query: packed per-(b, h) records over key ranges
+    qs = qd[:, 0].contiguous()
+    srecs = torch.stack([api.mea_single_query_partial_packed(qs, Hh.to_dev(k[:, a:b], torch.bfloat16),
+                                                             Hh.to_dev(v[:, a:b], torch.bfloat16), scale=scale)
+                         for a, b in zip(cuts[:-1], cuts[1:])])
+    sout = api.mea_merge_triples(srecs, out_dtype=torch.float32).reshape(B, H, d)
+    torch.cuda.synchronize()
+    sref = np.stack([[O.naive(q[b, 0, h][None], k[b, :, h], v[b, :, h], scale)[0][0] for h in range(H)]
+                     for b in range(B)])
+    Hh.assert_close_bf16(sout.double().cpu().numpy(), sref)

@@ -135,3 +135,31 @@ def test_single_query_exact_cases(n_k):
             assert np.abs(got - mean).max() <= 1e-6 + 1e-5 * np.abs(mean).max()
         else:
             Hh.assert_close_bf16(got, mean)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_single_query_head_blocks_and_split_counts(d):
+    """Every heads-per-CTA variant (adjacent head rows streamed by one CTA) and several CTA
+    counts give the oracle's result; repeated calls on one uninitialised workspace (stale
+    arrival tickets) stay correct."""
+    from paper_2112_05682_b200 import api
+    B, H, n_k = 2, 16, 5000
+    q, k, v = _sq_inputs(B, H, n_k, d, seed=9)
+    ref = _ref(q, k, v, 1 / math.sqrt(d))
+    qd, kd, vd = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v))
+    try:
+        for hc in (1, 2, 4, 8, 16):
+            for cps in (1, 2):
+                api.debug_set_option("sq_heads_per_cta", hc)
+                api.debug_set_option("sq_ctas_per_sm", cps)
+                nb = api.mea_single_query_workspace_size(B, H, n_k, d, api.MEA_BF16)
+                ws = torch.full((nb,), 0xA5, dtype=torch.uint8, device="cuda")   # garbage tickets
+                for _ in range(3):
+                    out = api.mea_single_query_fwd(qd, kd, vd, out_dtype=torch.float32, workspace=ws)
+                    torch.cuda.synchronize()
+                    got = out.double().cpu().numpy()
+                    err = np.abs(got - ref)
+                    assert (err <= 1e-3 * np.abs(ref) + 1e-5).all(), f"hc={hc} cps={cps}: {err.max():.3e}"
+    finally:
+        api.debug_set_option("sq_heads_per_cta", 0)
+        api.debug_set_option("sq_ctas_per_sm", 0)
