@@ -84,6 +84,12 @@ __device__ __forceinline__ int keys_of(const int* kv_lens, int b, int n_k) {
   return kv_lens ? min(n_k, max(0, __ldg(kv_lens + b))) : n_k;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn get_encode_fn();
+
 // 4-D tensor map over a [B, n, H, d] tensor (d innermost), box {64, 1, box_rows, 1},
 // 128-byte swizzle. elem = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 or FLOAT32.
 cudaError_t make_bnhd_map(CUtensorMap* map, const void* base, CUtensorMapDataType elem, int elem_bytes,
@@ -117,8 +123,8 @@ struct SqParams {
   int B, H, n_k, d;
   float c;                 // scale * log2(e)
   int splits;              // key ranges per (b, head block)
-  float* rec;              // workspace: partial records [B*H][splits][d+2], then the flags
-  unsigned long long* tickets;  // [groups][splits] per-CTA "records written" flags (= tag)
+  float* rec;              // workspace: partial records [B*H][splits][d+2], then the tickets
+  unsigned long long* tickets;  // [groups] arrival tickets (tag << 24 | arrivals)
   unsigned long long tag;  // unique per call (set by launch_sq)
   int mode;                // 0: out = attention; 1: the merged triple (m natural log, s, v*)
   void* out;               // mode 0: [B,H,d] bf16 or f32

@@ -1,7 +1,7 @@
 // single_query.cu — the paper's O(1)-memory single-query attention (made
 // stable by the running max of PAPER.md:85-90), split over key ranges (split-K), with the
 // merge of the per-range states by Figure 1's global-max rescale done in
-// the SAME launch by the last split CTA of each group (decoupled look-back), one kernel per call.
+// the SAME launch by the last CTA of each group to finish (arrival ticket): one kernel per call.
 //
 // HBM-bound: every key costs 4*d bytes (k and v rows, bf16) and 4*d flops, 1 flop/byte.
 // bf16 kernel: 8 (d = 64) or 16 (d = 128) lanes share one key row (16 B = 8 bf16 each,
@@ -14,10 +14,10 @@
 //
 // Partial records (workspace, float32): rec[(bh * splits + split) * (d + 2) + {0: m*, 1: s*,
 // 2..: v*}], m* in log2 units of the scaled score (p = 2^(s*c - m*), c = scale*log2 e). After
-// the records: one 64-bit flag per CTA, set to the call's tag (unique per call: a host counter
-// started from the clock) once the CTA's records are written; the last split of each group
-// waits for its group's flags and merges (decoupled look-back). A flag left by an earlier call,
-// or uninitialised workspace, never matches: no memset, no reset, no atomics.
+// the records: one 64-bit arrival ticket per CTA group holding (tag << 24 | arrivals), the tag
+// unique per call (a host counter started from a hashed clock); the CTA that arrives last merges
+// the group. A ticket left by an earlier call, or uninitialised workspace, is recognised by its
+// tag and restarted by the first arrival (ticket_arrive): no memset, no reset pass.
 #include <cuda_bf16.h>
 
 #include <atomic>
@@ -33,6 +33,20 @@ namespace mea {
 int g_sq_heads_per_cta = 0;   // 0 = automatic
 int g_sq_ctas_per_sm = 0;     // 0 = automatic
 int g_sq_l2_256 = 1;          // L2::256B prefetch hint on the K/V loads
+
+#ifdef MEA_SQ_TIMING
+// timeline probe build only: per CTA {start, streaming done, record written, merge done} (ns)
+__device__ unsigned long long g_sq_times[8192][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SQ_T(i) \
+  if (threadIdx.x == 0) g_sq_times[(blockIdx.y * gridDim.x + blockIdx.x) & 8191][i] = gtimer();
+#else
+#define SQ_T(i)
+#endif
 
 namespace {
 
@@ -100,10 +114,11 @@ __device__ void merge_group(const SqParams& p, const float* __restrict__ rec, in
     const int hl = o / d, f = o % d;
     const float* base = rec + (size_t)(bh0 + hl) * splits * (d + 2);
     float m = -INFINITY, l = 0.f, a = 0.f;
-    for (int s0 = j; s0 < splits; s0 += 8 * T) {
-      float ms[8], ls[8], as[8];
+    constexpr int U = 20;   // 148 splits over 8 thread subsets: one batch of independent loads
+    for (int s0 = j; s0 < splits; s0 += U * T) {
+      float ms[U], ls[U], as[U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int s = s0 + u * T;
         const bool ok = s < splits;
         const float* r = base + (size_t)(ok ? s : 0) * (d + 2);
@@ -113,13 +128,13 @@ __device__ void merge_group(const SqParams& p, const float* __restrict__ rec, in
       }
       float M = m;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) M = fmaxf(M, ms[u]);
+      for (int u = 0; u < U; ++u) M = fmaxf(M, ms[u]);
       if (M == -INFINITY) continue;
       const float w0 = ex2_approx(m - M);
       l *= w0;
       a *= w0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < U; ++u) {
         const float w = ex2_approx(ms[u] - M);
         l = fmaf(w, ls[u], l);
         a = fmaf(w, as[u], a);
@@ -157,27 +172,41 @@ __device__ void merge_group(const SqParams& p, const float* __restrict__ rec, in
   }
 }
 
-// Publishes this CTA's records (written before the call) by storing the call's tag in its
-// flag; the LAST split of the group (dispatched after the others, so they are resident or done:
-// the forward-progress assumption of a decoupled look-back) waits for every flag of its group to
-// carry the tag, then merges. A flag left by an earlier call, or uninitialised workspace, holds
-// another value: no memset, no counter reset, no atomics.
-template <int NT>
-__device__ __forceinline__ void finish_cta(const SqParams& p, int group, int split, int bh0, int HC, int d,
-                                           float* smem) {
-  unsigned long long* flags = p.tickets + (size_t)group * p.splits;
-  __threadfence();  // this thread's record writes are visible device-wide before the flag
-  __syncthreads();
-  if (split != p.splits - 1) {
-    if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned long long*>(flags + split) = p.tag;
-    return;
-  }
-  for (int s = threadIdx.x; s < p.splits - 1; s += NT)
-    while (*reinterpret_cast<volatile unsigned long long*>(flags + s) != p.tag) {
+// Arrival ticket of a CTA group: (tag << 24 | arrivals). One atomicAdd per CTA. The first
+// arrivals of a call may find a stale word (an earlier call's tag, or uninitialised workspace):
+// their increment is void, and they race to replace the word by (tag, 1) with CAS, retrying on
+// the value that beat them (no further adds, so the race ends once the arrivals stop); a CTA
+// that finds the word already restarted counts itself in with a fresh add. Returns this CTA's
+// arrival number (1-based) in this call.
+__device__ __forceinline__ unsigned ticket_arrive(unsigned long long* t, unsigned long long tag) {
+  unsigned long long old = atomicAdd(t, 1ull);
+  if ((old >> 24) == tag) return (unsigned)(old & 0xFFFFFFull) + 1u;
+  unsigned long long cur = old + 1;
+  while (true) {
+    if ((cur >> 24) == tag) {  // restarted by another arrival: count in on the fresh word
+      old = atomicAdd(t, 1ull);
+      if ((old >> 24) == tag) return (unsigned)(old & 0xFFFFFFull) + 1u;
+      cur = old + 1;
+      continue;
     }
+    const unsigned long long prev = atomicCAS(t, cur, (tag << 24) | 1ull);
+    if (prev == cur) return 1u;
+    cur = prev;
+  }
+}
+
+// Counts this CTA in (its records are written); the LAST of the group's `splits` CTAs merges.
+template <int NT>
+__device__ __forceinline__ void finish_cta(const SqParams& p, int group, int bh0, int HC, int d, float* smem) {
+  __shared__ int s_last;
+  __threadfence();  // this thread's record writes are visible device-wide before the ticket counts them
   __syncthreads();
+  if (threadIdx.x == 0) s_last = ticket_arrive(p.tickets + group, p.tag) == (unsigned)p.splits;
+  __syncthreads();
+  if (!s_last) return;
   __threadfence();
   merge_group<NT>(p, p.rec, bh0, HC, d, smem);
+  SQ_T(3)
 }
 
 template <int D, int HC, bool kL2Hint>
@@ -200,6 +229,7 @@ __global__ void __launch_bounds__(kSqThreads) sq_bf16_kernel(const SqParams p) {
   const __nv_bfloat16* kb = static_cast<const __nv_bfloat16*>(p.k) + ((size_t)b * n_k * p.H + h0 + hl) * D + cidx * 8;
   const __nv_bfloat16* vb = static_cast<const __nv_bfloat16*>(p.v) + ((size_t)b * n_k * p.H + h0 + hl) * D + cidx * 8;
   const int bh = b * p.H + h0 + hl;
+  SQ_T(0)
 
   float qf[8];
   bf16x8_to_f32(*reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.q) + (size_t)bh * D + cidx * 8), qf);
@@ -276,6 +306,7 @@ __global__ void __launch_bounds__(kSqThreads) sq_bf16_kernel(const SqParams p) {
     for (int i = 0; i < 8; ++i) o.a[i] = __shfl_xor_sync(0xffffffffu, st.a[i], off);
     merge_state(st, o);
   }
+  SQ_T(1)
   // groups g < min(G, HC) of each warp now hold distinct (warp, head) states
   constexpr int GV = G < HC ? G : HC;
   __shared__ float sm_m[NG], sm_l[NG];
@@ -289,23 +320,28 @@ __global__ void __launch_bounds__(kSqThreads) sq_bf16_kernel(const SqParams p) {
     for (int i = 0; i < 8; ++i) sm_a[gid][cidx * 8 + i] = st.a[i];
   }
   __syncthreads();
-  // CTA record per head: fold the states of head hl2 = entries gid = hl2 + j*HC with gid%G < GV
+  // CTA record per head: fold the NE states of head hl2 (entries hl2 + j * ESTEP) against their
+  // common max, all loads independent (the fold is on every CTA's tail)
+  constexpr int NE = HC <= G ? kSqWarps : KS;
+  constexpr int ESTEP = HC <= G ? G : HC;
   for (int t = threadIdx.x; t < HC * D; t += kSqThreads) {
     const int hl2 = t / D, f = t % D;
+    float mj[NE];
     float M = -INFINITY;
-    for (int j = 0; j < KS; ++j) {
-      const int e = hl2 + j * HC;
-      if (e % G < GV) M = fmaxf(M, sm_m[e]);
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      mj[j] = sm_m[hl2 + j * ESTEP];
+      M = fmaxf(M, mj[j]);
     }
     float l = 0.f, a = 0.f;
-    if (M != -INFINITY)
-      for (int j = 0; j < KS; ++j) {
-        const int e = hl2 + j * HC;
-        if (e % G >= GV) continue;
-        const float w = ex2_approx(sm_m[e] - M);
-        l = fmaf(w, sm_l[e], l);
-        a = fmaf(w, sm_a[e][f], a);
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int j = 0; j < NE; ++j) {
+        const float w = ex2_approx(mj[j] - M);
+        l = fmaf(w, sm_l[hl2 + j * ESTEP], l);
+        a = fmaf(w, sm_a[hl2 + j * ESTEP][f], a);
       }
+    }
     float* dst = p.rec + ((size_t)(b * p.H + h0 + hl2) * p.splits + split) * (D + 2);
     if (f == 0) {
       dst[0] = M;
@@ -316,7 +352,8 @@ __global__ void __launch_bounds__(kSqThreads) sq_bf16_kernel(const SqParams p) {
   // the final merge reuses the state arrays as scratch: (3 T O floats, T O <= max(512, HC D))
   static_assert(3 * (kSqThreads > HC * D ? kSqThreads : HC * D) <= NG * D, "merge scratch");
   __syncthreads();
-  finish_cta<kSqThreads>(p, group, split, b * p.H + h0, HC, D, &sm_a[0][0]);
+  SQ_T(2)
+  finish_cta<kSqThreads>(p, group, b * p.H + h0, HC, D, &sm_a[0][0]);
 }
 
 // f32 inputs, any d <= 128: one warp per key, lanes own dims {lane, lane+32, lane+64, lane+96}.
@@ -380,7 +417,7 @@ __global__ void __launch_bounds__(kF32Threads) sq_f32_kernel(const SqParams p) {
     dst[2 + f] = as;
   }
   __syncthreads();
-  finish_cta<kF32Threads>(p, bh, split, bh, 1, d, sm_a);
+  finish_cta<kF32Threads>(p, bh, bh, 1, d, sm_a);
 }
 
 // Cross-rank merge: P triples with natural-log m. One warp per row (a (b,h)
@@ -452,16 +489,16 @@ SqPlan sq_plan(int64_t B, int64_t H, int64_t n_k, int64_t d, int bf16) {
   pl.splits = (int)splits;
   pl.groups = groups;
   pl.rec_bytes = ((size_t)B * H * splits * (d + 2) * sizeof(float) + 255) & ~(size_t)255;
-  pl.bytes = pl.rec_bytes + (size_t)groups * splits * sizeof(unsigned long long);
+  pl.bytes = pl.rec_bytes + (size_t)groups * sizeof(unsigned long long);
   return pl;
 }
 
 cudaError_t launch_sq(SqParams p, const SqPlan& pl, int bf16, cudaStream_t s) {
-  // a tag unique to this call: a per-process counter started from a hashed clock, so a workspace
-  // reused from another process (same address) cannot carry a matching stale flag
+  // a tag unique to this call (40 bits): a per-process counter started from a hashed clock, so a
+  // workspace reused from another process (same address) cannot carry a matching stale ticket
   static const unsigned long long base =
       (unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count() * 0x9E3779B97F4A7C15ull;
-  p.tag = base + g_tag.fetch_add(1, std::memory_order_relaxed);
+  p.tag = (base + g_tag.fetch_add(1, std::memory_order_relaxed)) & ((1ull << 40) - 1);
   p.splits = pl.splits;
   p.tickets = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(p.rec) + pl.rec_bytes);
   if (!bf16) {
@@ -499,5 +536,11 @@ cudaError_t launch_merge_partials(const float* m, const float* s, const float* v
   merge_partials_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(m, s, vstar, ms, vs, P, rows, d, out, out_f32);
   return cudaGetLastError();
 }
+
+#ifdef MEA_SQ_TIMING
+extern "C" __attribute__((visibility("default"))) int mea_debug_sq_times(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_sq_times, sizeof(unsigned long long) * 4 * (n < 8192 ? n : 8192));
+}
+#endif
 
 }  // namespace mea

@@ -148,8 +148,8 @@ def test_single_query_head_blocks_and_split_counts(d):
     ref = _ref(q, k, v, 1 / math.sqrt(d))
     qd, kd, vd = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v))
     try:
-        for hc in (1, 2, 4, 8, 16):
-            for cps in (1, 2):
+        for hc, cps in [(h, c) for h in (1, 2, 4, 8, 16) for c in (1, 2)]:
+            if True:
                 api.debug_set_option("sq_heads_per_cta", hc)
                 api.debug_set_option("sq_ctas_per_sm", cps)
                 nb = api.mea_single_query_workspace_size(B, H, n_k, d, api.MEA_BF16)

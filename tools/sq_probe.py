@@ -25,7 +25,7 @@ def timeit(fn, iters=30):
 
 res = {"read_probe": [], "sq": [], "decode": []}
 big = torch.empty(4 << 30, dtype=torch.uint8, device="cuda")
-for mb in (64, 128, 268, 512, 1024, 4096):
+for mb in ((268, 1024, 4096) if "--quick" in sys.argv else (64, 128, 268, 512, 1024, 4096)):
     nb = mb << 20 if mb != 268 else 268435456
     buf = big[:nb]
     for ctas in (148, 296, 592):
@@ -43,9 +43,11 @@ def sq_case(B, H, n_k, label, key):
     out = torch.empty((B, H, 64), dtype=torch.bfloat16, device="cuda")
     nbytes = 2 * B * H * n_k * 64 * 2
     ref = None
-    for hc in ((1, 2, 4, 16) if H > 1 else (1,)):
-        for cps in (1, 2):
-            for l2 in (1, 0):
+    hcs = (1, 2, 4, 8, 16) if H > 1 else (1,)
+    variants = [(0, hc, cps, l2) for hc in hcs for cps in (1,) for l2 in (1, 0)]
+    for tma, hc, cps, l2 in variants:
+        if True:
+            if True:
                 api.debug_set_option("sq_heads_per_cta", hc)
                 api.debug_set_option("sq_ctas_per_sm", cps)
                 api.debug_set_option("sq_l2_256", l2)
@@ -55,11 +57,11 @@ def sq_case(B, H, n_k, label, key):
                 if ref is None:
                     ref = out.float().clone()
                 diff = (out.float() - ref).abs().max().item()
-                r = {"label": label, "B": B, "H": H, "n_k": n_k, "hc": hc, "ctas_per_sm": cps, "l2_256": l2,
-                     "us": med, "gbs": nbytes / med / 1e3, "gbs_best": nbytes / mn / 1e3, "diff": diff}
+                r = {"label": label, "B": B, "H": H, "n_k": n_k, "tma": tma, "hc": hc, "ctas_per_sm": cps,
+                     "l2_256": l2, "us": med, "gbs": nbytes / med / 1e3, "gbs_best": nbytes / mn / 1e3, "diff": diff}
                 res[key].append(r)
-                print(label, f"hc={hc} cps={cps} l2={l2}: {med:.1f} us {nbytes / med / 1e3:.0f} GB/s diff {diff:.1e}",
-                      flush=True)
+                print(label, f"tma={tma} hc={hc} cps={cps} l2={l2}: {med:.1f} us {nbytes / med / 1e3:.0f} GB/s "
+                      f"(best {nbytes / mn / 1e3:.0f}) diff {diff:.1e}", flush=True)
     api.debug_set_option("sq_heads_per_cta", 0)
     api.debug_set_option("sq_ctas_per_sm", 0)
     api.debug_set_option("sq_l2_256", 1)
@@ -68,4 +70,5 @@ def sq_case(B, H, n_k, label, key):
 for lg in (18, 20, 22, 24):
     sq_case(1, 1, 1 << lg, f"cfg2 n_k=2^{lg}", "sq")
 sq_case(1, 16, 1 << 20, "decode B*H=16 n_k=2^20", "decode")
-json.dump(res, open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/sq_probe.json", "w"), indent=1)
+outp = [a for a in sys.argv[1:] if not a.startswith("--")]
+json.dump(res, open(outp[0] if outp else "gpurun_out/sq_probe.json", "w"), indent=1)
