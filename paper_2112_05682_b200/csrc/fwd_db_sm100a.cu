@@ -22,6 +22,11 @@
 //
 // Warp roles: 0 TMA producer (Q0, Q1 once; kStages-deep K/V ring of 96-row tiles), 1 / 3 MMA
 // issuers for query tile 0 / 1, 2 TMEM allocator, 4-19 softmax (as fwd_sm100a.cu).
+//
+// kStats = true is the backward's statistics pass B0 (the forward's
+// statistics recomputed when they were not saved): the same row max / row sum of exponentials
+// over Q K^T, but no V stream, no P store, no P V product and no output: only lse is written.
+// Without P V the issuer refills a score buffer as soon as the softmax has read it.
 #include <cuda_bf16.h>
 
 #include "internal.h"
@@ -61,7 +66,7 @@ struct DbSmem {
   uint64_t kv_full[kStages];
   uint64_t kv_empty[kStages];
   uint64_t s_full[2][2];  // [query tile][buffer]
-  uint64_t p_full[2];
+  uint64_t p_full[2][2];  // [query tile][tile parity]: an arrival for tile t+1 never lands in tile t's phase
   uint64_t pv_done[2];
   uint64_t o_done[2];
   uint32_t tmem_base;
@@ -72,6 +77,7 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
 
+template <bool kStats>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_db_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const FwdParams p) {
@@ -102,7 +108,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.s_full[i][0], 1);
       mbar_init(&sm.s_full[i][1], 1);
-      mbar_init(&sm.p_full[i], 256);
+      mbar_init(&sm.p_full[i][0], 256);
+      mbar_init(&sm.p_full[i][1], 256);
       mbar_init(&sm.pv_done[i], 1);
       mbar_init(&sm.o_done[i], 1);
     }
@@ -134,9 +141,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int st = t % kStages;
         if (t >= kStages) mbar_wait(&sm.kv_empty[st], ((t / kStages) - 1) & 1);
         if (elect_one()) {
-          mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kKVTileBytes);
+          mbar_arrive_expect_tx(&sm.kv_full[st], (kStats ? 1 : 2) * kKVTileBytes);
           tma_load_4d(sm.k[st], &mk, &sm.kv_full[st], 0, h, t * kN, b, keep);
-          tma_load_4d(sm.v[st], &mv, &sm.kv_full[st], 0, h, t * kN, b, keep);
+          if (!kStats) tma_load_4d(sm.v[st], &mv, &sm.kv_full[st], 0, h, t * kN, b, keep);
         }
         __syncwarp();
       }
@@ -181,8 +188,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       // as soon as the last softmax warp has stored P_t, without burning issue slots and power on
       // long waits (vs try_wait: -2 % at full clocks; vs pure polling: -0.7 % at full clocks and
       // -1 % under the sustained power cap, measured).
-      for (int t = 0; t < Tq; ++t) {
-        mbar_poll_wait<32>(&sm.p_full[qt], t & 1);
+      if (kStats) {
+        // scores only: K_t is released when QK_t completes; S_{t+2} refills S_t's buffer as soon
+        // as the softmax has read S_t into registers (p_full)
+        for (int t = 0; t < Tq; ++t) {
+          if (elect_one()) umma_commit(&sm.kv_empty[t % kStages]);   // tracks QK_t (issued above)
+          __syncwarp();
+          mbar_poll_wait<32>(&sm.p_full[qt][t & 1], (t >> 1) & 1);
+          if (t + 2 < Tq) {
+            mbar_poll_wait<32>(&sm.kv_full[(t + 2) % kStages], ((t + 2) / kStages) & 1);
+            tc_fence_after();
+            if (elect_one()) qk(t + 2);
+            __syncwarp();
+          }
+        }
+      }
+      for (int t = 0; t < (kStats ? 0 : Tq); ++t) {
+        mbar_poll_wait<32>(&sm.p_full[qt][t & 1], (t >> 1) & 1);
         IPROBE(0)
         tc_fence_after();
         if (elect_one()) {
@@ -255,6 +277,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       TPROBE(0)
       tmem_ld_wait();
       TPROBE(1)
+      if (kStats) {  // S_t is in registers: its buffer may be refilled
+        tc_fence_before();
+        mbar_arrive(&sm.p_full[qt][t & 1]);
+      }
 #ifdef MEA_EXP_TIMING
       if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && t >= 8 && t < 12) {
         tdbg[1024 + (t - 8) * 32 + sw * 2 + 1] = clock64();
@@ -308,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_ref = m_cand;
           l *= alpha;
         }
-        if (t > 0 && __any_sync(0xffffffffu, need)) {
+        if (!kStats && t > 0 && __any_sync(0xffffffffu, need)) {
           // v* <- v* alpha once PV_{t-1} has finished (lanes 0-15: O columns [0,32), 16-31: [32,64))
           mbar_wait(&sm.pv_done[qt], (t - 1) & 1);
           tc_fence_after();
@@ -343,12 +369,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         load_s(t + 1);
       }
       TPROBE(2)
-      const uint32_t pa = lane_base + col_s(qt, t & 1);
-      tmem_st16_split<24>(pa, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
-      tmem_st8_split<24>(pa + 16, *reinterpret_cast<uint32_t(*)[8]>(&pk[16]));
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(&sm.p_full[qt]);
+      if (!kStats) {
+        const uint32_t pa = lane_base + col_s(qt, t & 1);
+        tmem_st16_split<24>(pa, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+        tmem_st8_split<24>(pa + 16, *reinterpret_cast<uint32_t(*)[8]>(&pk[16]));
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&sm.p_full[qt][t & 1]);
+      }
       TPROBE(5)
 #ifdef MEA_EXP_TIMING
       if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && t >= 8 && t < 12) {
@@ -358,6 +386,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // ------------------------------------------------------------ epilogue: out = v*/s*
     const float lrow = l + __shfl_xor_sync(0xffffffffu, l, 16);
+    if (kStats) {
+      if (row < q_end && half == 0)
+        p.lse[((size_t)b * p.H + h) * p.n_q + row] = (m_ref + __log2f(lrow)) * 0.6931471805599453f;
+    } else {
     mbar_wait(&sm.o_done[qt], 0);
     tc_fence_after();
     uint32_t o[32];
@@ -389,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.lse && half == 0) p.lse[bh * p.n_q + row] = (m_ref + __log2f(lrow)) * 0.6931471805599453f;
 #endif
     }
+    }  // !kStats
   }
   tc_fence_before();
   __syncthreads();
@@ -404,10 +437,16 @@ int fwd_db_key_tile() { return kN; }
 
 cudaError_t launch_fwd_db_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                                const CUtensorMap& mv, cudaStream_t s) {
-  const cudaError_t attr = ensure_smem_attr<fwd_db_kernel>((int)kDbSmemBytes);
-  if (attr != cudaSuccess) return attr;
   const dim3 grid = p.causal ? dim3(p.num_q_blocks * p.H * p.B) : dim3(p.num_q_blocks, p.H, p.B);
-  fwd_db_kernel<<<grid, kThreads, kDbSmemBytes, s>>>(mq, mk, mv, p);
+  if (p.stats_only) {
+    const cudaError_t attr = ensure_smem_attr<fwd_db_kernel<true>>((int)kDbSmemBytes);
+    if (attr != cudaSuccess) return attr;
+    fwd_db_kernel<true><<<grid, kThreads, kDbSmemBytes, s>>>(mq, mk, mv, p);
+  } else {
+    const cudaError_t attr = ensure_smem_attr<fwd_db_kernel<false>>((int)kDbSmemBytes);
+    if (attr != cudaSuccess) return attr;
+    fwd_db_kernel<false><<<grid, kThreads, kDbSmemBytes, s>>>(mq, mk, mv, p);
+  }
   return cudaGetLastError();
 }
 

@@ -60,6 +60,7 @@ struct FwdParams {
                            // (griddepcontrol.wait) only before its first global write
   const int* kv_lens;      // [B] keys per batch element (key padding: keys >= kv_lens[b] masked);
                            // nullable; online schedule only (no causal mask, no key split)
+  int stats_only;          // B0 (fwd_db, d = 64): row statistics only — lse written, no V, no out
 };
 
 struct BwdParams {

@@ -211,7 +211,8 @@ mea_status_t mea_attention_fwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
 static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* out, int64_t B, int64_t H,
                              int64_t n_q, int64_t n_k, int64_t d, mea_dtype_t in_dtype, mea_dtype_t out_dtype,
                              float scale, float* lse, int64_t q_chunk, int64_t k_chunk, void* workspace,
-                             size_t workspace_bytes, void* stream, bool causal, const int* kv_lens = nullptr) {
+                             size_t workspace_bytes, void* stream, bool causal, const int* kv_lens = nullptr,
+                             bool stats_only = false) {
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, scale)) return s;
   if (causal && n_q != n_k) return fail(MEA_ERR_UNSUPPORTED, "causal attention needs n_q == n_k");
   if (causal && in_dtype != MEA_BF16) return fail(MEA_ERR_UNSUPPORTED, "causal attention: bf16 path only");
@@ -224,7 +225,10 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
     return fail(MEA_ERR_UNSUPPORTED, "MEA_F32_SPLIT: d == 64, float32 output, no key chunks, not causal");
   if (n_q == 0) return MEA_OK;
   if (n_k == 0) return fail(MEA_ERR_EMPTY_KEYS, "attention over an empty key list");
-  if (!q || !k || !v || !out) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
+  // B0 (backward statistics pass): lse only, no output (d = 64 online schedule)
+  if (stats_only && (d != kHeadDim || in_dtype != MEA_BF16 || !lse || (k_chunk > 0 && k_chunk < n_k) || !MEA_FWD_DB))
+    return fail(MEA_ERR_UNSUPPORTED, "statistics pass: bf16, d = 64, online schedule, lse required");
+  if (!q || !k || !v || (!out && !stats_only)) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out))
     return fail(MEA_ERR_MISALIGNED, "q, k, v, out must be 16-byte aligned");
   if (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)) return fail(MEA_ERR_MISALIGNED, "lse must be 4-byte aligned");
@@ -323,6 +327,7 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
   p.lse = lse;
   p.causal = causal ? 1 : 0;
   p.kv_lens = kv_lens;
+  p.stats_only = stats_only ? 1 : 0;
   p.d = (int)d;
   p.num_splits = pl.splits;
   p.tiles_per_split = pl.tiles_per_split;
@@ -349,7 +354,7 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
       ProfScope ps("fwd128_bf16", st);
       if ((e = launch_fwd128_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd128_bf16 launch");
     } else if (use_db) {
-      ProfScope ps("fwd_bf16", st);
+      ProfScope ps(stats_only ? "bwd_stats" : "fwd_bf16", st);
       if ((e = launch_fwd_db_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_db_bf16 launch");
     } else {
       ProfScope ps("fwd_bf16", st);
@@ -751,9 +756,11 @@ BwdLayout bwd_layout(int64_t B, int64_t H, int64_t n_q, int64_t d, bool lse_give
     L.dq_acc = off; off = align256(off + (size_t)B * n_q * H * d * sizeof(float));
     L.aug = off;    off = align256(off + rows_pad / kTileM * 2 * kAugTileBytes);
   }
-  if (!lse_given) {
+  if (!lse_given) {  // B0: lse recomputed (d = 64: statistics pass, no output; d = 128: full forward)
     L.lse_tmp = off; off = align256(off + (size_t)B * H * n_q * sizeof(float));
-    L.out_tmp = off; off = align256(off + (size_t)B * n_q * H * d * 2);
+    if (d != kHeadDim) {
+      L.out_tmp = off; off = align256(off + (size_t)B * n_q * H * d * 2);
+    }
   }
   L.total = off;
   return L;
@@ -827,10 +834,13 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
     return cuda_fail(e, why);
 
   if (!lse) {
-    // B0: the statistics pass — rerun the forward for lse (its output goes to scratch).
+    // B0: the statistics pass. d = 64: Q K^T and the exponential row sums
+    // only (fwd_db_kernel<true>: no V, no P V, no output); d = 128: the forward rerun with its
+    // output in scratch.
     float* lse_tmp = reinterpret_cast<float*>(ws + L.lse_tmp);
-    mea_status_t r = fwd_impl(q, k, v, ws + L.out_tmp, B, H, n_q, n_k, d, MEA_BF16, MEA_BF16, scale, lse_tmp, 0, 0,
-                              nullptr, 0, stream, causal, kv_lens);
+    const bool stats = d == kHeadDim;
+    mea_status_t r = fwd_impl(q, k, v, stats ? nullptr : ws + L.out_tmp, B, H, n_q, n_k, d, MEA_BF16, MEA_BF16, scale,
+                              lse_tmp, 0, 0, nullptr, 0, stream, causal, kv_lens, stats);
     if (r != MEA_OK) return r;
     lse = lse_tmp;
   }

@@ -167,3 +167,18 @@ def test_padded_entry_points_validate_on_the_host(lib):
     assert lib.mea_attention_bwd_padded(p, p, p, p, p, p, p, p, 1, 1, 8, 8, 64, 1, 1.0, None, None, None, 0, None) == 1
     assert lib.mea_attention_bwd_padded(p, p, p, p, p, p, p, p, 1, 1, 8, 8, 64, 0, 1.0, None, p, None, 0, None) == 3
     assert lib.mea_attention_bwd_padded(p, p, p, p, p, p, p, p, 1, 1, 8, 8, 64, 1, 1.0, None, p, p, 16, None) == 5
+
+
+def test_stats_pass_workspace_is_lse_only(lib):
+    """B0 (lse not given): at d = 64 the statistics pass writes lse only, so the
+    backward workspace grows by the lse buffer (4 B per query row) and no output-sized scratch;
+    d = 128 still reruns the forward (output in scratch)."""
+    B, H, n = 1, 16, 16384
+    for fn in (lib.mea_attention_bwd_workspace_size, lib.mea_attention_bwd_deterministic_workspace_size):
+        a, b = ctypes.c_size_t(0), ctypes.c_size_t(0)
+        assert fn(B, H, n, n, 64, 1, 1, ctypes.byref(a)) == 0
+        assert fn(B, H, n, n, 64, 1, 0, ctypes.byref(b)) == 0
+        assert b.value - a.value == B * H * n * 4
+        assert fn(B, H, n, n, 128, 1, 1, ctypes.byref(a)) == 0
+        assert fn(B, H, n, n, 128, 1, 0, ctypes.byref(b)) == 0
+        assert b.value - a.value == B * H * n * 4 + B * n * H * 128 * 2
