@@ -175,8 +175,9 @@ MEA_API mea_status_t mea_attention_fwd_padded(const void* q, const void* k, cons
  * workspace and the last CTA of each (b, head block) merges them with Figure 1's
  * global-max rescale in the same launch. Workspace (>= 8-byte aligned,
  * mea_single_query_workspace_size bytes) is independent of n_k (bounded by the split count);
- * its contents need no initialisation and are scratch between calls (the arrival tickets
- * carry a per-call tag). Calls sharing one workspace must be stream-ordered.
+ * its contents need no initialisation (counters left by a call are reset by that call;
+ * uninitialised ones are recognised and restarted). Calls sharing one workspace must be
+ * stream-ordered.
  */
 MEA_API mea_status_t mea_single_query_fwd(const void* q, const void* k, const void* v, void* out,
                                   int64_t B, int64_t H, int64_t n_k, int64_t d,

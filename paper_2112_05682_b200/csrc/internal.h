@@ -125,8 +125,7 @@ struct SqParams {
   float c;                 // scale * log2(e)
   int splits;              // key ranges per (b, head block)
   float* rec;              // workspace: partial records [B*H][splits][d+2], then the tickets
-  unsigned long long* tickets;  // [groups] arrival tickets (tag << 24 | arrivals)
-  unsigned long long tag;  // unique per call (set by launch_sq)
+  unsigned long long* tickets;  // [groups] arrival tickets (single_query.cu counter_take)
   int mode;                // 0: out = attention; 1: the merged triple (m natural log, s, v*)
   void* out;               // mode 0: [B,H,d] bf16 or f32
   int out_f32;

@@ -14,10 +14,9 @@
 //
 // Partial records (workspace, float32): rec[(bh * splits + split) * (d + 2) + {0: m*, 1: s*,
 // 2..: v*}], m* in log2 units of the scaled score (p = 2^(s*c - m*), c = scale*log2 e). After
-// the records: one 64-bit arrival ticket per CTA group holding (tag << 24 | arrivals), the tag
-// unique per call (a host counter started from a hashed clock); the CTA that arrives last merges
-// the group. A ticket left by an earlier call, or uninitialised workspace, is recognised by its
-// tag and restarted by the first arrival (ticket_arrive): no memset, no reset pass.
+// the records: per CTA group (b, head block) a 64-bit arrival ticket (counter_take: the merging
+// CTA leaves it reset for the next call; uninitialised workspace is recognised and restarted by
+// the first arrivals): no memset, no extra launch.
 #include <cuda_bf16.h>
 
 #include <atomic>
@@ -172,40 +171,46 @@ __device__ void merge_group(const SqParams& p, const float* __restrict__ rec, in
   }
 }
 
-// Arrival ticket of a CTA group: (tag << 24 | arrivals). One atomicAdd per CTA. The first
-// arrivals of a call may find a stale word (an earlier call's tag, or uninitialised workspace):
-// their increment is void, and they race to replace the word by (tag, 1) with CAS, retrying on
-// the value that beat them (no further adds, so the race ends once the arrivals stop); a CTA
-// that finds the word already restarted counts itself in with a fresh add. Returns this CTA's
-// arrival number (1-based) in this call.
-__device__ __forceinline__ unsigned ticket_arrive(unsigned long long* t, unsigned long long tag) {
+// The arrival ticket of a CTA group in the workspace is a 64-bit word (kClean << 24 | count).
+// The CTA that merges a group resets it to (kClean, 0) at the
+// end of the call, so the next call on the same workspace counts from 0 with plain atomicAdds.
+// A word with another tag (uninitialised workspace, first use) is stale: its first users' adds
+// are void and they race to replace it by (kClean, 1) with CAS, retrying on the value that beat
+// them (no further adds, so the race ends once the first users stop); a user that finds the word
+// already restarted counts itself in with a fresh add. Returns the 0-based count this user took.
+constexpr unsigned long long kClean = 0xC1EA5ED5A1ull;   // 40-bit marker of a reset counter
+__device__ __forceinline__ unsigned counter_take(unsigned long long* t) {
   unsigned long long old = atomicAdd(t, 1ull);
-  if ((old >> 24) == tag) return (unsigned)(old & 0xFFFFFFull) + 1u;
+  if ((old >> 24) == kClean) return (unsigned)(old & 0xFFFFFFull);
   unsigned long long cur = old + 1;
   while (true) {
-    if ((cur >> 24) == tag) {  // restarted by another arrival: count in on the fresh word
+    if ((cur >> 24) == kClean) {  // restarted by another user: count in on the fresh word
       old = atomicAdd(t, 1ull);
-      if ((old >> 24) == tag) return (unsigned)(old & 0xFFFFFFull) + 1u;
+      if ((old >> 24) == kClean) return (unsigned)(old & 0xFFFFFFull);
       cur = old + 1;
       continue;
     }
-    const unsigned long long prev = atomicCAS(t, cur, (tag << 24) | 1ull);
-    if (prev == cur) return 1u;
+    const unsigned long long prev = atomicCAS(t, cur, (kClean << 24) | 1ull);
+    if (prev == cur) return 0u;
     cur = prev;
   }
 }
 
-// Counts this CTA in (its records are written); the LAST of the group's `splits` CTAs merges.
+// Counts this CTA in (its records are written); the LAST of the group's `splits` CTAs merges and
+// resets the group's ticket for the next call.
 template <int NT>
 __device__ __forceinline__ void finish_cta(const SqParams& p, int group, int bh0, int HC, int d, float* smem) {
   __shared__ int s_last;
   __threadfence();  // this thread's record writes are visible device-wide before the ticket counts them
   __syncthreads();
-  if (threadIdx.x == 0) s_last = ticket_arrive(p.tickets + group, p.tag) == (unsigned)p.splits;
+  if (threadIdx.x == 0) s_last = counter_take(p.tickets + group) + 1 == (unsigned)p.splits;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
   merge_group<NT>(p, p.rec, bh0, HC, d, smem);
+  if (threadIdx.x == 0) {   // every CTA of the group has arrived
+    p.tickets[group] = kClean << 24;
+  }
   SQ_T(3)
 }
 
@@ -242,59 +247,67 @@ __global__ void __launch_bounds__(kSqThreads) sq_bf16_kernel(const SqParams p) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) st.a[i] = 0.f;
 
-  // the trip count must be warp-uniform (the shuffles below take the full mask): the loop runs
-  // while the warp's first key slot has keys left; other slots mask their keys individually
-  const int ks_warp = (warp * G) / HC;
-  for (int base0 = k_lo; base0 + ks_warp < k_hi; base0 += kStep * kUnroll) {
-    const int base = base0 + ks;
-    uint4 kr[kUnroll][4], vr[kUnroll][4];
+  // Per-group stream update over 4 keys x kUnroll steps per iteration (one rescale per 4 keys),
+  // the CTA streaming its static key range [k_lo, k_hi). (Measured and rejected: warps claiming
+  // 16 KiB chunks from a per-group counter to balance SMs that stream at different rates — the
+  // claims' latency under load made it 1.3-1.45x slower at 2^22-2^24 keys and for the decode batch.)
+  constexpr int KW = KS;                             // key slots per CTA
+  constexpr int kWStep = 4 * KW;                     // keys per step
+  const int kslot = ks;
+  auto run_keys = [&](int lo, int hi, int base_first) {
+    // the trip count must be warp-uniform (the shuffles below take the full mask)
+    for (int base0 = lo; base0 + base_first < hi; base0 += kWStep * kUnroll) {
+      const int base = base0 + kslot;
+      uint4 kr[kUnroll][4], vr[kUnroll][4];
 #pragma unroll
-    for (int s = 0; s < kUnroll; ++s)
+      for (int s = 0; s < kUnroll; ++s)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int key = base + s * kStep + u * KS;
-        if (key < k_hi) {
-          kr[s][u] = ld_stream<kL2Hint>(kb + (size_t)key * row_stride);
-          vr[s][u] = ld_stream<kL2Hint>(vb + (size_t)key * row_stride);
-        } else {
-          kr[s][u] = make_uint4(0, 0, 0, 0);
-          vr[s][u] = make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < 4; ++u) {
+          const int key = base + s * kWStep + u * KW;
+          if (key < hi) {
+            kr[s][u] = ld_stream<kL2Hint>(kb + (size_t)key * row_stride);
+            vr[s][u] = ld_stream<kL2Hint>(vb + (size_t)key * row_stride);
+          } else {
+            kr[s][u] = make_uint4(0, 0, 0, 0);
+            vr[s][u] = make_uint4(0, 0, 0, 0);
+          }
         }
+#pragma unroll
+      for (int s = 0; s < kUnroll; ++s) {
+        float sc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float kf[8];
+          bf16x8_to_f32(kr[s][u], kf);
+          float dot = 0.f;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) dot = fmaf(qf[i], kf[i], dot);
+#pragma unroll
+          for (int o = 1; o < LPR; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+          const int key = base + s * kWStep + u * KW;
+          sc[u] = key < hi ? dot : -INFINITY;
+        }
+        const float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+        const float m_new = fmaxf(st.m, mx);
+        if (m_new == -INFINITY) continue;  // nothing valid yet for this group
+        const float alpha = ex2_approx(st.m - m_new);
+        st.l *= alpha;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) st.a[i] *= alpha;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float pu = ex2_approx(sc[u] - m_new);
+          st.l += pu;
+          float vf[8];
+          bf16x8_to_f32(vr[s][u], vf);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) st.a[i] = fmaf(pu, vf[i], st.a[i]);
+        }
+        st.m = m_new;
       }
-#pragma unroll
-    for (int s = 0; s < kUnroll; ++s) {
-      float sc[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float kf[8];
-        bf16x8_to_f32(kr[s][u], kf);
-        float dot = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) dot = fmaf(qf[i], kf[i], dot);
-#pragma unroll
-        for (int o = 1; o < LPR; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        const int key = base + s * kStep + u * KS;
-        sc[u] = key < k_hi ? dot : -INFINITY;
-      }
-      const float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
-      const float m_new = fmaxf(st.m, mx);
-      if (m_new == -INFINITY) continue;  // nothing valid yet for this group
-      const float alpha = ex2_approx(st.m - m_new);
-      st.l *= alpha;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) st.a[i] *= alpha;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float pu = ex2_approx(sc[u] - m_new);
-        st.l += pu;
-        float vf[8];
-        bf16x8_to_f32(vr[s][u], vf);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) st.a[i] = fmaf(pu, vf[i], st.a[i]);
-      }
-      st.m = m_new;
     }
-  }
+  };
+  run_keys(k_lo, k_hi, (warp * G) / HC);
   // merge the groups of the warp that share a head (group ids equal mod HC)
 #pragma unroll
   for (int gx = HC; gx < G; gx <<= 1) {
@@ -461,11 +474,11 @@ int num_sms() {
   return n;
 }
 
-std::atomic<unsigned long long> g_tag{0};
+
 
 }  // namespace
 
-// Plan: heads per CTA (HC) and key splits. HC = the largest power of two <= 16 dividing H (a
+// Plan: heads per CTA (HC) and key splits. HC = the largest power of two <= 4 dividing H (a
 // CTA then streams HC adjacent rows per key); splits so that the grid fills the SMs (one
 // 512-thread CTA per SM keeps ~128 KB of loads in flight, HBM needs ~50 KB per SM), with at
 // least ~1024 keys per split.
@@ -473,8 +486,11 @@ SqPlan sq_plan(int64_t B, int64_t H, int64_t n_k, int64_t d, int bf16) {
   SqPlan pl{};
   int hc = 1;
   if (bf16) {
-    const int lim = d == 128 ? 8 : 16;   // the merge scratch bounds HC * d (sq_bf16_kernel)
-    const int cap = g_sq_heads_per_cta > 0 ? (g_sq_heads_per_cta < lim ? g_sq_heads_per_cta : lim) : lim;
+    // 4 adjacent head rows per key (512 B contiguous at d = 64) measured best for a decode batch
+    // (16 heads x 2^20 keys: 7.0-7.2 TB/s vs 6.9 at 8 or 16 and 4.0-4.5 head-strided); the
+    // merge scratch bounds HC * d (sq_bf16_kernel)
+    const int lim = d == 128 ? 8 : 16;
+    const int cap = g_sq_heads_per_cta > 0 ? (g_sq_heads_per_cta < lim ? g_sq_heads_per_cta : lim) : 4;
     while (hc * 2 <= cap && H % (hc * 2) == 0) hc *= 2;
   }
   pl.hc = hc;
@@ -494,11 +510,6 @@ SqPlan sq_plan(int64_t B, int64_t H, int64_t n_k, int64_t d, int bf16) {
 }
 
 cudaError_t launch_sq(SqParams p, const SqPlan& pl, int bf16, cudaStream_t s) {
-  // a tag unique to this call (40 bits): a per-process counter started from a hashed clock, so a
-  // workspace reused from another process (same address) cannot carry a matching stale ticket
-  static const unsigned long long base =
-      (unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count() * 0x9E3779B97F4A7C15ull;
-  p.tag = (base + g_tag.fetch_add(1, std::memory_order_relaxed)) & ((1ull << 40) - 1);
   p.splits = pl.splits;
   p.tickets = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(p.rec) + pl.rec_bytes);
   if (!bf16) {
