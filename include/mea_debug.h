@@ -28,7 +28,8 @@ MEA_API mea_status_t mea_profile_read(char* buf, size_t cap);
 
 /*
  * Experiment knobs (A/B measurements without a rebuild; defaults are the shipped design):
- *   "sq_heads_per_cta" (0 = auto), "sq_ctas_per_sm" (0 = auto), "sq_l2_256" (1 = L2::256B hint).
+ *   "sq_heads_per_cta" (0 = auto), "sq_ctas_per_sm" (0 = auto), "sq_l2_256" (1 = L2::256B hint),
+ *   "sq_static_pct" (percent of the keys in static per-CTA ranges, the rest a dynamic pool; 100 = all static, -1 = auto).
  */
 MEA_API mea_status_t mea_debug_set_option(const char* name, int value);
 

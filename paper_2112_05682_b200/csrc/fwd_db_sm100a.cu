@@ -218,7 +218,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (t + 2 < Tq) {
           // S_{t+2} goes into the buffer P_t occupies: wait until PV_t has read it
           mbar_poll_wait<32>(&sm.kv_full[(t + 2) % kStages], ((t + 2) / kStages) & 1);
+#ifndef MEA_DB_NO_PV_WAIT
           mbar_poll_wait<32>(&sm.pv_done[qt], t & 1);
+#endif
           IPROBE(2)
           tc_fence_after();
           if (elect_one()) qk(t + 2);

@@ -126,6 +126,11 @@ struct SqParams {
   int splits;              // key ranges per (b, head block)
   float* rec;              // workspace: partial records [B*H][splits][d+2], then the tickets
   unsigned long long* tickets;  // [groups] arrival tickets (single_query.cu counter_take)
+  unsigned long long* claims;   // [groups] dynamic-pool claim counters (same tagged scheme)
+  int static_keys;         // keys of each split's static range (pool mode: split * static_keys ...)
+  int chunk_keys;          // keys per pool chunk (one CTA step)
+  int pool_begin;          // first key of the dynamic pool (= splits * static_keys)
+  int pool_chunks;         // chunks in the pool (0: static ranges only)
   int mode;                // 0: out = attention; 1: the merged triple (m natural log, s, v*)
   void* out;               // mode 0: [B,H,d] bf16 or f32
   int out_f32;
@@ -134,12 +139,13 @@ struct SqParams {
 };
 struct SqPlan {
   int hc, splits;
+  int static_keys, chunk_keys, pool_begin, pool_chunks;
   int64_t groups;
   size_t rec_bytes, bytes;
 };
 SqPlan sq_plan(int64_t B, int64_t H, int64_t n_k, int64_t d, int bf16);
 cudaError_t launch_sq(SqParams p, const SqPlan& pl, int bf16, cudaStream_t s);
-extern int g_sq_heads_per_cta, g_sq_ctas_per_sm, g_sq_l2_256;
+extern int g_sq_heads_per_cta, g_sq_ctas_per_sm, g_sq_l2_256, g_sq_static_pct;
 // m at m[(i*rows + r)*ms], s likewise, v* at vstar[(i*rows + r)*vs + f]
 cudaError_t launch_merge_partials(const float* m, const float* s, const float* vstar, int64_t ms, int64_t vs, int P,
                                   int64_t rows, int d, void* out, int out_f32, cudaStream_t st);

@@ -1024,6 +1024,7 @@ mea_status_t mea_debug_set_option(const char* name, int value) {
   if (n == "sq_heads_per_cta") mea::g_sq_heads_per_cta = value;
   else if (n == "sq_ctas_per_sm") mea::g_sq_ctas_per_sm = value;
   else if (n == "sq_l2_256") mea::g_sq_l2_256 = value;
+  else if (n == "sq_static_pct") mea::g_sq_static_pct = value;
   else return fail(MEA_ERR_INVALID_VALUE, "unknown option");
   return MEA_OK;
 }

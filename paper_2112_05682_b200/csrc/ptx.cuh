@@ -330,6 +330,9 @@ __device__ __forceinline__ void setmaxnreg_dec() {
 #endif
 }
 
+// gpu-scope acquire-release fence (cumulative over writes ordered before it, e.g. by bar.sync)
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -32,6 +32,7 @@ namespace mea {
 int g_sq_heads_per_cta = 0;   // 0 = automatic
 int g_sq_ctas_per_sm = 0;     // 0 = automatic
 int g_sq_l2_256 = 1;          // L2::256B prefetch hint on the K/V loads
+int g_sq_static_pct = -1;     // keys in static per-CTA ranges (%), the rest a dynamic pool (-1: auto)
 
 #ifdef MEA_SQ_TIMING
 // timeline probe build only: per CTA {start, streaming done, record written, merge done} (ns)
@@ -179,9 +180,8 @@ __device__ void merge_group(const SqParams& p, const float* __restrict__ rec, in
 // them (no further adds, so the race ends once the first users stop); a user that finds the word
 // already restarted counts itself in with a fresh add. Returns the 0-based count this user took.
 constexpr unsigned long long kClean = 0xC1EA5ED5A1ull;   // 40-bit marker of a reset counter
-__device__ __forceinline__ unsigned counter_take(unsigned long long* t) {
-  unsigned long long old = atomicAdd(t, 1ull);
-  if ((old >> 24) == kClean) return (unsigned)(old & 0xFFFFFFull);
+// completes a take whose first atomicAdd returned `old`
+__device__ __noinline__ unsigned counter_take_slow(unsigned long long* t, unsigned long long old) {
   unsigned long long cur = old + 1;
   while (true) {
     if ((cur >> 24) == kClean) {  // restarted by another user: count in on the fresh word
@@ -195,21 +195,35 @@ __device__ __forceinline__ unsigned counter_take(unsigned long long* t) {
     cur = prev;
   }
 }
+__device__ __forceinline__ unsigned counter_finish(unsigned long long* t, unsigned long long old) {
+  if ((old >> 24) == kClean) return (unsigned)(old & 0xFFFFFFull);
+  return counter_take_slow(t, old);
+}
+__device__ __forceinline__ unsigned counter_take(unsigned long long* t) {
+  return counter_finish(t, atomicAdd(t, 1ull));
+}
 
 // Counts this CTA in (its records are written); the LAST of the group's `splits` CTAs merges and
 // resets the group's ticket for the next call.
 template <int NT>
 __device__ __forceinline__ void finish_cta(const SqParams& p, int group, int bh0, int HC, int d, float* smem) {
   __shared__ int s_last;
-  __threadfence();  // this thread's record writes are visible device-wide before the ticket counts them
+  // release: the CTA's record writes (ordered before thread 0 by the barrier) become visible
+  // device-wide before the ticket counts them (fence.acq_rel is cumulative); acquire on the
+  // last arrival before anyone reads the other CTAs' records
   __syncthreads();
-  if (threadIdx.x == 0) s_last = counter_take(p.tickets + group) + 1 == (unsigned)p.splits;
+  if (threadIdx.x == 0) {
+    fence_acq_rel_gpu();
+    const bool last = counter_take(p.tickets + group) + 1 == (unsigned)p.splits;
+    if (last) fence_acq_rel_gpu();
+    s_last = last;
+  }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   merge_group<NT>(p, p.rec, bh0, HC, d, smem);
-  if (threadIdx.x == 0) {   // every CTA of the group has arrived
+  if (threadIdx.x == 0) {   // every CTA of the group has arrived (and made its last claim)
     p.tickets[group] = kClean << 24;
+    if (p.claims) p.claims[group] = kClean << 24;
   }
   SQ_T(3)
 }
@@ -228,7 +242,11 @@ __global__ void __launch_bounds__(kSqThreads) sq_bf16_kernel(const SqParams p) {
   const int gid = warp * G + g;               // group in the CTA
   const int hl = gid % HC, ks = gid / HC;     // its head (of the block) and key slot
   const int n_k = p.n_k;
-  const int per = (n_k + p.splits - 1) / p.splits;
+  // static range of this split; with a pool, the keys past splits * static_keys are handed out
+  // in CTA-step chunks to whichever CTA of the group asks first (balances SMs that stream at
+  // different rates: measured 34-41 us per static 1/148 of configs[1])
+  const bool pool = p.pool_chunks > 0;
+  const int per = pool ? p.static_keys : (n_k + p.splits - 1) / p.splits;
   const int k_lo = split * per, k_hi = min(n_k, k_lo + per);
   const size_t row_stride = (size_t)p.H * D;  // elements between consecutive keys
   const __nv_bfloat16* kb = static_cast<const __nv_bfloat16*>(p.k) + ((size_t)b * n_k * p.H + h0 + hl) * D + cidx * 8;
@@ -307,7 +325,48 @@ __global__ void __launch_bounds__(kSqThreads) sq_bf16_kernel(const SqParams p) {
       }
     }
   };
-  run_keys(k_lo, k_hi, (warp * G) / HC);
+  // Pool claims: thread 0 takes chunks two ahead of use (the atomics' latency hides under a
+  // chunk of streaming) and publishes chunk i in a ring slot tagged with i; every warp walks the
+  // ring on its own (no CTA barrier between chunks).
+  constexpr int kRing = 32;
+  __shared__ unsigned long long s_ring[kRing];
+  unsigned long long* const claims = p.claims + group;
+  unsigned long long a0 = 0, a1 = 0;
+  if (pool) {
+    for (int t = threadIdx.x; t < kRing; t += kSqThreads) s_ring[t] = ~0ull;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a0 = atomicAdd(claims, 1ull);
+      a1 = atomicAdd(claims, 1ull);
+    }
+  }
+  const int base_first = (warp * G) / HC;
+  run_keys(k_lo, k_hi, base_first);
+  if (pool) {
+    auto publish = [&](int i, unsigned long long raw) {
+      const unsigned c = counter_finish(claims, raw);
+      const unsigned long long v = ((unsigned long long)i << 32) | (c < (unsigned)p.pool_chunks ? c : 0xFFFFFFFFu);
+      *reinterpret_cast<volatile unsigned long long*>(&s_ring[i % kRing]) = v;
+    };
+    if (threadIdx.x == 0) {
+      publish(0, a0);
+      publish(1, a1);
+    }
+    for (int i = 0;; ++i) {
+      unsigned long long v;
+      do {
+        v = *reinterpret_cast<volatile unsigned long long*>(&s_ring[i % kRing]);
+      } while (v == ~0ull || (int)(v >> 32) < i);
+      if ((int)(v >> 32) != i) __trap();  // the ring lapped a warp (cannot happen at kRing >> 2)
+      const unsigned c = (unsigned)v;
+      if (c == 0xFFFFFFFFu) break;       // pool exhausted (later slots are never read)
+      unsigned long long an = 0;
+      if (threadIdx.x == 0) an = atomicAdd(claims, 1ull);
+      const int lo = p.pool_begin + (int)c * p.chunk_keys;
+      run_keys(lo, min(n_k, lo + p.chunk_keys), base_first);
+      if (threadIdx.x == 0) publish(i + 2, an);
+    }
+  }
   // merge the groups of the warp that share a head (group ids equal mod HC)
 #pragma unroll
   for (int gx = HC; gx < G; gx <<= 1) {
@@ -497,21 +556,57 @@ SqPlan sq_plan(int64_t B, int64_t H, int64_t n_k, int64_t d, int bf16) {
   const int64_t groups = B * H / hc;
   const int64_t per_sm = g_sq_ctas_per_sm > 0 ? g_sq_ctas_per_sm : 1;
   const int64_t target = (bf16 ? per_sm * num_sms() : 4 * num_sms());
-  int64_t splits = (target + groups - 1) / groups;
+  // one wave: the largest split count whose grid fits the SMs, when that still fills >= 85 % of
+  // them; otherwise (e.g. 100 groups on 148 SMs) more splits than fit, balanced by the pool below
+  int64_t splits = target / groups;
+  bool overfull = false;
+  if (splits < 1 || groups * splits < target * 85 / 100) {
+    splits = (target + groups - 1) / groups;
+    overfull = groups * splits > target;
+  }
   const int64_t max_by_keys = (n_k + 1023) / 1024;
   if (splits > max_by_keys) splits = max_by_keys;
   if (splits < 1) splits = 1;
   if (splits > 4096) splits = 4096;
   pl.splits = (int)splits;
   pl.groups = groups;
+  // dynamic pool (bf16): chunks of one CTA step (4 keys x kUnroll per key slot, NG / hc slots);
+  // each split keeps g_sq_static_pct % of its share as a static range; only when every split
+  // still has >= 2 static chunks and the pool has >= 1 chunk per split
+  pl.static_keys = 0;
+  pl.chunk_keys = 0;
+  pl.pool_begin = 0;
+  pl.pool_chunks = 0;
+  // static share: the knob, else 100 % for a single wave (a pool measured no faster there:
+  // the SMs share one HBM, a fast SM does not steal bandwidth from a slow one) and 0 % when the
+  // grid overfills the SMs (late CTAs find the pool drained instead of adding a second wave)
+  const int pct = g_sq_static_pct >= 0 ? g_sq_static_pct : (overfull ? 0 : 100);
+  if (bf16 && pct < 100) {
+    const int64_t ng = (int64_t)kSqWarps * (32 / (d / 8));
+    const int64_t chunk = 4 * (ng / hc) * kUnroll;
+    const int64_t total = (n_k + chunk - 1) / chunk;
+    const int64_t sc = total * pct / 100 / splits;
+    const int64_t pool = total - sc * splits;
+    if ((sc >= 2 || pct == 0) && pool >= splits) {
+      pl.chunk_keys = (int)chunk;
+      pl.static_keys = (int)(sc * chunk);
+      pl.pool_begin = (int)(sc * chunk * splits);
+      pl.pool_chunks = (int)((n_k - pl.pool_begin + chunk - 1) / chunk);
+    }
+  }
   pl.rec_bytes = ((size_t)B * H * splits * (d + 2) * sizeof(float) + 255) & ~(size_t)255;
-  pl.bytes = pl.rec_bytes + (size_t)groups * sizeof(unsigned long long);
+  pl.bytes = pl.rec_bytes + 2 * (size_t)groups * sizeof(unsigned long long);   // tickets, claims
   return pl;
 }
 
 cudaError_t launch_sq(SqParams p, const SqPlan& pl, int bf16, cudaStream_t s) {
   p.splits = pl.splits;
   p.tickets = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(p.rec) + pl.rec_bytes);
+  p.claims = pl.pool_chunks > 0 ? p.tickets + pl.groups : nullptr;
+  p.static_keys = pl.static_keys;
+  p.chunk_keys = pl.chunk_keys;
+  p.pool_begin = pl.pool_begin;
+  p.pool_chunks = pl.pool_chunks;
   if (!bf16) {
     sq_f32_kernel<<<dim3(pl.splits, (unsigned)(p.B * p.H)), kF32Threads, 0, s>>>(p);
     return cudaGetLastError();
