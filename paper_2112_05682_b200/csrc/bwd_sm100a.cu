@@ -318,12 +318,15 @@ __global__ void __launch_bounds__(kBThreads, 1)
       if (i > 0) mbar_wait(&sm.p_free, (i - 1) & 1);  // tile i-1's MMAs no longer read P / dS
       TPROBE(3)
       tmem_st16(lane_base + kColP + g * 16, pk);
+      TPROBE(5)
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
         const int phys = (chunk0 + cc) ^ (j & 7);
         *reinterpret_cast<uint4*>(ds_row + phys * 16) = make_uint4(dk[4 * cc], dk[4 * cc + 1], dk[4 * cc + 2], dk[4 * cc + 3]);
       }
+      TPROBE(6)
       fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+      TPROBE(7)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm.p_full);

@@ -65,7 +65,7 @@ struct FwdParams {
 
 struct BwdParams {
   int B, H, n_q, n_k;
-  int d;                   // head dimension: 64, or 128 (two-kernel path only)
+  int d;                   // head dimension: 64 or 128
   float scale, scale_log2;
   const float* lse2;       // [B*H][nq_pad]: lse * log2(e), +inf in the padding
   const float* delta;      // [B*H][nq_pad]: dO_i . O_i, 0 in the padding
@@ -160,6 +160,9 @@ constexpr int kAugTileBytes = 4096;   // 128 rows x 16 bf16, no-swizzle K-major 
 cudaError_t launch_bwd_bf16(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                             const CUtensorMap& mdo, const CUtensorMap& mdq, cudaStream_t s);
 cudaError_t launch_dq_convert(const float* dq_acc, void* dq, int64_t numel, float scale, cudaStream_t s);
+// d = 128 fused backward (bwd128_sm100a.cu): mq / mdo boxes of 64 rows, mdq {32, 1, 64, 1} f32
+cudaError_t launch_bwd128(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                          const CUtensorMap& mdo, const CUtensorMap& mdq, cudaStream_t s);
 cudaError_t launch_bwd_dkdv(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
                             const CUtensorMap& mdo, cudaStream_t s);
 cudaError_t launch_bwd_dq(const BwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,

@@ -752,9 +752,11 @@ BwdLayout bwd_layout(int64_t B, int64_t H, int64_t n_q, int64_t d, bool lse_give
   size_t off = 0;
   L.delta = off;  off = align256(off + rows_pad * sizeof(float));
   L.lse2 = off;   off = align256(off + rows_pad * sizeof(float));
-  if (fused) {  // the fused kernel's dQ reduction target and its score K-extension tiles
+  if (fused) {  // the fused kernel's dQ reduction target (+ at d = 64 its score K-extension tiles)
     L.dq_acc = off; off = align256(off + (size_t)B * n_q * H * d * sizeof(float));
-    L.aug = off;    off = align256(off + rows_pad / kTileM * 2 * kAugTileBytes);
+    if (d == kHeadDim) {
+      L.aug = off;  off = align256(off + rows_pad / kTileM * 2 * kAugTileBytes);
+    }
   }
   if (!lse_given) {  // B0: lse recomputed (d = 64: statistics pass, no output; d = 128: full forward)
     L.lse_tmp = off; off = align256(off + (size_t)B * H * n_q * sizeof(float));
@@ -772,7 +774,7 @@ mea_status_t mea_attention_bwd_workspace_size(int64_t B, int64_t H, int64_t n_q,
   if (!bytes) return fail(MEA_ERR_INVALID_VALUE, "bytes is NULL");
   if (mea_status_t s = check_common(B, H, n_q, n_k, d, 1.f)) return s;
   if (!valid_dtype(dtype)) return fail(MEA_ERR_INVALID_VALUE, "bad dtype");
-  *bytes = bwd_layout(B, H, n_q, d, lse_given != 0, d == kHeadDim).total;  // d = 128: two-kernel path
+  *bytes = bwd_layout(B, H, n_q, d, lse_given != 0, true).total;  // the fused path (d = 64 and 128)
   return MEA_OK;
 }
 
@@ -800,10 +802,10 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
     return MEA_OK;
   }
   if (!q || !out || !dout || !dq) return fail(MEA_ERR_INVALID_VALUE, "NULL tensor pointer");
-  // The fused kernel folds lse/scale into its score MMA; scale == 0 (all scores 0, P uniform)
-  // takes the two-kernel path, whose workspace is a prefix-sized subset of the fused one.
-  if (fused && scale == 0.f) fused = false;
-  if (d == 128) fused = false;  // d = 128: the two-kernel path (the fused kernel's TMEM holds d = 64)
+  // The d = 64 fused kernel folds lse/scale into its score MMA; scale == 0 (all scores 0, P
+  // uniform) takes the two-kernel path, whose workspace is a prefix-sized subset of the fused one.
+  // The d = 128 fused kernel (bwd128_sm100a.cu) reads lse per column and takes any scale.
+  if (fused && scale == 0.f && d == kHeadDim) fused = false;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(dout) || !aligned16(dq) ||
       !aligned16(dk) || !aligned16(dv))
     return fail(MEA_ERR_MISALIGNED, "tensors must be 16-byte aligned");
@@ -817,7 +819,7 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   float* delta = reinterpret_cast<float*>(ws + L.delta);
   float* lse2 = reinterpret_cast<float*>(ws + L.lse2);
   float* dq_acc = fused ? reinterpret_cast<float*>(ws + L.dq_acc) : nullptr;
-  uint8_t* aug = fused ? ws + L.aug : nullptr;
+  uint8_t* aug = fused && d == kHeadDim ? ws + L.aug : nullptr;
 
   CUtensorMap mq, mk, mv, mdo, mdq;
   const char* why = "";
@@ -829,8 +831,8 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
                          CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
       (e = make_bnhd_map(&mv, v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_k, H, d, 64, kTileN,
                          CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
-      (fused && (e = make_bnhd_map(&mdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, n_q, H, d, 32, kTileM,
-                                   CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess))
+      (fused && (e = make_bnhd_map(&mdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, n_q, H, d, 32,
+                                   d == kHeadDim ? kTileM : 64, CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess))
     return cuda_fail(e, why);
 
   if (!lse) {
@@ -869,7 +871,22 @@ static mea_status_t bwd_impl(const void* q, const void* k, const void* v, const 
   p.causal = causal ? 1 : 0;
   p.kv_lens = kv_lens;
   p.d = (int)d;
-  if (fused) {
+  if (fused && d == 128) {
+    // 64-query tiles (TMEM holds dV and dK at 128 columns each): Q / dO boxes of 64 rows
+    CUtensorMap mq_t, mdo_t;
+    if ((e = make_bnhd_map(&mq_t, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_q, H, d, 64, 64,
+                           CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess ||
+        (e = make_bnhd_map(&mdo_t, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, n_q, H, d, 64, 64,
+                           CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess)
+      return cuda_fail(e, why);
+    {
+      ProfScope ps("bwd128", st);
+      if ((e = launch_bwd128(p, mq_t, mk, mv, mdo_t, mdq, st)) != cudaSuccess) return cuda_fail(e, "bwd128 launch");
+    }
+    ProfScope ps("dq_convert", st);
+    if ((e = launch_dq_convert(dq_acc, dq, B * n_q * H * d, scale, st)) != cudaSuccess)
+      return cuda_fail(e, "dq_convert launch");
+  } else if (fused) {
     {
       ProfScope ps("bwd_bf16", st);
       if ((e = launch_bwd_bf16(p, mq, mk, mv, mdo, mdq, st)) != cudaSuccess) return cuda_fail(e, "bwd_bf16 launch");

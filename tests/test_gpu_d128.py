@@ -123,3 +123,21 @@ def test_d128_backward_sampled_rows_n4096():
         for got, ref, name in ((dq[0, qr, h], sq, "dq"), (dk[0, kr, h], sk, "dk"), (dv[0, kr, h], sv, "dv")):
             Hh.assert_close_bf16(got.double().cpu().numpy(), ref, abs_tol=Hh.TOL_BF16_GRAD,
                                  rel_tol=Hh.REL_NORM_GRAD, what=name)
+
+
+@pytest.mark.parametrize("scale", [0.0, 0.05, 0.3, -0.1])
+def test_d128_fused_backward_scales(scale):
+    """The fused d = 128 backward (bwd128_sm100a.cu: lse per column, any scale incl. 0 and
+    negative) against O6, next to the deterministic two-kernel path."""
+    from paper_2112_05682_b200 import api
+    q, k, v, do = Hh.host_inputs(1, 200, 300, 2, D, seed=46, with_dout=True)
+    dq_r, dk_r, dv_r = O.mha_backward(q, k, v, do, scale)
+    qd, kd, vd, dod = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v, do))
+    out, lse = api.mea_attention_fwd(qd, kd, vd, scale=scale, want_lse=True)
+    strict = abs(scale) <= 1 / math.sqrt(D)
+    for fn in (api.mea_attention_bwd, api.mea_attention_bwd_deterministic):
+        dq, dk, dv = fn(qd, kd, vd, out, dod, lse=lse, scale=scale)
+        torch.cuda.synchronize()
+        for got, ref, name in ((dq, dq_r, "dq"), (dk, dk_r, "dk"), (dv, dv_r, "dv")):
+            Hh.assert_close_bf16(got.double().cpu().numpy(), ref, abs_tol=Hh.TOL_BF16_GRAD * max(1.0, abs(scale) * math.sqrt(D)),
+                                 rel_tol=Hh.REL_NORM_GRAD, what=name, strict=strict)

@@ -26,6 +26,11 @@ for g in range(4):
         r = ts[g, i, :5] - base
         print(f"g{g} i={i+8}", " ".join(f"{x:7d}" for x in r), "| dt:", " ".join(f"{n}={x}" for n, x in zip(names, np.diff(r))))
 
+sub = ts[:, :, [3, 5, 6, 7, 4]]
+dd = np.diff(sub, axis=2).mean(axis=1)
+print("store phase split (p_free seen -> tmem_st issued -> STS done -> proxy fence done -> st_wait+arrive):")
+for g in range(4):
+    print(f"  g{g} " + " ".join(f"{x:.0f}" for x in dd[g]))
 print("softmax means over 16 tiles (cycles):")
 for g in range(4):
     dd = np.diff(ts[g, :, :5], axis=1).mean(axis=0)
