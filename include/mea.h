@@ -255,8 +255,10 @@ MEA_API mea_status_t mea_merge_triples(const float* triples, int64_t P, int64_t 
  * residual; NULL makes the call recompute it first (one extra statistics pass).
  * The max carries no gradient (stop_gradient).
  * Workspace: delta [B,H,n_q] f32 + dq accumulator [B,n_q,H,d] f32 (+ lse if NULL).
- * bf16 with d in {64, 128}; d = 128 (and scale == 0) runs the two-kernel path of
- * mea_attention_bwd_deterministic (the workspace asked for here covers it).
+ * bf16 with d in {64, 128}: one fused kernel per call at either d (dq reduced across key tiles
+ * in the f32 accumulator, so dq is reproducible only to rounding order; use
+ * mea_attention_bwd_deterministic for bitwise results); d = 64 with scale == 0 runs the
+ * two-kernel path of mea_attention_bwd_deterministic (the workspace asked for here covers it).
  */
 MEA_API mea_status_t mea_attention_bwd(const void* q, const void* k, const void* v, const void* out,
                                const void* dout, void* dq, void* dk, void* dv, int64_t B,
