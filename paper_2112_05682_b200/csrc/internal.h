@@ -112,7 +112,7 @@ cudaError_t launch_fwd_db_bf16(const FwdParams& p, const CUtensorMap& mq, const 
 cudaError_t launch_fwd128_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                                const CUtensorMap& mv, cudaStream_t s);
 cudaError_t launch_split_f32(const float* x, void* const* parts, int nparts, int64_t n, cudaStream_t s);
-cudaError_t launch_fwd_f32tc(const FwdParams& p, const CUtensorMap (&maps)[8], cudaStream_t s);
+cudaError_t launch_fwd_f32tc(const FwdParams& p, const CUtensorMap (&maps)[9], cudaStream_t s);
 cudaError_t launch_empty_triples(float* m, float* s, float* vstar, int64_t ms, int64_t vs, int64_t rows, int d,
                                  cudaStream_t st);
 cudaError_t launch_fwd_f32(const float* q, const float* k, const float* v, float* out, float* lse, int B,

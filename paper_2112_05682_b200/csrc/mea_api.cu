@@ -156,9 +156,9 @@ FwdPlan plan_fwd(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t q_chunk
   return pl;
 }
 
-// f32 inputs at d = 64: bf16 parts of q, k (three each) and v (two): 6 + 6 + 4 bytes per element
+// f32 inputs at d = 64: three bf16 parts of q, k and v: 6 + 6 + 6 bytes per element
 size_t f32tc_workspace(int64_t B, int64_t H, int64_t n_q, int64_t n_k) {
-  return (size_t)B * H * kHeadDim * (6 * n_q + 10 * n_k);
+  return (size_t)B * H * kHeadDim * (6 * n_q + 12 * n_k);
 }
 
 mea_status_t check_common(int64_t B, int64_t H, int64_t n_q, int64_t n_k, int64_t d, float scale) {
@@ -239,30 +239,30 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
     if (out_dtype != MEA_F32) return fail(MEA_ERR_UNSUPPORTED, "f32 inputs need f32 output");
     if (k_chunk > 0 && k_chunk < n_k) return fail(MEA_ERR_UNSUPPORTED, "key chunking is a bf16-path schedule");
     if (in_dtype == MEA_F32_SPLIT) {
-      // split-precision tensor-core path (fwd_f32tc_sm100a.cu): q, k, v -> bf16 hi/lo in the workspace
+      // split-precision tensor-core path (fwd_f32tc_sm100a.cu): q, k, v -> three bf16 parts in the workspace
       const size_t need = f32tc_workspace(B, H, n_q, n_k);
       if (!workspace || workspace_bytes < need) return fail(MEA_ERR_WORKSPACE_TOO_SMALL, "f32 split workspace");
       if (!aligned16(workspace)) return fail(MEA_ERR_MISALIGNED, "workspace must be 16-byte aligned");
       uint8_t* w = static_cast<uint8_t*>(workspace);
       const size_t nq_el = (size_t)B * n_q * H * d, nk_el = (size_t)B * n_k * H * d;
-      // q, k: three bf16 parts each; v: two
+      // q, k, v: three bf16 parts each
       void* qp[3] = {w, w + nq_el * 2, w + nq_el * 4};
       uint8_t* wk = w + nq_el * 6;
       void* kp[3] = {wk, wk + nk_el * 2, wk + nk_el * 4};
       uint8_t* wv = wk + nk_el * 6;
-      void* vp[2] = {wv, wv + nk_el * 2};
+      void* vp[3] = {wv, wv + nk_el * 2, wv + nk_el * 4};
       cudaError_t e;
       {
         ProfScope ps("split_f32", st);
         if ((e = launch_split_f32(static_cast<const float*>(q), qp, 3, (int64_t)nq_el, st)) != cudaSuccess ||
             (e = launch_split_f32(static_cast<const float*>(k), kp, 3, (int64_t)nk_el, st)) != cudaSuccess ||
-            (e = launch_split_f32(static_cast<const float*>(v), vp, 2, (int64_t)nk_el, st)) != cudaSuccess)
+            (e = launch_split_f32(static_cast<const float*>(v), vp, 3, (int64_t)nk_el, st)) != cudaSuccess)
           return cuda_fail(e, "split_f32 launch");
       }
-      CUtensorMap maps[8];
+      CUtensorMap maps[9];
       const char* why = "";
-      const void* bases[8] = {qp[0], qp[1], qp[2], kp[0], kp[1], kp[2], vp[0], vp[1]};
-      for (int i = 0; i < 8; ++i)
+      const void* bases[9] = {qp[0], qp[1], qp[2], kp[0], kp[1], kp[2], vp[0], vp[1], vp[2]};
+      for (int i = 0; i < 9; ++i)
         if ((e = make_bnhd_map(&maps[i], bases[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, i < 3 ? n_q : n_k, H, d,
                                64, 128, CU_TENSOR_MAP_SWIZZLE_128B, &why)) != cudaSuccess)
           return cuda_fail(e, why);

@@ -141,3 +141,32 @@ def test_d128_fused_backward_scales(scale):
         for got, ref, name in ((dq, dq_r, "dq"), (dk, dk_r, "dk"), (dv, dv_r, "dv")):
             Hh.assert_close_bf16(got.double().cpu().numpy(), ref, abs_tol=Hh.TOL_BF16_GRAD * max(1.0, abs(scale) * math.sqrt(D)),
                                  rel_tol=Hh.REL_NORM_GRAD, what=name, strict=strict)
+
+
+def test_d128_full_size_sampled_rows_bench_config():
+    """The bench's d = 128 extras at configs[2]/[3] shape (B=1 H=16 n=16384 d=128 bf16, device-
+    generated inputs, the launch configuration bench.py times): forward and the fused backward
+    on sampled rows of 2 heads against O1 / O6."""
+    from paper_2112_05682_b200 import api
+    from synth import gen
+    B, n, H = 1, 16384, 16
+    shape = (B, n, H, D)
+    ts = [torch.empty(shape, dtype=torch.bfloat16, device="cuda") for _ in range(4)]
+    for t, tid in zip(ts, (gen.TENSOR_Q, gen.TENSOR_K, gen.TENSOR_V, gen.TENSOR_DO)):
+        api.mea_fill_synthetic(t, 0, tid)
+    q, k, v, do = ts
+    out, lse = api.mea_attention_fwd(q, k, v, want_lse=True)
+    dq, dk, dv = api.mea_attention_bwd(q, k, v, out, do, lse=lse)
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 63, 64, 127, 128, 8191, 16383])
+    scale = 1 / math.sqrt(D)
+    for h in (0, 9):
+        hq, hk, hv, hdo = (gen.rows_of(shape, 0, tid, 0, np.arange(n), h)
+                           for tid in (gen.TENSOR_Q, gen.TENSOR_K, gen.TENSOR_V, gen.TENSOR_DO))
+        ro, rl = O.naive(hq[rows], hk, hv, scale)
+        Hh.assert_close_bf16(out[0, rows, h].double().cpu().numpy(), ro)
+        assert np.abs(lse[0, h, rows].double().cpu().numpy() - rl).max() < 1e-3
+        rq, rk, rv = O.backward_rows(hq, hk, hv, hdo, scale, rows, rows)
+        Hh.assert_close_bf16(dq[0, rows, h].double().cpu().numpy(), rq, Hh.TOL_BF16_GRAD, Hh.REL_NORM_GRAD, "dq")
+        Hh.assert_close_bf16(dk[0, rows, h].double().cpu().numpy(), rk, Hh.TOL_BF16_GRAD, Hh.REL_NORM_GRAD, "dk")
+        Hh.assert_close_bf16(dv[0, rows, h].double().cpu().numpy(), rv, Hh.TOL_BF16_GRAD, Hh.REL_NORM_GRAD, "dv")
