@@ -46,10 +46,11 @@ constexpr int kControlRegs = 32;
 constexpr float kLazyThreshold = 8.0f;
 constexpr float kSafeSum = 18446744073709551616.0f;   // 2^64
 __host__ __device__ constexpr uint32_t col_s(int qt, int b) { return (uint32_t)((qt * 2 + b) * kN); }
-__host__ __device__ constexpr uint32_t col_p(int qt, int b) { return 256u + 32u * (qt * 2 + b); }
-__host__ __device__ constexpr uint32_t col_o(int qt) { return 384u + 64u * qt; }
+__host__ __device__ constexpr uint32_t col_p(int qt) { return 256u + 32u * qt; }
+__host__ __device__ constexpr uint32_t col_o(int qt) { return 320u + 64u * qt; }
+__host__ __device__ constexpr uint32_t col_q(int qt) { return 448u + 32u * qt; }
 
-constexpr uint32_t kIdescQK = idesc_bf16_f32(128, kN, false, false);   // A = Q, B = K, both K-major
+constexpr uint32_t kIdescQK = idesc_bf16_f32(128, kN, false, false);   // A = Q (TMEM), B = K K-major
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 64, false, true);    // A = P (TMEM), B = V MN-major
 
 #ifndef MEA_DB_POLY_MASK
@@ -65,12 +66,13 @@ struct DbSmem {
   uint8_t k[kStages][kKVTileBytes];
   uint8_t v[kStages][kKVTileBytes];
   uint64_t q_full;
+  uint64_t q_tmem[2];     // [query tile]: Q copied into TMEM (256 softmax threads)
   uint64_t kv_full[kStages];
   uint64_t kv_empty[kStages];
   uint64_t s_full[2][2];  // [query tile][buffer]: Q K_t^T done
   uint64_t s_free[2][2];  // [query tile][buffer]: the softmax has read S_t (256 threads)
-  uint64_t p_full[2][2];  // [query tile][P buffer]: P_t stored (256 threads)
-  uint64_t pv_done[2][2]; // [query tile][P buffer]: P_t V_t done
+  uint64_t p_full[2];     // P_t stored (256 threads)
+  uint64_t pv_done[2];
   uint64_t o_done[2];
   uint32_t tmem_base;
 };
@@ -109,14 +111,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.kv_empty[i], 2);  // one commit per query tile
     }
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.q_tmem[i], 256);
       mbar_init(&sm.s_full[i][0], 1);
       mbar_init(&sm.s_full[i][1], 1);
       mbar_init(&sm.s_free[i][0], 256);
       mbar_init(&sm.s_free[i][1], 256);
-      mbar_init(&sm.p_full[i][0], 256);
-      mbar_init(&sm.p_full[i][1], 256);
-      mbar_init(&sm.pv_done[i][0], 1);
-      mbar_init(&sm.pv_done[i][1], 1);
+      mbar_init(&sm.p_full[i], 256);
+      mbar_init(&sm.pv_done[i], 1);
       mbar_init(&sm.o_done[i], 1);
     }
     fence_barrier_init();
@@ -161,23 +162,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dv0 = shfl0_u64(sdesc_sw128(smem_u32(sm.v[0]), 16, 1024));
       constexpr uint64_t kStageStep = kKVTileBytes >> 4;
       const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
-      const uint64_t dq = shfl0_u64(sdesc_sw128(smem_u32(sm.q[qt]), 16, 1024));
-      const uint32_t to = tmem_u + col_o(qt);
-      auto qk = [&](int t) {  // S[qt][t & 1] = Q K_t^T
+      const uint32_t to = tmem_u + col_o(qt), tq = tmem_u + col_q(qt), tp = tmem_u + col_p(qt);
+      auto qk = [&](int t) {  // S[qt][t & 1] = Q K_t^T (A = Q from TMEM)
         const uint64_t dk = dk0 + (t % kStages) * kStageStep;
         const uint32_t ts = tmem_u + col_s(qt, t & 1);
 #pragma unroll
-        for (int kk = 0; kk < kHeadDim / 16; ++kk) umma_ss(ts, dq + kk * 2, dk + kk * 2, kIdescQK, kk > 0);
+        for (int kk = 0; kk < kHeadDim / 16; ++kk) umma_ts(ts, tq + kk * 8, dk + kk * 2, kIdescQK, kk > 0);
         umma_commit(&sm.s_full[qt][t & 1]);
       };
       auto pv = [&](int t) {  // O += P_t V_t
         const uint64_t dv = dv0 + (t % kStages) * kStageStep;
-        const uint32_t tp = tmem_u + col_p(qt, t & 1);
 #pragma unroll
         for (int kk = 0; kk < kN / 16; ++kk)
           umma_ts(to, tp + kk * 8, dv + kk * 128, kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
       };
-      IWAIT(&sm.q_full, 0);
+      IWAIT(&sm.q_tmem[qt], 0);
       for (int t = 0; t < 2 && t < Tq; ++t) {
         IWAIT(&sm.kv_full[t % kStages], (t / kStages) & 1);
         tc_fence_after();
@@ -207,14 +206,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           continue;
         }
-        IWAIT(&sm.p_full[qt][t & 1], (t >> 1) & 1);
+        IWAIT(&sm.p_full[qt], t & 1);
         IPROBE(2)
         tc_fence_after();
         IPROBE(5)
         if (elect_one()) {
           pv(t);
           umma_commit(&sm.kv_empty[t % kStages]);
-          umma_commit(&sm.pv_done[qt][t & 1]);
+          umma_commit(&sm.pv_done[qt]);
           if (t + 1 == Tq) umma_commit(&sm.o_done[qt]);
         }
         __syncwarp();
@@ -248,6 +247,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float c = p.scale_log2;
     float m_ref = -INFINITY;  // reference max m* (log2 units of the scaled score)
     float l = 0.f;            // this half's part of s*
+    {
+      // Q row rloc, d [32 half, 32 half + 32) -> TMEM Q columns [16 half, 16 half + 16): the
+      // 128B-swizzled TMA tile holds 16-byte chunk j of row r at chunk position j ^ (r & 7)
+      mbar_wait(&sm.q_full, 0);
+      const uint8_t* qrow = sm.q[qt] + (rloc >> 3) * 1024 + (rloc & 7) * 128;
+      uint32_t w[16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint4 x = *reinterpret_cast<const uint4*>(qrow + (((half * 4 + j) ^ (rloc & 7)) << 4));
+        w[4 * j] = x.x; w[4 * j + 1] = x.y; w[4 * j + 2] = x.z; w[4 * j + 3] = x.w;
+      }
+      tmem_st16_split<16>(lane_base + col_q(qt), w);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&sm.q_tmem[qt]);
+    }
 #ifdef MEA_EXP_TIMING
     unsigned long long* tdbg = reinterpret_cast<unsigned long long*>(p.lse);
     const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && quarter == 0;
@@ -316,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (!kStats && t > 0 && __any_sync(0xffffffffu, need)) {
           // v* <- v* alpha once PV_{t-1} has finished (lanes 0-15: O columns [0,32), 16-31: [32,64))
-          mbar_wait(&sm.pv_done[qt][(t - 1) & 1], ((t - 1) >> 1) & 1);
+          mbar_wait(&sm.pv_done[qt], (t - 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int part = 0; part < 2; ++part) {
@@ -342,14 +357,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       TPROBE(3)
       if (!kStats) {
-        // P_t over P_{t-2} once P_{t-2} V_{t-2} has read it
-        if (t > 1) mbar_wait(&sm.pv_done[qt][t & 1], ((t - 2) >> 1) & 1);
+        // P_t over P_{t-1} once P_{t-1} V_{t-1} has read it
+        if (t > 0) mbar_wait(&sm.pv_done[qt], (t - 1) & 1);
         TPROBE(4)
         tc_fence_after();
-        tmem_st16_split<16>(lane_base + col_p(qt, t & 1), pk);
+        tmem_st16_split<16>(lane_base + col_p(qt), pk);
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&sm.p_full[qt][t & 1]);
+        mbar_arrive(&sm.p_full[qt]);
       }
       TPROBE(5)
     }
@@ -365,6 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_ld32_split<32>(lane_base + col_o(qt), o);
     tmem_ld_wait();
     if (row < q_end) {
+      const size_t bh = (size_t)b * p.H + h;
       const float inv = lrow > 0.f ? 1.f / lrow : 0.f;  // a row with no keys (padding): out = 0, lse = -inf
       const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + half * 32;
       if (p.out_f32) {
@@ -386,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
 #ifndef MEA_EXP_TIMING
-      if (p.lse && half == 0) p.lse[((size_t)b * p.H + h) * p.n_q + row] = (m_ref + __log2f(lrow)) * 0.6931471805599453f;
+      if (p.lse && half == 0) p.lse[bh * p.n_q + row] = (m_ref + __log2f(lrow)) * 0.6931471805599453f;
 #endif
     }
     }  // !kStats
