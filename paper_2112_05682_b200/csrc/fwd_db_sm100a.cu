@@ -1,30 +1,32 @@
-// fwd_db_sm100a.cu — d = 64 self-attention forward (bf16 in, fp32 accumulate): the d = 64
-// forward online over all keys, with or without the causal mask or key padding (the key-split
-// schedule and the triple output run fwd_sm100a.cu).
+// fwd_db_sm100a.cu — d = 64 self-attention forward with double-buffered scores (bf16 in, fp32
+// accumulate): the d = 64 forward online over all keys, with or without the causal mask (the
+// key-split schedule and the triple output run fwd_sm100a.cu).
 //
 // Same method as fwd_sm100a.cu (the paper's per-query stream, key chunk by
 // key chunk, Figure 1 lines 12-19 = PAPER.md:118-126; lazy rescale "as needed"), same
 // CTA shape (two 128-row query tiles of one (b, h), 16 softmax warps, a thread = one
-// row-half), laid out so that no product waits for another one:
+// row-half), but the key tile is 96 wide so that each query tile gets TWO score buffers:
 //
-//   TMEM (512 columns): S[qt][0], S[qt][1] = 4 x 64 columns at 0, 64, 128, 192 (64-key tiles);
-//                       P0 [256,288), P1 [288,320) (bf16 pairs);  O0 [320,384), O1 [384,448);
-//                       Q0 [448,480), Q1 [480,512) (the query tiles as bf16 pairs).
+//   TMEM (512 columns): S[qt][0] S[qt][1] = 4 x 96 columns at 0, 96, 192, 288;
+//                       O0 [384,448), O1 [448,512).
+//   P_t (bf16 pairs, 48 columns) is written over the first half of the buffer S_t came from.
 //
-// * Q sits in TMEM, so S = Q K^T is a TS product (A from TMEM, B = the K tile): it runs at the
-//   full tensor rate (an SS product at N = 96 is shared-memory bound at 86 %, tools/micro).
-// * P has its own columns, so S_{t+2} is computed as soon as the softmax has READ S_t (s_free),
-//   not after P_t V_t: the scores run two tiles ahead of the softmax whatever the P V chain
-//   does, and P_{t+1} only waits for P_t V_t (pv_done) before its store.
-// The previous layout (96-key tiles, P over S_t) made S_{t+2} wait for P_t V_t, and the chain
-// arrive(P_t) -> P_t V_t -> Q K_{t+2}^T left the softmax waiting ~350 cycles per tile.
+// With one buffer (fwd_sm100a.cu) S_{t+1} could only be computed after the softmax had read
+// S_t, and it queued behind the PV products of both tiles on the tensor pipe: the softmax
+// waited for scores ~150 cycles and for PV_{t-1} ~300 cycles per tile, and the two query tiles
+// drifted into phase, leaving the exponential unit (the binding unit at d = 64: 2 exps per
+// 128 MMA flops) idle ~22 % of the time. Here QK_{t+2} is issued as soon as PV_t has consumed
+// P_t, a whole softmax step ahead, so the scores of the next tile are always waiting; the
+// softmax prefetches them (tcgen05.ld) before storing P_t, hiding the TMEM latency, and never
+// waits on PV except before a (rare) O rescale.
 //
-// Warp roles: 0 TMA producer (Q0, Q1 once; kStages-deep K/V ring of 64-row tiles), 1 / 3 MMA
-// issuers for query tile 0 / 1, 2 TMEM allocator, 4-19 softmax (they also copy Q into TMEM).
+// Warp roles: 0 TMA producer (Q0, Q1 once; kStages-deep K/V ring of 96-row tiles), 1 / 3 MMA
+// issuers for query tile 0 / 1, 2 TMEM allocator, 4-19 softmax (as fwd_sm100a.cu).
 //
 // kStats = true is the backward's statistics pass B0 (the forward's
 // statistics recomputed when they were not saved): the same row max / row sum of exponentials
 // over Q K^T, but no V stream, no P store, no P V product and no output: only lse is written.
+// Without P V the issuer refills a score buffer as soon as the softmax has read it.
 #include <cuda_bf16.h>
 
 #include "internal.h"
@@ -33,45 +35,38 @@
 namespace mea {
 namespace {
 
-constexpr int kN = 64;                                // keys per tile
+constexpr int kN = 96;                                // keys per tile
 #ifndef MEA_DB_STAGES
-#define MEA_DB_STAGES 8
+#define MEA_DB_STAGES 6
 #endif
 constexpr int kStages = MEA_DB_STAGES;                // K/V ring depth
 constexpr int kQTileBytes = kTileM * kHeadDim * 2;    // 16 KiB
-constexpr int kKVTileBytes = kN * kHeadDim * 2;       // 8 KiB (a multiple of the 1 KiB swizzle atom)
+constexpr int kKVTileBytes = kN * kHeadDim * 2;       // 12 KiB (a multiple of the 1 KiB swizzle atom)
 constexpr int kThreads = 640;
 constexpr int kSoftmaxRegs = 112;                     // 32 + 4 x 112 = 480 per lane slot
 constexpr int kControlRegs = 32;
 constexpr float kLazyThreshold = 8.0f;
 constexpr float kSafeSum = 18446744073709551616.0f;   // 2^64
 __host__ __device__ constexpr uint32_t col_s(int qt, int b) { return (uint32_t)((qt * 2 + b) * kN); }
-__host__ __device__ constexpr uint32_t col_p(int qt) { return 256u + 32u * qt; }
-__host__ __device__ constexpr uint32_t col_o(int qt) { return 320u + 64u * qt; }
-__host__ __device__ constexpr uint32_t col_q(int qt) { return 448u + 32u * qt; }
+__host__ __device__ constexpr uint32_t col_o(int qt) { return qt ? 448u : 384u; }
 
-constexpr uint32_t kIdescQK = idesc_bf16_f32(128, kN, false, false);   // A = Q (TMEM), B = K K-major
+constexpr uint32_t kIdescQK = idesc_bf16_f32(128, kN, false, false);   // A = Q, B = K, both K-major
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 64, false, true);    // A = P (TMEM), B = V MN-major
 
 #ifndef MEA_DB_POLY_MASK
-#define MEA_DB_POLY_MASK 0x00000080u  // pair 7 of the 16 pairs of a half row on the FMA pipe
+#define MEA_DB_POLY_MASK 0x00080080u  // pairs 7 and 19 of the 24 pairs of a half row on the FMA pipe
 #endif
 __device__ __forceinline__ constexpr bool poly_pair(int i) { return ((MEA_DB_POLY_MASK) >> i) & 1u; }
-
-// MMA-issuer waits: up to 32 unrolled polls, then suspend
-#define IWAIT mbar_poll_wait<32>
 
 struct DbSmem {
   uint8_t q[2][kQTileBytes];
   uint8_t k[kStages][kKVTileBytes];
   uint8_t v[kStages][kKVTileBytes];
   uint64_t q_full;
-  uint64_t q_tmem[2];     // [query tile]: Q copied into TMEM (256 softmax threads)
   uint64_t kv_full[kStages];
   uint64_t kv_empty[kStages];
-  uint64_t s_full[2][2];  // [query tile][buffer]: Q K_t^T done
-  uint64_t s_free[2][2];  // [query tile][buffer]: the softmax has read S_t (256 threads)
-  uint64_t p_full[2];     // P_t stored (256 threads)
+  uint64_t s_full[2][2];  // [query tile][buffer]
+  uint64_t p_full[2][2];  // [query tile][tile parity]: an arrival for tile t+1 never lands in tile t's phase
   uint64_t pv_done[2];
   uint64_t o_done[2];
   uint32_t tmem_base;
@@ -111,12 +106,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.kv_empty[i], 2);  // one commit per query tile
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.q_tmem[i], 256);
       mbar_init(&sm.s_full[i][0], 1);
       mbar_init(&sm.s_full[i][1], 1);
-      mbar_init(&sm.s_free[i][0], 256);
-      mbar_init(&sm.s_free[i][1], 256);
-      mbar_init(&sm.p_full[i], 256);
+      mbar_init(&sm.p_full[i][0], 256);
+      mbar_init(&sm.p_full[i][1], 256);
       mbar_init(&sm.pv_done[i], 1);
       mbar_init(&sm.o_done[i], 1);
     }
@@ -158,58 +151,62 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------------------------------------------------- MMA issuers
       const int qt = warp >> 1;
       const int Tq = tiles_for(qt);
+      const uint64_t dq = shfl0_u64(sdesc_sw128(smem_u32(sm.q[qt]), 16, 1024));
       const uint64_t dk0 = shfl0_u64(sdesc_sw128(smem_u32(sm.k[0]), 16, 1024));
       const uint64_t dv0 = shfl0_u64(sdesc_sw128(smem_u32(sm.v[0]), 16, 1024));
       constexpr uint64_t kStageStep = kKVTileBytes >> 4;
       const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
-      const uint32_t to = tmem_u + col_o(qt), tq = tmem_u + col_q(qt), tp = tmem_u + col_p(qt);
-      auto qk = [&](int t) {  // S[qt][t & 1] = Q K_t^T (A = Q from TMEM)
+      const uint32_t to = tmem_u + col_o(qt);
+      auto qk = [&](int t) {  // S[qt][t & 1] = Q K_t^T
         const uint64_t dk = dk0 + (t % kStages) * kStageStep;
         const uint32_t ts = tmem_u + col_s(qt, t & 1);
 #pragma unroll
-        for (int kk = 0; kk < kHeadDim / 16; ++kk) umma_ts(ts, tq + kk * 8, dk + kk * 2, kIdescQK, kk > 0);
+        for (int kk = 0; kk < kHeadDim / 16; ++kk) umma_ss(ts, dq + kk * 2, dk + kk * 2, kIdescQK, kk > 0);
         umma_commit(&sm.s_full[qt][t & 1]);
       };
-      auto pv = [&](int t) {  // O += P_t V_t
+      auto pv = [&](int t) {  // O += P_t V_t, P_t over the first 48 columns of S[qt][t & 1]
         const uint64_t dv = dv0 + (t % kStages) * kStageStep;
+        const uint32_t tp = tmem_u + col_s(qt, t & 1);
 #pragma unroll
         for (int kk = 0; kk < kN / 16; ++kk)
           umma_ts(to, tp + kk * 8, dv + kk * 128, kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
       };
-      IWAIT(&sm.q_tmem[qt], 0);
+      mbar_wait(&sm.q_full, 0);
       for (int t = 0; t < 2 && t < Tq; ++t) {
-        IWAIT(&sm.kv_full[t % kStages], (t / kStages) & 1);
+        mbar_wait(&sm.kv_full[t], 0);
         tc_fence_after();
         if (elect_one()) qk(t);
         __syncwarp();
       }
 #ifdef MEA_EXP_TIMING
 #define IPROBE(k) if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && t >= 8 && t < 24) \
-    reinterpret_cast<unsigned long long*>(p.lse)[2048 + (qt * 16 + (t - 8)) * 8 + (k)] = clock64();
+    reinterpret_cast<unsigned long long*>(p.lse)[512 + (qt * 16 + (t - 8)) * 8 + (k)] = clock64();
 #else
 #define IPROBE(k)
 #endif
-      for (int t = 0; t < Tq; ++t) {
-        // S_{t+2} into the buffer S_t came from, as soon as the softmax has read S_t
-        if (t + 2 < Tq) {
-          IWAIT(&sm.s_free[qt][t & 1], (t >> 1) & 1);
-          IPROBE(0)
-          IWAIT(&sm.kv_full[(t + 2) % kStages], ((t + 2) / kStages) & 1);
-          tc_fence_after();
-          IPROBE(4)
-          if (elect_one()) qk(t + 2);
+      // The issuer's waits poll (mbarrier.test_wait) up to 32 times before suspending: it resumes
+      // as soon as the last softmax warp has stored P_t, without burning issue slots and power on
+      // long waits (vs try_wait: -2 % at full clocks; vs pure polling: -0.7 % at full clocks and
+      // -1 % under the sustained power cap, measured).
+      if (kStats) {
+        // scores only: K_t is released when QK_t completes; S_{t+2} refills S_t's buffer as soon
+        // as the softmax has read S_t into registers (p_full)
+        for (int t = 0; t < Tq; ++t) {
+          if (elect_one()) umma_commit(&sm.kv_empty[t % kStages]);   // tracks QK_t (issued above)
           __syncwarp();
-          IPROBE(1)
+          mbar_poll_wait<32>(&sm.p_full[qt][t & 1], (t >> 1) & 1);
+          if (t + 2 < Tq) {
+            mbar_poll_wait<32>(&sm.kv_full[(t + 2) % kStages], ((t + 2) / kStages) & 1);
+            tc_fence_after();
+            if (elect_one()) qk(t + 2);
+            __syncwarp();
+          }
         }
-        if (kStats) {
-          if (elect_one()) umma_commit(&sm.kv_empty[t % kStages]);   // tracks Q K_t^T
-          __syncwarp();
-          continue;
-        }
-        IWAIT(&sm.p_full[qt], t & 1);
-        IPROBE(2)
+      }
+      for (int t = 0; t < (kStats ? 0 : Tq); ++t) {
+        mbar_poll_wait<32>(&sm.p_full[qt][t & 1], (t >> 1) & 1);
+        IPROBE(0)
         tc_fence_after();
-        IPROBE(5)
         if (elect_one()) {
           pv(t);
           umma_commit(&sm.kv_empty[t % kStages]);
@@ -217,7 +214,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (t + 1 == Tq) umma_commit(&sm.o_done[qt]);
         }
         __syncwarp();
-        IPROBE(3)
+        IPROBE(1)
+        if (t + 2 < Tq) {
+          // S_{t+2} goes into the buffer P_t occupies: wait until PV_t has read it
+          mbar_poll_wait<32>(&sm.kv_full[(t + 2) % kStages], ((t + 2) / kStages) & 1);
+#ifndef MEA_DB_NO_PV_WAIT
+          mbar_poll_wait<32>(&sm.pv_done[qt], t & 1);
+#endif
+          IPROBE(2)
+          tc_fence_after();
+          if (elect_one()) qk(t + 2);
+          __syncwarp();
+          IPROBE(3)
+        }
       }
       // key tiles past this query tile's last row (causal): release their ring stages unused
       for (int t = Tq; t < T; ++t) {
@@ -230,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     setmaxnreg_inc<kSoftmaxRegs>();
     // ------------------------------------------------------------ softmax warps
     // warp (qt, sub, quarter) owns rows quarter*32 + sub*16 + [0,16) of query tile qt; with the
-    // 16x32bx2 shape lanes 0-15 hold key columns [0,32) and lanes 16-31 [32,64) of those rows.
+    // 16x32bx2 shape lanes 0-15 hold key columns [0,48) and lanes 16-31 [48,96) of those rows.
     const int sw = warp - 4;
     const int qt = sw >> 3;
     const int sub = (sw >> 2) & 1;
@@ -244,52 +253,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     // tiles [0, full) are complete for every row of the query tile (fast-path candidates)
     const int full = (p.causal ? min(nk, r0 + 1) : nk) / kN;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32 + sub * 16) << 16);
+    const uint32_t colO = col_o(qt);
     const float c = p.scale_log2;
     float m_ref = -INFINITY;  // reference max m* (log2 units of the scaled score)
     float l = 0.f;            // this half's part of s*
-    {
-      // Q row rloc, d [32 half, 32 half + 32) -> TMEM Q columns [16 half, 16 half + 16): the
-      // 128B-swizzled TMA tile holds 16-byte chunk j of row r at chunk position j ^ (r & 7)
-      mbar_wait(&sm.q_full, 0);
-      const uint8_t* qrow = sm.q[qt] + (rloc >> 3) * 1024 + (rloc & 7) * 128;
-      uint32_t w[16];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint4 x = *reinterpret_cast<const uint4*>(qrow + (((half * 4 + j) ^ (rloc & 7)) << 4));
-        w[4 * j] = x.x; w[4 * j + 1] = x.y; w[4 * j + 2] = x.z; w[4 * j + 3] = x.w;
-      }
-      tmem_st16_split<16>(lane_base + col_q(qt), w);
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(&sm.q_tmem[qt]);
-    }
 #ifdef MEA_EXP_TIMING
     unsigned long long* tdbg = reinterpret_cast<unsigned long long*>(p.lse);
-    const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && quarter == 0;
-#define TPROBE(k) if (probe && t >= 8 && t < 24) tdbg[(((qt * 2 + sub) * 16 + (t - 8))) * 8 + (k)] = clock64();
+    const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && quarter == 0 && sub == 0 && (lane & 15) == 0;
+#define TPROBE(k) if (probe && t >= 8 && t < 24) tdbg[((qt * 2 + half) * 16 + (t - 8)) * 8 + (k)] = clock64();
 #else
 #define TPROBE(k)
 #endif
-    uint32_t sr[32];
+    uint32_t sr[48];
+    auto load_s = [&](int t) {
+      const uint32_t a = lane_base + col_s(qt, t & 1);
+      tmem_ld32_split<48>(a, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld16_split<48>(a + 32, *reinterpret_cast<uint32_t(*)[16]>(&sr[32]));
+    };
+    if (Tq > 0) {
+      mbar_wait(&sm.s_full[qt][0], 0);
+      tc_fence_after();
+      load_s(0);
+    }
     for (int t = 0; t < Tq; ++t) {
       TPROBE(0)
-      mbar_wait(&sm.s_full[qt][t & 1], (t >> 1) & 1);
-      TPROBE(1)
-      tc_fence_after();
-      tmem_ld32_split<32>(lane_base + col_s(qt, t & 1), sr);
       tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&sm.s_free[qt][t & 1]);  // S_t is in registers: its buffer may be refilled
-      TPROBE(2)
-      const int valid = (key_lim - t * kN) - half * 32;  // keys of this tile in my half (may be <= 0)
-      uint32_t pk[16];
+      TPROBE(1)
+      if (kStats) {  // S_t is in registers: its buffer may be refilled
+        tc_fence_before();
+        mbar_arrive(&sm.p_full[qt][t & 1]);
+      }
+#ifdef MEA_EXP_TIMING
+      if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && t >= 8 && t < 12) {
+        tdbg[1024 + (t - 8) * 32 + sw * 2 + 1] = clock64();
+      }
+#endif
+      const int valid = (key_lim - t * kN) - half * 48;  // keys of this tile in my half (may be <= 0)
+      uint32_t pk[24];
       // fast path: m* set, and every row of the query tile sees every key of this tile
       bool fast = (t > 0) && (t < full) && (c >= 0.f);
       if (fast) {
         const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
         float2 rs = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < 24; ++i) {
           const float2 s2 = make_float2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]));
           const float2 x = __ffma2_rn(s2, c2, nm2);  // s*c - m*
 #ifdef MEA_EXP_NOEXP
@@ -311,13 +318,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c >= 0.f) {
           e0 = -INFINITY;
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
+          for (int i = 0; i < 48; ++i)
             if (i < valid) e0 = fmaxf(e0, __uint_as_float(sr[i]));
           ext = fmaxf(e0, __shfl_xor_sync(0xffffffffu, e0, 16));
         } else {
           e0 = INFINITY;
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
+          for (int i = 0; i < 48; ++i)
             if (i < valid) e0 = fminf(e0, __uint_as_float(sr[i]));
           ext = fminf(e0, __shfl_xor_sync(0xffffffffu, e0, 16));
         }
@@ -336,17 +343,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int part = 0; part < 2; ++part) {
             uint32_t o[16];
-            tmem_ld16_split<32>(lane_base + col_o(qt) + part * 16, o);
+            tmem_ld16_split<32>(lane_base + colO + part * 16, o);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16_split<32>(lane_base + col_o(qt) + part * 16, o);
+            tmem_st16_split<32>(lane_base + colO + part * 16, o);
           }
         }
         const float neg_m = -m_ref;
         float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < 24; ++i) {
           const float p0 = (2 * i < valid) ? ex2_approx(fmaf(__uint_as_float(sr[2 * i]), c, neg_m)) : 0.f;
           const float p1 = (2 * i + 1 < valid) ? ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), c, neg_m)) : 0.f;
           rs0 += p0;
@@ -355,18 +362,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         l += rs0 + rs1;
       }
-      TPROBE(3)
-      if (!kStats) {
-        // P_t over P_{t-1} once P_{t-1} V_{t-1} has read it
-        if (t > 0) mbar_wait(&sm.pv_done[qt], (t - 1) & 1);
-        TPROBE(4)
+      TPROBE(4)
+      // prefetch S_{t+1} (already computed: it sits in the other buffer), then store P_t over
+      // the first half of S_t's buffer
+      if (t + 1 < Tq) {
+        mbar_wait(&sm.s_full[qt][(t + 1) & 1], ((t + 1) >> 1) & 1);
         tc_fence_after();
-        tmem_st16_split<16>(lane_base + col_p(qt), pk);
+        load_s(t + 1);
+      }
+      TPROBE(2)
+      if (!kStats) {
+        const uint32_t pa = lane_base + col_s(qt, t & 1);
+        tmem_st16_split<24>(pa, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+        tmem_st8_split<24>(pa + 16, *reinterpret_cast<uint32_t(*)[8]>(&pk[16]));
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&sm.p_full[qt]);
+        mbar_arrive(&sm.p_full[qt][t & 1]);
       }
       TPROBE(5)
+#ifdef MEA_EXP_TIMING
+      if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && t >= 8 && t < 12) {
+        tdbg[1024 + (t - 8) * 32 + sw * 2] = clock64();
+      }
+#endif
     }
     // ------------------------------------------------------------ epilogue: out = v*/s*
     const float lrow = l + __shfl_xor_sync(0xffffffffu, l, 16);
@@ -377,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(&sm.o_done[qt], 0);
     tc_fence_after();
     uint32_t o[32];
-    tmem_ld32_split<32>(lane_base + col_o(qt), o);
+    tmem_ld32_split<32>(lane_base + colO, o);
     tmem_ld_wait();
     if (row < q_end) {
       const size_t bh = (size_t)b * p.H + h;

@@ -100,10 +100,10 @@ __global__ void __launch_bounds__(640, 1) kern(int mode, int iters, float cin, u
 
 template <unsigned P>
 void run(int mode, const char* name, unsigned long long* d, float* sink, int nthr = 640) {
-  cudaFuncSetAttribute(kern<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+  cudaFuncSetAttribute(kern<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
   for (int rep = 0; rep < 2; ++rep) {
     cudaMemset(d, 0, 148 * 17 * 8);
-    kern<P><<<148, nthr, 66 * 1024>>>(mode, 400, 0.01f, d, sink);
+    kern<P><<<148, nthr, 120 * 1024>>>(mode, 400, 0.01f, d, sink);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); exit(1); }
   }

@@ -96,11 +96,11 @@ int main() {
   auto run = [&](auto F, auto L) {
       constexpr int f = decltype(F)::value, l = decltype(L)::value;
       const int G = 2000;
-      cudaFuncSetAttribute(kern<f, l>, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+      cudaFuncSetAttribute(kern<f, l>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
       for (int rep = 0; rep < 2; ++rep) {
-        kern<f, l><<<148, 640, 66 * 1024>>>(G, d, sink);
+        kern<f, l><<<148, 640, 120 * 1024>>>(G, d, sink);
         cudaError_t e = cudaDeviceSynchronize();
-        if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
+        if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); exit(1); }
       }
       unsigned long long h[148];
       cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
