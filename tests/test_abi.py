@@ -112,13 +112,13 @@ def test_host_only_validation_of_the_newer_entry_points(lib):
     # partial forward: bf16 d in {64, 128}; n_q == 0 no-op
     assert lib.mea_attention_partial_fwd(p, p, p, p, p, p, 1, 1, 8, 8, 96, 1, 1.0, None) == 3
     assert lib.mea_attention_partial_fwd(p, p, p, p, p, p, 1, 1, 0, 8, 64, 1, 1.0, None) == 0
-    # d = 128 workspace sizes: forward none; backward (two-kernel path) delta and lse2 only,
-    # each padded to 128 rows per (b, h) and 256-byte aligned
+    # d = 128 workspace sizes: forward none; backward (fused kernel, bwd128_sm100a.cu) delta and
+    # lse2 (each padded to 128 rows per (b, h), 256-byte aligned) + the f32 dQ accumulator
     n = ctypes.c_size_t(7)
     assert lib.mea_attention_fwd_workspace_size(1, 2, 300, 300, 128, 1, 0, 0, ctypes.byref(n)) == 0
     assert n.value == 0
     assert lib.mea_attention_bwd_workspace_size(1, 2, 300, 300, 128, 1, 1, ctypes.byref(n)) == 0
-    assert n.value == 2 * (2 * 384 * 4)
+    assert n.value == 2 * (2 * 384 * 4) + 300 * 2 * 128 * 4
     assert lib.mea_attention_bwd_workspace_size(1, 2, 300, 300, 64, 1, 1, ctypes.byref(n)) == 0
     assert n.value > 300 * 2 * 64 * 4                       # d = 64 fused: + dq accumulator
 
