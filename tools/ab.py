@@ -3,7 +3,8 @@ shape (B=1, H=16, n=16384, bf16): calls alternate build by build so every build 
 clock / power state, with a 512 MiB L2 read-flush before each call; results are compared with the
 first build's (experiments only; parity is tests/).
 
-    CASE=fwd|fwd_paper|fwd_causal|bwd|bwd_causal|bwd_det|fwd128|bwd128 ITERS=30 python tools/ab.py A.so B.so ...
+    CASE=fwd|fwd_paper|fwd_causal|bwd|bwd_causal|bwd_det|fwd128|bwd128|sq|sq16 ITERS=30 python tools/ab.py A.so B.so ...
+(sq: configs[1], one query over 2^20 keys; sq16: the 16-head decode batch; TFLOP/s column = GB/s / 1000)
 """
 import ctypes, os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -38,7 +39,21 @@ vis = (n * (n + 1) / 2) if causal else n * n
 flops = (4 if case.startswith("fwd") else 10) * vis * d * H
 
 
+if case.startswith("sq"):
+    hs = 16 if case == "sq16" else 1
+    sq_q = torch.empty((1, hs, 64), dtype=torch.bfloat16, device="cuda")
+    sq_k = torch.empty((1, 1 << 20, hs, 64), dtype=torch.bfloat16, device="cuda")
+    sq_v = torch.empty_like(sq_k)
+    for t, tid in ((sq_q, 1), (sq_k, 2), (sq_v, 3)):
+        api.mea_fill_synthetic(t, 0, tid)
+    sq_ws = torch.empty(api.mea_single_query_workspace_size(1, hs, 1 << 20, 64, api.MEA_BF16), dtype=torch.uint8,
+                        device="cuda")
+    flops = 2 * hs * (1 << 20) * 64 * 2   # bytes (the column reads GB/s / 1000)
+
+
 def call():
+    if case.startswith("sq"):
+        return (api.mea_single_query_fwd(sq_q, sq_k, sq_v, workspace=sq_ws, out_dtype=torch.float32),)
     if case == "fwd_paper":   # configs[2]'s literal schedule: query chunk 1024, key chunk 4096
         return (api.mea_attention_fwd(q, k, v, q_chunk=1024, k_chunk=4096),)
     if case.startswith("fwd"):
