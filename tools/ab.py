@@ -3,7 +3,7 @@ shape (B=1, H=16, n=16384, bf16): calls alternate build by build so every build 
 clock / power state, with a 512 MiB L2 read-flush before each call; results are compared with the
 first build's (experiments only; parity is tests/).
 
-    CASE=fwd|fwd_paper|fwd_causal|bwd|bwd_causal|bwd_det|fwd128|bwd128|sq|sq16 ITERS=30 python tools/ab.py A.so B.so ...
+    CASE=fwd|fwd_paper|fwd_causal|bwd|bwd_causal|bwd_det|bwd_nolse|fwd128|bwd128|sq|sq16 ITERS=30 python tools/ab.py A.so B.so ...
 (sq: configs[1], one query over 2^20 keys; sq16: the 16-head decode batch; TFLOP/s column = GB/s / 1000)
 """
 import ctypes, os, statistics, sys
@@ -58,6 +58,8 @@ def call():
         return (api.mea_attention_fwd(q, k, v, q_chunk=1024, k_chunk=4096),)
     if case.startswith("fwd"):
         return (fwd(q, k, v),)
+    if case == "bwd_nolse":   # lse recomputed by the statistics pass B0
+        return api.mea_attention_bwd(q, k, v, out, do)
     bwd = {"bwd": api.mea_attention_bwd, "bwd128": api.mea_attention_bwd, "bwd_det": api.mea_attention_bwd_deterministic,
            "bwd_causal": api.mea_attention_bwd_causal}[case]
     return bwd(q, k, v, out, do, lse=lse)
