@@ -53,10 +53,12 @@ extern "C" {
 
 /*
  * MEA_F32_SPLIT (mea_attention_fwd's in_dtype only): float32 tensors computed on the bf16 tensor
- * cores by split precision (q, k in three bf16 parts, v and P in two; d == 64, float32 output,
- * no key chunks, not causal). Scores and the lse are fp32-accurate; each output element is within
- * 3 * 2^-18 * max|v| (~1.1e-5 max|v|) of exact — the P.V terms keep 16 bits. MEA_F32 is exact
- * fp32 FFMA arithmetic (any d <= 128) and is what the fp32 parity bar of BASELINE.json is held to.
+ * cores by split precision (q, k, v and P each in three bf16 parts, 24 bits; S and O as 6
+ * products each down to 2^-16 of the leading term, every key tile's P.V summed into a fresh TMEM
+ * tile and added to v* in fp32 registers; d == 64, float32 output, no key chunks, not causal).
+ * Scores, lse and outputs meet the strict fp32 bar (1e-5 absolute) at any finite scale
+ * (tests/test_gpu_forward.py::test_f32_split_precision_tensor_core_path). MEA_F32 is exact fp32
+ * FFMA arithmetic (any d <= 128), the default fp32 path.
  */
 typedef enum { MEA_F32 = 0, MEA_BF16 = 1, MEA_F32_SPLIT = 2 } mea_dtype_t;
 

@@ -182,3 +182,29 @@ def test_stats_pass_workspace_is_lse_only(lib):
         assert fn(B, H, n, n, 128, 1, 1, ctypes.byref(a)) == 0
         assert fn(B, H, n, n, 128, 1, 0, ctypes.byref(b)) == 0
         assert b.value - a.value == B * H * n * 4 + B * n * H * 128 * 2
+
+
+def c_example_binary(out_dir):
+    """Compile examples/mea_example.c (plain C99 against include/mea.h) and link libmea.so."""
+    import shutil
+    import subprocess
+    from paper_2112_05682_b200 import _lib
+    cc = shutil.which("gcc") or shutil.which("cc")
+    cuda_inc = "/usr/local/cuda/include"
+    if cc is None or not os.path.exists(os.path.join(cuda_inc, "cuda_runtime_api.h")):
+        pytest.skip("no C compiler / CUDA headers")
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2112_05682_b200 import build
+        build.build()
+    exe = os.path.join(out_dir, "mea_example")
+    cmd = [cc, "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"), "-I", cuda_inc,
+           os.path.join(ROOT, "examples", "mea_example.c"), "-L", os.path.dirname(_lib.LIB_PATH), "-lmea",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", "-lm", "-o", exe]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_example_compiles_and_links(tmp_path):
+    """The C ABI is usable from plain C99: the example builds warning-free and links libmea.so."""
+    assert os.path.exists(c_example_binary(str(tmp_path)))
