@@ -109,10 +109,6 @@ cudaError_t launch_merge_pair(float* dst_o, float2* dst_ml, const float* src_o, 
 int fwd_db_key_tile();
 cudaError_t launch_fwd_db_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                                const CUtensorMap& mv, cudaStream_t s);
-// d = 64 forward as four key-parity streams per CTA (fwd_kp_sm100a.cu): same contract as fwd_db
-int fwd_kp_key_tile();
-cudaError_t launch_fwd_kp_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
-                               const CUtensorMap& mv, cudaStream_t s);
 cudaError_t launch_fwd128_bf16(const FwdParams& p, const CUtensorMap& mq, const CUtensorMap& mk,
                                const CUtensorMap& mv, cudaStream_t s);
 cudaError_t launch_split_f32(const float* x, void* const* parts, int nparts, int64_t n, cudaStream_t s);

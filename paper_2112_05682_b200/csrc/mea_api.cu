@@ -68,10 +68,6 @@ struct ProfScope {
 #ifndef MEA_FWD_DB
 #define MEA_FWD_DB 1
 #endif
-// the online d = 64 forward (and B0): fwd_kp (four key-parity streams per CTA) or fwd_db
-#ifndef MEA_FWD_KP
-#define MEA_FWD_KP 0
-#endif
 
 namespace mea {
 
@@ -307,7 +303,7 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
   // key padding is implemented by fwd_db (d = 64) and fwd128 only: never silently drop the mask
   if (kv_lens && d == kHeadDim && !use_db)
     return fail(MEA_ERR_UNSUPPORTED, "key padding needs the online d = 64 forward (no key split; MEA_FWD_DB build)");
-  const int key_box = use_db ? (MEA_FWD_KP ? fwd_kp_key_tile() : fwd_db_key_tile()) : kTileN;
+  const int key_box = use_db ? fwd_db_key_tile() : kTileN;
   CUtensorMap mq, mk, mv;
   const char* why = "";
   cudaError_t e;
@@ -359,8 +355,7 @@ static mea_status_t fwd_impl(const void* q, const void* k, const void* v, void* 
       if ((e = launch_fwd128_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd128_bf16 launch");
     } else if (use_db) {
       ProfScope ps(stats_only ? "bwd_stats" : "fwd_bf16", st);
-      if ((e = (MEA_FWD_KP ? launch_fwd_kp_bf16 : launch_fwd_db_bf16)(p, mq, mk, mv, st)) != cudaSuccess)
-        return cuda_fail(e, "fwd_db_bf16 launch");
+      if ((e = launch_fwd_db_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_db_bf16 launch");
     } else {
       ProfScope ps("fwd_bf16", st);
       if ((e = launch_fwd_bf16(p, mq, mk, mv, st)) != cudaSuccess) return cuda_fail(e, "fwd_bf16 launch");

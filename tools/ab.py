@@ -3,16 +3,17 @@ shape (B=1, H=16, n=16384, bf16): calls alternate build by build so every build 
 clock / power state, with a 512 MiB L2 read-flush before each call; results are compared with the
 first build's (experiments only; parity is tests/).
 
-    CASE=fwd|fwd_paper|fwd_causal|bwd|bwd_causal|bwd_det|bwd_nolse|fwd128|bwd128|sq|sq16 ITERS=30 python tools/ab.py A.so B.so ...
+    [COOL_MS=ms] CASE=fwd|fwd_paper|fwd_causal|bwd|bwd_causal|bwd_det|bwd_nolse|fwd128|bwd128|sq|sq16 ITERS=30 python tools/ab.py A.so B.so ...
 (sq: configs[1], one query over 2^20 keys; sq16: the 16-head decode batch; TFLOP/s column = GB/s / 1000)
 """
-import ctypes, os, statistics, sys
+import ctypes, os, statistics, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2112_05682_b200 import _lib, api
 
 case = os.environ.get("CASE", "fwd")
 iters = int(os.environ.get("ITERS", "30"))
+cool_ms = float(os.environ.get("COOL_MS", "0"))
 libs = sys.argv[1:]
 d = 128 if case.endswith("128") else 64
 n, H = 16384, 16
@@ -68,6 +69,9 @@ def call():
 for i in range(iters + 2):
     for path in libs:
         _lib._lib = fns[path]
+        if cool_ms:   # idle before each call: the board leaves its power cap, clocks return to max
+            torch.cuda.synchronize()
+            time.sleep(cool_ms / 1e3)
         torch.sum(flush, dim=0, out=sink)
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         e0.record()
