@@ -92,9 +92,10 @@ def peaks():
     try:
         mp = json.load(open(path))
         return {"tflops": mp["bf16_tflops"], "tflops_sustained": mp.get("bf16_tflops_sustained"),
-                "hbm_gbs": mp["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+                "hbm_gbs": mp["hbm_gbs"], "sm_max_mhz": mp.get("sm_max_mhz", 1965.0),
+                "source": "measured (MEASURED_PEAKS.json)"}
     except Exception:
-        return {"tflops": 1590.0, "tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+        return {"tflops": 1590.0, "tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "sm_max_mhz": 1965.0,
                 "source": "fallback (B200_PROFILING.md)"}
 
 
@@ -425,6 +426,16 @@ def main():
         fwd_ms = tmean(fwd, max(3, a.steps // 2))
         extras["fwd"] = {"ms": fwd_ms, "tflops": flop_fwd / (fwd_ms * 1e-3) / 1e12,
                          "frac": flop_fwd / (fwd_ms * 1e-3) / 1e12 / pk["tflops"]}
+        if D == 64 and a.dtype == "bf16":
+            # the d = 64 forward's own roofline is the exponential unit (2 exps per 256 flops):
+            # 16 ex2 / clk / SM (tools/micro/exp_throughput.cu measured 16.4) x 148 SMs x the max SM clock
+            exps = flop_fwd / (4 * D)
+            exp_peak = 16 * 148 * pk["sm_max_mhz"] * 1e6
+            extras["fwd"]["exp_roofline"] = {
+                "bound": "alu (MUFU ex2)", "achieved": exps / (fwd_ms * 1e-3) / 1e12, "peak": exp_peak / 1e12,
+                "unit": "Tex2/s", "frac": exps / (fwd_ms * 1e-3) / exp_peak,
+                "peak_basis": "16 exp/clk/SM x 148 SMs x %d MHz (max SM clock); 2 of 24 exponential pairs run on "
+                              "the FMA pipe, so the frac can exceed the MUFU-only reading" % pk["sm_max_mhz"]}
         if a.dtype == "bf16":
             out32 = torch.empty(shape, dtype=torch.float32, device=dev)
             f32_ms = tmean(lambda: api.mea_attention_fwd(q, k, v, out=out32, lse=lse), max(3, a.steps // 2))
