@@ -5,7 +5,7 @@
 //   bit 0: tcgen05.ld of 48 columns (.16x32bx2 x32 + x16) and tcgen05.st of 24 (x16 + x8)
 //   bit 1: two mbarrier ops (test_wait of a completed phase, arrive on a never-waited barrier)
 //   bit 2: one __any_sync + one xor-shuffle
-//   bit 3: the tcgen05.ld alone, bit 4: the tcgen05.st alone
+//   bit 3: the tcgen05.ld alone, bit 4: the tcgen05.st alone, bit 5: the load in the .32x32b shape
 // cycles per exponential pair per SM sub-partition are reported.
 #include <cstdio>
 #include <cstdlib>
@@ -42,8 +42,14 @@ __global__ void __launch_bounds__(640, 1) kern(int iters, unsigned long long* ou
     for (int it = 0; it < iters; ++it) {
       if (MODE & 9) {
         uint32_t r[48];
-        tmem_ld32_split<48>(lb, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-        tmem_ld16_split<48>(lb + 32, *reinterpret_cast<uint32_t(*)[16]>(&r[32]));
+        if (MODE & 32) {   // same 48 columns x 32 lanes as .32x32b (thread = TMEM lane)
+          const uint32_t lq = tm + ((uint32_t)(quarter * 32) << 16) + qt * 192 + sub * 96;
+          tmem_ld32(lq, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld16(lq + 32, *reinterpret_cast<uint32_t(*)[16]>(&r[32]));
+        } else {
+          tmem_ld32_split<48>(lb, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld16_split<48>(lb + 32, *reinterpret_cast<uint32_t(*)[16]>(&r[32]));
+        }
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 48; ++i) v[i] += __uint_as_float(r[i]) * 1e-30f;
@@ -115,6 +121,7 @@ int main() {
   run<1, 0x00080080u>("+ tcgen05.ld 48 cols / st 24 cols", d, sink);
   run<8, 0x00080080u>("+ tcgen05.ld 48 cols only", d, sink);
   run<16, 0x00080080u>("+ tcgen05.st 24 cols only", d, sink);
+  run<8 | 32, 0x00080080u>("+ tcgen05.ld 48 cols only, .32x32b shape", d, sink);
   run<2, 0x00080080u>("+ 2 mbarrier ops", d, sink);
   run<4, 0x00080080u>("+ vote + shuffle", d, sink);
   run<7, 0x00080080u>("+ all of the above (the forward's mix)", d, sink);
