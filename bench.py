@@ -438,7 +438,7 @@ def main():
                               "the FMA pipe, so the frac can exceed the MUFU-only reading" % pk["sm_max_mhz"]}
             # with the scores' TMEM load and the P store each tile also needs, the exponential loop runs at
             # 18.2 cycles per pair per SM sub-partition (tools/micro/mio_mix.cu): the kernel's practical floor
-            pairs_per_smsp = exps / 2 / (148 * 4)
+            pairs_per_smsp = exps / 64 / (148 * 4)   # warp-wide pairs: 32 lanes x 2 exponentials
             floor_ms = pairs_per_smsp * 18.2 / (pk["sm_max_mhz"] * 1e6) * 1e3
             extras["fwd"]["exp_roofline"].update({"practical_floor_ms": floor_ms, "frac_of_practical_floor": floor_ms / fwd_ms,
                                                   "practical_floor_basis": "18.2 cycles per exp pair per SMSP incl. "
