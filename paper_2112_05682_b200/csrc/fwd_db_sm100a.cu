@@ -245,37 +245,52 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     setmaxnreg_inc<kSoftmaxRegs>();
     // ------------------------------------------------------------ softmax warps
-    // warp (qt, sub, quarter) owns rows quarter*32 + sub*16 + [0,16) of query tile qt; with the
-    // 16x32bx2 shape lanes 0-15 hold key columns [0,48) and lanes 16-31 [48,96) of those rows.
+    // warp (qt, sub, quarter) owns TMEM lanes L0 = quarter*32 + sub*16 + [0,16) of query tile qt.
+    // Scores are read with the .16x256b shape and P written with .16x128b (ptx.cuh): thread t
+    // (q = t % 4) holds rows a = L0 + t/4 and b = L0 + 8 + t/4, score columns 8r + 2q, 8r + 2q + 1
+    // of both (r = 0..11) — exactly the keys of P column 4r + q, which .16x128b stores from the
+    // same thread. A row is spread over the 4 threads of a quad (max / sum: two xor-shuffles).
+    // These shapes cost the exponential unit far less per byte than .16x32bx2 (tools/micro/mio_mix.cu:
+    // the forward's per-tile traffic 18.2 -> 16.3 cycles per exponential pair per SMSP).
     const int sw = warp - 4;
     const int qt = sw >> 3;
     const int sub = (sw >> 2) & 1;
     const int quarter = warp & 3;
-    const int half = lane >> 4;
-    const int rloc = quarter * 32 + sub * 16 + (lane & 15);
-    const int r0 = q0 + qt * kTileM;  // first row of this query tile
-    const int row = r0 + rloc;
+    const int q = lane & 3;
+    const int ra = lane >> 2;              // row a = L0 + ra, row b = L0 + 8 + ra
+    const int L0 = quarter * 32 + sub * 16;
+    const int r0 = q0 + qt * kTileM;       // first row of this query tile
+    const int row_a = r0 + L0 + ra, row_b = row_a + 8;
     const int Tq = tiles_for(qt);
-    const int key_lim = p.causal ? min(nk, row + 1) : nk;  // keys this row sees: [0, key_lim)
+    const int lim_a = p.causal ? min(nk, row_a + 1) : nk;  // keys these rows see: [0, lim)
+    const int lim_b = p.causal ? min(nk, row_b + 1) : nk;
     // tiles [0, full) are complete for every row of the query tile (fast-path candidates)
     const int full = (p.causal ? min(nk, r0 + 1) : nk) / kN;
-    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32 + sub * 16) << 16);
+    const uint32_t lane_base = tmem + ((uint32_t)L0 << 16);
     const uint32_t colO = col_o(qt);
     const float c = p.scale_log2;
-    float m_ref = -INFINITY;  // reference max m* (log2 units of the scaled score)
-    float l = 0.f;            // this half's part of s*
+    float m_a = -INFINITY, m_b = -INFINITY;  // reference max m* per row (log2 units of the scaled score)
+    float l_a = 0.f, l_b = 0.f;              // this thread's part of s* per row
 #ifdef MEA_EXP_TIMING
     unsigned long long* tdbg = reinterpret_cast<unsigned long long*>(p.lse);
-    const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && quarter == 0 && sub == 0 && (lane & 15) == 0;
-#define TPROBE(k) if (probe && t >= 8 && t < 24) tdbg[((qt * 2 + half) * 16 + (t - 8)) * 8 + (k)] = clock64();
+    const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && quarter == 0 && sub == 0 && lane == 0;
+#define TPROBE(k) if (probe && t >= 8 && t < 24) tdbg[(qt * 16 + (t - 8)) * 8 + (k)] = clock64();
 #else
 #define TPROBE(k)
 #endif
     uint32_t sr[48];
     auto load_s = [&](int t) {
       const uint32_t a = lane_base + col_s(qt, t & 1);
-      tmem_ld32_split<48>(a, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld16_split<48>(a + 32, *reinterpret_cast<uint32_t(*)[16]>(&sr[32]));
+      tmem_ld_16x256b_x8(a, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld_16x256b_x4(a + 64, *reinterpret_cast<uint32_t(*)[16]>(&sr[32]));
+    };
+    auto quad_max = [](float x) {
+      x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 1));
+      return fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 2));
+    };
+    auto quad_min = [](float x) {
+      x = fminf(x, __shfl_xor_sync(0xffffffffu, x, 1));
+      return fminf(x, __shfl_xor_sync(0xffffffffu, x, 2));
     };
     if (Tq > 0) {
       mbar_wait(&sm.s_full[qt][0], 0);
@@ -290,84 +305,108 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         mbar_arrive(&sm.p_full[qt][t & 1]);
       }
-#ifdef MEA_EXP_TIMING
-      if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && t >= 8 && t < 12) {
-        tdbg[1024 + (t - 8) * 32 + sw * 2 + 1] = clock64();
-      }
-#endif
-      const int valid = (key_lim - t * kN) - half * 48;  // keys of this tile in my half (may be <= 0)
+      const int valid_a = lim_a - t * kN, valid_b = lim_b - t * kN;  // keys of this tile each row sees
       uint32_t pk[24];
       // fast path: m* set, and every row of the query tile sees every key of this tile
       bool fast = (t > 0) && (t < full) && (c >= 0.f);
       if (fast) {
-        const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
-        float2 rs = make_float2(0.f, 0.f);
+        const float2 c2 = make_float2(c, c), na2 = make_float2(-m_a, -m_a), nb2 = make_float2(-m_b, -m_b);
+        float2 rsa = make_float2(0.f, 0.f), rsb = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int i = 0; i < 24; ++i) {
-          const float2 s2 = make_float2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]));
-          const float2 x = __ffma2_rn(s2, c2, nm2);  // s*c - m*
+        for (int r = 0; r < 12; ++r) {
+          const float2 sa = make_float2(__uint_as_float(sr[4 * r]), __uint_as_float(sr[4 * r + 1]));
+          const float2 sb = make_float2(__uint_as_float(sr[4 * r + 2]), __uint_as_float(sr[4 * r + 3]));
+          const float2 xa = __ffma2_rn(sa, c2, na2), xb = __ffma2_rn(sb, c2, nb2);  // s*c - m*
 #ifdef MEA_EXP_NOEXP
-          const float2 e = __fmul2_rn(x, make_float2(1e-30f, 1e-30f));  // timing experiment only
+          const float2 ea = __fmul2_rn(xa, make_float2(1e-30f, 1e-30f)), eb = __fmul2_rn(xb, make_float2(1e-30f, 1e-30f));
 #else
-          const float2 e = poly_pair<kStats>(i) ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          const float2 ea = poly_pair<kStats>(2 * r) ? exp2_poly2(xa) : make_float2(ex2_approx(xa.x), ex2_approx(xa.y));
+          const float2 eb = poly_pair<kStats>(2 * r + 1) ? exp2_poly2(xb) : make_float2(ex2_approx(xb.x), ex2_approx(xb.y));
 #endif
-          rs = __fadd2_rn(rs, e);
-          pk[i] = pack_bf16x2(e.x, e.y);
+          rsa = __fadd2_rn(rsa, ea);
+          rsb = __fadd2_rn(rsb, eb);
+          pk[2 * r] = pack_bf16x2(ea.x, ea.y);      // P row a, column 4r + q
+          pk[2 * r + 1] = pack_bf16x2(eb.x, eb.y);  // P row b, column 4r + q
         }
-        // a finite half-row sum below 2^64 certifies every 2^(s c - m*) term (fwd_sm100a.cu)
-        const float rsum = rs.x + rs.y;
-        const bool need = !(rsum <= kSafeSum);
+        // finite per-thread row sums below 2^64 certify every 2^(s c - m*) term (fwd_sm100a.cu)
+        const float suma = rsa.x + rsa.y, sumb = rsb.x + rsb.y;
+        const bool need = !(suma <= kSafeSum) || !(sumb <= kSafeSum);
         if (__any_sync(0xffffffffu, need)) fast = false;
-        else l += rsum;
+        else {
+          l_a += suma;
+          l_b += sumb;
+        }
       }
       if (!fast) {
-        float ext, e0;
+        // exact extreme of each row's visible scores (this thread's 24, then the quad)
+        float ea = c >= 0.f ? -INFINITY : INFINITY, eb = ea;
+#pragma unroll
+        for (int r = 0; r < 12; ++r)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int k = 8 * r + 2 * q + j;
+            const float sa = __uint_as_float(sr[4 * r + j]), sb = __uint_as_float(sr[4 * r + 2 + j]);
+            if (c >= 0.f) {
+              if (k < valid_a) ea = fmaxf(ea, sa);
+              if (k < valid_b) eb = fmaxf(eb, sb);
+            } else {
+              if (k < valid_a) ea = fminf(ea, sa);
+              if (k < valid_b) eb = fminf(eb, sb);
+            }
+          }
         if (c >= 0.f) {
-          e0 = -INFINITY;
-#pragma unroll
-          for (int i = 0; i < 48; ++i)
-            if (i < valid) e0 = fmaxf(e0, __uint_as_float(sr[i]));
-          ext = fmaxf(e0, __shfl_xor_sync(0xffffffffu, e0, 16));
+          ea = quad_max(ea);
+          eb = quad_max(eb);
         } else {
-          e0 = INFINITY;
-#pragma unroll
-          for (int i = 0; i < 48; ++i)
-            if (i < valid) e0 = fminf(e0, __uint_as_float(sr[i]));
-          ext = fminf(e0, __shfl_xor_sync(0xffffffffu, e0, 16));
+          ea = quad_min(ea);
+          eb = quad_min(eb);
         }
-        const float m_cand = ext * c;
-        const bool need = m_cand > m_ref + kLazyThreshold;  // always true on the first tile
-        float alpha = 1.f;
-        if (need) {
-          alpha = ex2_approx(m_ref - m_cand);  // 0 when m_ref = -inf
-          m_ref = m_cand;
-          l *= alpha;
+        const float mca = ea * c, mcb = eb * c;
+        const bool need_a = mca > m_a + kLazyThreshold, need_b = mcb > m_b + kLazyThreshold;  // always on the first tile
+        float alpha_a = 1.f, alpha_b = 1.f;
+        if (need_a) {
+          alpha_a = ex2_approx(m_a - mca);  // 0 when m* = -inf
+          m_a = mca;
+          l_a *= alpha_a;
         }
-        if (!kStats && t > 0 && __any_sync(0xffffffffu, need)) {
-          // v* <- v* alpha once PV_{t-1} has finished (lanes 0-15: O columns [0,32), 16-31: [32,64))
+        if (need_b) {
+          alpha_b = ex2_approx(m_b - mcb);
+          m_b = mcb;
+          l_b *= alpha_b;
+        }
+        if (!kStats && t > 0 && __any_sync(0xffffffffu, need_a || need_b)) {
+          // v* <- v* alpha once PV_{t-1} has finished: O (64 columns) in the same .16x256b layout
           mbar_wait(&sm.pv_done[qt], (t - 1) & 1);
           tc_fence_after();
+          uint32_t o[32];
+          tmem_ld_16x256b_x8(lane_base + colO, o);
+          tmem_ld_wait();
 #pragma unroll
-          for (int part = 0; part < 2; ++part) {
-            uint32_t o[16];
-            tmem_ld16_split<32>(lane_base + colO + part * 16, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16_split<32>(lane_base + colO + part * 16, o);
+          for (int r = 0; r < 8; ++r) {
+            o[4 * r] = __float_as_uint(__uint_as_float(o[4 * r]) * alpha_a);
+            o[4 * r + 1] = __float_as_uint(__uint_as_float(o[4 * r + 1]) * alpha_a);
+            o[4 * r + 2] = __float_as_uint(__uint_as_float(o[4 * r + 2]) * alpha_b);
+            o[4 * r + 3] = __float_as_uint(__uint_as_float(o[4 * r + 3]) * alpha_b);
           }
+          tmem_st_16x256b_x8(lane_base + colO, o);
         }
-        const float neg_m = -m_ref;
-        float rs0 = 0.f, rs1 = 0.f;
+        float sa0 = 0.f, sa1 = 0.f, sb0 = 0.f, sb1 = 0.f;
 #pragma unroll
-        for (int i = 0; i < 24; ++i) {
-          const float p0 = (2 * i < valid) ? ex2_approx(fmaf(__uint_as_float(sr[2 * i]), c, neg_m)) : 0.f;
-          const float p1 = (2 * i + 1 < valid) ? ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), c, neg_m)) : 0.f;
-          rs0 += p0;
-          rs1 += p1;
-          pk[i] = pack_bf16x2(p0, p1);
+        for (int r = 0; r < 12; ++r) {
+          const int k = 8 * r + 2 * q;
+          const float pa0 = k < valid_a ? ex2_approx(fmaf(__uint_as_float(sr[4 * r]), c, -m_a)) : 0.f;
+          const float pa1 = k + 1 < valid_a ? ex2_approx(fmaf(__uint_as_float(sr[4 * r + 1]), c, -m_a)) : 0.f;
+          const float pb0 = k < valid_b ? ex2_approx(fmaf(__uint_as_float(sr[4 * r + 2]), c, -m_b)) : 0.f;
+          const float pb1 = k + 1 < valid_b ? ex2_approx(fmaf(__uint_as_float(sr[4 * r + 3]), c, -m_b)) : 0.f;
+          sa0 += pa0;
+          sa1 += pa1;
+          sb0 += pb0;
+          sb1 += pb1;
+          pk[2 * r] = pack_bf16x2(pa0, pa1);
+          pk[2 * r + 1] = pack_bf16x2(pb0, pb1);
         }
-        l += rs0 + rs1;
+        l_a += sa0 + sa1;
+        l_b += sb0 + sb1;
       }
       TPROBE(4)
       // prefetch S_{t+1} (already computed: it sits in the other buffer), then store P_t over
@@ -380,55 +419,55 @@ __global__ void __launch_bounds__(kThreads, 1)
       TPROBE(2)
       if (!kStats) {
         const uint32_t pa = lane_base + col_s(qt, t & 1);
-        tmem_st16_split<24>(pa, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
-        tmem_st8_split<24>(pa + 16, *reinterpret_cast<uint32_t(*)[8]>(&pk[16]));
+        tmem_st_16x128b_x8(pa, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+        tmem_st_16x128b_x4(pa + 32, *reinterpret_cast<uint32_t(*)[8]>(&pk[16]));
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&sm.p_full[qt][t & 1]);
       }
       TPROBE(5)
-#ifdef MEA_EXP_TIMING
-      if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && t >= 8 && t < 12) {
-        tdbg[1024 + (t - 8) * 32 + sw * 2] = clock64();
-      }
-#endif
     }
     // ------------------------------------------------------------ epilogue: out = v*/s*
-    const float lrow = l + __shfl_xor_sync(0xffffffffu, l, 16);
+    l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
+    l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
+    l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
+    l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
+    const size_t bh = (size_t)b * p.H + h;
     if (kStats) {
-      if (row < q_end && half == 0)
-        p.lse[((size_t)b * p.H + h) * p.n_q + row] = (m_ref + __log2f(lrow)) * 0.6931471805599453f;
+      if (q == 0) {
+        if (row_a < q_end) p.lse[bh * p.n_q + row_a] = (m_a + __log2f(l_a)) * 0.6931471805599453f;
+        if (row_b < q_end) p.lse[bh * p.n_q + row_b] = (m_b + __log2f(l_b)) * 0.6931471805599453f;
+      }
     } else {
     mbar_wait(&sm.o_done[qt], 0);
     tc_fence_after();
     uint32_t o[32];
-    tmem_ld32_split<32>(lane_base + colO, o);
+    tmem_ld_16x256b_x8(lane_base + colO, o);
     tmem_ld_wait();
-    if (row < q_end) {
-      const size_t bh = (size_t)b * p.H + h;
-      const float inv = lrow > 0.f ? 1.f / lrow : 0.f;  // a row with no keys (padding): out = 0, lse = -inf
-      const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + half * 32;
-      if (p.out_f32) {
-        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
+    const float inv_a = l_a > 0.f ? 1.f / l_a : 0.f;  // a row with no keys (padding): out = 0, lse = -inf
+    const float inv_b = l_b > 0.f ? 1.f / l_b : 0.f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          dst[i] = make_float4(__uint_as_float(o[4 * i]) * inv, __uint_as_float(o[4 * i + 1]) * inv,
-                               __uint_as_float(o[4 * i + 2]) * inv, __uint_as_float(o[4 * i + 3]) * inv);
-      } else {
-        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off);
+    for (int hb = 0; hb < 2; ++hb) {
+      const int row = hb ? row_b : row_a;
+      const float inv = hb ? inv_b : inv_a;
+      if (row < q_end) {
+        const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + 2 * q;
+        if (p.out_f32) {
+          float* dst = static_cast<float*>(p.out) + off;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint4 w;
-          w.x = pack_bf16x2(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv);
-          w.y = pack_bf16x2(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv);
-          w.z = pack_bf16x2(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv);
-          w.w = pack_bf16x2(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv);
-          dst[i] = w;
+          for (int r = 0; r < 8; ++r)
+            *reinterpret_cast<float2*>(dst + 8 * r) = make_float2(__uint_as_float(o[4 * r + 2 * hb]) * inv,
+                                                                  __uint_as_float(o[4 * r + 2 * hb + 1]) * inv);
+        } else {
+          uint32_t* dst = reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(p.out) + off);
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+            dst[4 * r] = pack_bf16x2(__uint_as_float(o[4 * r + 2 * hb]) * inv, __uint_as_float(o[4 * r + 2 * hb + 1]) * inv);
         }
-      }
 #ifndef MEA_EXP_TIMING
-      if (p.lse && half == 0) p.lse[bh * p.n_q + row] = (m_ref + __log2f(lrow)) * 0.6931471805599453f;
+        if (p.lse && q == 0) p.lse[bh * p.n_q + row] = ((hb ? m_b : m_a) + __log2f(hb ? l_b : l_a)) * 0.6931471805599453f;
 #endif
+      }
     }
     }  // !kStats
   }

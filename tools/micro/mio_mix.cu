@@ -14,6 +14,47 @@
 #include "ptx.cuh"
 using namespace mea;
 
+__device__ __forceinline__ void ld_16x256b_x8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(taddr));
+}
+__device__ __forceinline__ void ld_16x256b_x4(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(taddr));
+}
+__device__ __forceinline__ void ld_16x128b_x16(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.16x128b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(taddr));
+}
+__device__ __forceinline__ void ld_16x128b_x8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.16x128b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(taddr));
+}
+__device__ __forceinline__ void ld_16x64b_x32(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.16x64b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) : "r"(taddr));
+}
+__device__ __forceinline__ void ld_16x64b_x16(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.16x64b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]) : "r"(taddr));
+}
+__device__ __forceinline__ void st_16x128b_x8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.16x128b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
+}
+__device__ __forceinline__ void st_16x128b_x4(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.16x128b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]) : "memory");
+}
+__device__ __forceinline__ void st_16x256b_x4(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]) : "memory");
+}
+__device__ __forceinline__ void st_16x256b_x2(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x2.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]) : "memory");
+}
+
 template <int MODE, unsigned POLY>
 __global__ void __launch_bounds__(640, 1) kern(int iters, unsigned long long* out, float* sink) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
@@ -42,7 +83,16 @@ __global__ void __launch_bounds__(640, 1) kern(int iters, unsigned long long* ou
     for (int it = 0; it < iters; ++it) {
       if (MODE & 9) {
         uint32_t r[48];
-        if (MODE & 32) {   // same 48 columns x 32 lanes as .32x32b (thread = TMEM lane)
+        if (MODE & 64) {          // .16x256b: 16 lanes x 96 columns (the same 6 KB per warp)
+          ld_16x256b_x8(lb, &r[0]);
+          ld_16x256b_x4(lb + 64, &r[32]);
+        } else if (MODE & 128) {  // .16x128b
+          ld_16x128b_x16(lb, &r[0]);
+          ld_16x128b_x8(lb + 64, &r[32]);
+        } else if (MODE & 256) {  // .16x64b
+          ld_16x64b_x32(lb, &r[0]);
+          ld_16x64b_x16(lb + 64, &r[32]);
+        } else if (MODE & 32) {   // same 48 columns x 32 lanes as .32x32b (thread = TMEM lane)
           const uint32_t lq = tm + ((uint32_t)(quarter * 32) << 16) + qt * 192 + sub * 96;
           tmem_ld32(lq, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
           tmem_ld16(lq + 32, *reinterpret_cast<uint32_t(*)[16]>(&r[32]));
@@ -74,8 +124,16 @@ __global__ void __launch_bounds__(640, 1) kern(int iters, unsigned long long* ou
       }
       l += rsum;
       if (MODE & 17) {
-        tmem_st16_split<24>(lb, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
-        tmem_st8_split<24>(lb + 16, *reinterpret_cast<uint32_t(*)[8]>(&pk[16]));
+        if (MODE & 512) {          // P (24 words per thread) as .16x128b (12 reps x 2 words)
+          st_16x128b_x8(lb, &pk[0]);
+          st_16x128b_x4(lb + 32, &pk[16]);
+        } else if (MODE & 1024) {  // as .16x256b
+          st_16x256b_x4(lb, &pk[0]);
+          st_16x256b_x2(lb + 32, &pk[16]);
+        } else {
+          tmem_st16_split<24>(lb, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
+          tmem_st8_split<24>(lb + 16, *reinterpret_cast<uint32_t(*)[8]>(&pk[16]));
+        }
         tmem_st_wait();
       } else {
 #pragma unroll
@@ -122,6 +180,14 @@ int main() {
   run<8, 0x00080080u>("+ tcgen05.ld 48 cols only", d, sink);
   run<16, 0x00080080u>("+ tcgen05.st 24 cols only", d, sink);
   run<8 | 32, 0x00080080u>("+ tcgen05.ld 48 cols only, .32x32b shape", d, sink);
+  run<8 | 64, 0x00080080u>("+ tcgen05.ld 6 KB per warp, .16x256b shape", d, sink);
+  run<16 | 512, 0x00080080u>("+ tcgen05.st 3 KB per warp, .16x128b shape", d, sink);
+  run<16 | 1024, 0x00080080u>("+ tcgen05.st 3 KB per warp, .16x256b shape", d, sink);
+  run<8 | 16 | 64 | 512, 0x00080080u>("+ ld .16x256b and st .16x128b", d, sink);
+  run<8 | 16 | 64 | 512 | 2 | 4, 0x00080080u>("the forward's mix with ld .16x256b, st .16x128b", d, sink);
+  run<8 | 16 | 64 | 512 | 2 | 4, 0x00410041u>("... with 4 poly pairs", d, sink);
+  run<8 | 128, 0x00080080u>("+ tcgen05.ld 6 KB per warp, .16x128b shape", d, sink);
+  run<8 | 256, 0x00080080u>("+ tcgen05.ld 6 KB per warp, .16x64b shape", d, sink);
   run<2, 0x00080080u>("+ 2 mbarrier ops", d, sink);
   run<4, 0x00080080u>("+ vote + shuffle", d, sink);
   run<7, 0x00080080u>("+ all of the above (the forward's mix)", d, sink);
