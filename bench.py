@@ -434,7 +434,7 @@ def main():
             extras["fwd"]["exp_roofline"] = {
                 "bound": "alu (MUFU ex2)", "achieved": exps / (fwd_ms * 1e-3) / 1e12, "peak": exp_peak / 1e12,
                 "unit": "Tex2/s", "frac": exps / (fwd_ms * 1e-3) / exp_peak,
-                "peak_basis": "16 exp/clk/SM x 148 SMs x %d MHz (max SM clock); 2 of 24 exponential pairs run on "
+                "peak_basis": "16 exp/clk/SM x 148 SMs x %d MHz (max SM clock); 1 of 24 exponential pairs runs on "
                               "the FMA pipe, so the frac can exceed the MUFU-only reading" % pk["sm_max_mhz"]}
             # with the scores' TMEM load and the P store each tile also needs, the exponential loop runs at
             # 18.2 cycles per pair per SM sub-partition (tools/micro/mio_mix.cu): the kernel's practical floor
