@@ -436,13 +436,14 @@ def main():
                 "unit": "Tex2/s", "frac": exps / (fwd_ms * 1e-3) / exp_peak,
                 "peak_basis": "16 exp/clk/SM x 148 SMs x %d MHz (max SM clock); 1 of 24 exponential pairs runs on "
                               "the FMA pipe, so the frac can exceed the MUFU-only reading" % pk["sm_max_mhz"]}
-            # with the scores' TMEM load and the P store each tile also needs, the exponential loop runs at
-            # 18.2 cycles per pair per SM sub-partition (tools/micro/mio_mix.cu): the kernel's practical floor
+            # with the scores' TMEM load and the P store each tile also needs (.16x256b / .16x128b shapes), the
+            # exponential loop runs at 16.3 cycles per pair per SM sub-partition (tools/micro/mio_mix.cu): the
+            # kernel's practical floor
             pairs_per_smsp = exps / 64 / (148 * 4)   # warp-wide pairs: 32 lanes x 2 exponentials
-            floor_ms = pairs_per_smsp * 18.2 / (pk["sm_max_mhz"] * 1e6) * 1e3
+            floor_ms = pairs_per_smsp * 16.3 / (pk["sm_max_mhz"] * 1e6) * 1e3
             extras["fwd"]["exp_roofline"].update({"practical_floor_ms": floor_ms, "frac_of_practical_floor": floor_ms / fwd_ms,
-                                                  "practical_floor_basis": "18.2 cycles per exp pair per SMSP incl. "
-                                                  "the per-tile tcgen05.ld of S / st of P, at the max SM clock"})
+                                                  "practical_floor_basis": "16.3 cycles per exp pair per SMSP incl. "
+                                                  "the per-tile tcgen05.ld of S (.16x256b) / st of P (.16x128b), at the max SM clock"})
         if a.dtype == "bf16":
             out32 = torch.empty(shape, dtype=torch.float32, device=dev)
             f32_ms = tmean(lambda: api.mea_attention_fwd(q, k, v, out=out32, lse=lse), max(3, a.steps // 2))
