@@ -4,8 +4,9 @@
 //
 // Same method as fwd_sm100a.cu (the paper's per-query stream, key chunk by
 // key chunk, Figure 1 lines 12-19 = PAPER.md:118-126; lazy rescale "as needed"), same
-// CTA shape (two 128-row query tiles of one (b, h), 16 softmax warps, a thread = one
-// row-half), but the key tile is 96 wide so that each query tile gets TWO score buffers:
+// CTA shape (two 128-row query tiles of one (b, h), 16 softmax warps of 16 rows each; here a
+// quad of threads shares two rows, see the softmax section), but the key tile is 96 wide so that
+// each query tile gets TWO score buffers:
 //
 //   TMEM (512 columns): S[qt][0] S[qt][1] = 4 x 96 columns at 0, 96, 192, 288;
 //                       O0 [384,448), O1 [448,512).
