@@ -284,27 +284,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     setmaxnreg_inc<kSoftmaxRegs>();
     // ------------------------------------------------------------ softmax warps
-    // 16 warps; warp (qt, sub, quarter) owns query tile qt, rows quarter*32 + sub*16 + [0,16).
-    // With the 16x32bx2 TMEM shape, lanes 0-15 hold score columns [0,64) of those rows and
-    // lanes 16-31 columns [64,128) of the same rows: the two halves of a row are lanes t and
-    // t^16 of one warp, so the row max and row sum combine with a single xor-shuffle. Every
-    // thread keeps the row's reference max m* (identical in both halves) and its half of s*.
+    // 16 warps; warp (qt, sub, quarter) owns query tile qt, TMEM lanes L0 = quarter*32 + sub*16
+    // + [0,16). S is read as .16x256b and P written as .16x128b (ptx.cuh, as fwd_db): thread t
+    // (q = t % 4) holds rows a = L0 + t/4 and b = a + 8, score columns 8r + 2q, 8r + 2q + 1
+    // (r = 0..15) of both — the keys of P column 4r + q it stores; a row is spread over a quad
+    // (max / sum: two xor-shuffles). Every thread keeps both rows' reference max m* (identical
+    // across the quad) and its part of their s*.
     const int sw = warp - 4;
     const int qt = sw >> 3;
     const int sub = (sw >> 2) & 1;
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    const int half = lane >> 4;
-    const int rloc = quarter * 32 + sub * 16 + (lane & 15);
-    const int row = q0 + qt * kTileM + rloc;
-    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32 + sub * 16) << 16);
+    const int q = lane & 3, ra = lane >> 2;
+    const int L0 = quarter * 32 + sub * 16;
+    const int row_a = q0 + qt * kTileM + L0 + ra, row_b = row_a + 8;
+    const uint32_t lane_base = tmem + ((uint32_t)L0 << 16);
     const uint32_t colS = col_s(qt), colO = col_o(qt), colP = col_p(qt);
     const float c = p.scale_log2;
-    float m_ref = -INFINITY;  // reference max m*, log2 units of the scaled score
-    float l = 0.f;            // this half's part of s*
+    float m_a = -INFINITY, m_b = -INFINITY;  // reference max m*, log2 units of the scaled score
+    float l_a = 0.f, l_b = 0.f;              // this thread's part of s*
 #ifdef MEA_EXP_TIMING
     unsigned long long* tdbg = reinterpret_cast<unsigned long long*>(p.lse);
-    const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && quarter == 0 && sub == 0 && (lane & 15) == 0;
-#define TPROBE(k) if (probe && t >= 8 && t < 24) tdbg[((qt * 2 + half) * 16 + (t - 8)) * 8 + (k)] = clock64();
+    const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && quarter == 0 && sub == 0 && lane == 0;
+#define TPROBE(k) if (probe && t >= 8 && t < 24) tdbg[(qt * 16 + (t - 8)) * 8 + (k)] = clock64();
 #else
 #define TPROBE(k)
 #endif
@@ -316,169 +317,190 @@ __global__ void __launch_bounds__(kThreads, 1)
       TPROBE(1)
       tc_fence_after();
       uint32_t sr[64];
-      // keys of this tile in range (causal: keys <= row)
-      const int tile_valid = (p.causal ? min(key_end, row + 1) : key_end) - (t_begin + t) * kTileN;
-      const int valid = tile_valid - half * 64;                // ... of my half (may be <= 0)
-      uint32_t pk[32];  // P in bf16 pairs
-      float ext = 0.f;
-      bool have_ext = false;
+      // keys of this tile in range per row (causal: keys <= row)
+      const int kb = (t_begin + t) * kTileN;
+      const int valid_a = (p.causal ? min(key_end, row_a + 1) : key_end) - kb;
+      const int valid_b = (p.causal ? min(key_end, row_b + 1) : key_end) - kb;
+      uint32_t pk[32];  // P in bf16 pairs: [2r] row a, [2r + 1] row b, column 4r + q
       // Fast path (full tile, m* already set): exponentiate against the current reference max.
-      // The second 32 score columns load while the first 32 are exponentiated.
-      bool fast = (t > 0) && (t != diag) && (key_end - (t_begin + t) * kTileN >= kTileN) && (c >= 0.f);
-      tmem_ld32_split<64>(lane_base + colS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      // The second 64 score columns load while the first 64 are exponentiated.
+      bool fast = (t > 0) && (t != diag) && (key_end - kb >= kTileN) && (c >= 0.f);
+      tmem_ld_16x256b_x8(lane_base + colS + 0, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
       if (fast) {
         tmem_ld_wait();
-        tmem_ld32_split<64>(lane_base + colS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-        const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
-        float2 rs = make_float2(0.f, 0.f);
+        tmem_ld_16x256b_x8(lane_base + colS + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+        const float2 c2 = make_float2(c, c), na2 = make_float2(-m_a, -m_a), nb2 = make_float2(-m_b, -m_b);
+        float2 rsa = make_float2(0.f, 0.f), rsb = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          if (i == 16) {  // second half of the scores has landed; S_t may now be overwritten
+        for (int r = 0; r < 16; ++r) {
+          if (r == 8) {  // second half of the scores has landed; S_t may now be overwritten
             tmem_ld_wait();
             tc_fence_before();
             mbar_arrive(&sm.s_loaded[qt]);
           }
-          const float2 s2 = make_float2(__uint_as_float(sr[2 * i]), __uint_as_float(sr[2 * i + 1]));
-          const float2 x = __ffma2_rn(s2, c2, nm2);  // s*c - m*
-          const float2 e = poly_pair(i) ? exp2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
-          rs = __fadd2_rn(rs, e);
-          pk[i] = pack_bf16x2(e.x, e.y);
+          const float2 sa = make_float2(__uint_as_float(sr[4 * r]), __uint_as_float(sr[4 * r + 1]));
+          const float2 sb = make_float2(__uint_as_float(sr[4 * r + 2]), __uint_as_float(sr[4 * r + 3]));
+          const float2 xa = __ffma2_rn(sa, c2, na2), xb = __ffma2_rn(sb, c2, nb2);  // s*c - m*
+          const float2 ea = poly_pair(2 * r) ? exp2_poly2(xa) : make_float2(ex2_approx(xa.x), ex2_approx(xa.y));
+          const float2 eb = poly_pair(2 * r + 1) ? exp2_poly2(xb) : make_float2(ex2_approx(xb.x), ex2_approx(xb.y));
+          rsa = __fadd2_rn(rsa, ea);
+          rsb = __fadd2_rn(rsb, eb);
+          pk[2 * r] = pack_bf16x2(ea.x, ea.y);
+          pk[2 * r + 1] = pack_bf16x2(eb.x, eb.y);
         }
         // No row max here: the max only guards overflow, and every term is
         // bounded by the row sum, so a finite row sum below 2^64 certifies that all
         // 2^(s c - m*) terms (and hence P in bf16 and the fp32 sums) are safe. Otherwise redo
         // the tile with the exact max (rare: the max must grow by > 2^64).
-        const float rsum = rs.x + rs.y;
-        const bool need = !(rsum <= kSafeSum);  // also catches inf / NaN
-        if (__any_sync(0xffffffffu, need)) {  // warp-uniform: covers both halves of these rows
+        const float suma = rsa.x + rsa.y, sumb = rsb.x + rsb.y;
+        const bool need = !(suma <= kSafeSum) || !(sumb <= kSafeSum);  // also catches inf / NaN
+        if (__any_sync(0xffffffffu, need)) {  // warp-uniform: covers every quad of these rows
           fast = false;  // redo from the raw scores (still in registers)
         } else {
-          l += rsum;
+          l_a += suma;
+          l_b += sumb;
         }
       } else {
-        tmem_ld32_split<64>(lane_base + colS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+        tmem_ld_16x256b_x8(lane_base + colS + 64, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&sm.s_loaded[qt]);  // S_t is in registers: the MMA may overwrite it
       }
       if (!fast) {
-        if (!have_ext) {
-          // row extremum of the raw score over valid keys: max if c >= 0, min if c < 0
-          float e0;
-          if (c >= 0.f) {
-            e0 = -INFINITY;
+        // row extremum of the raw score over valid keys: max if c >= 0, min if c < 0 (thread, quad)
+        float ea = c >= 0.f ? -INFINITY : INFINITY, eb = ea;
 #pragma unroll
-            for (int i = 0; i < 64; ++i)
-              if (i < valid) e0 = fmaxf(e0, __uint_as_float(sr[i]));
-            ext = fmaxf(e0, __shfl_xor_sync(0xffffffffu, e0, 16));
-          } else {
-            e0 = INFINITY;
+        for (int r = 0; r < 16; ++r)
 #pragma unroll
-            for (int i = 0; i < 64; ++i)
-              if (i < valid) e0 = fminf(e0, __uint_as_float(sr[i]));
-            ext = fminf(e0, __shfl_xor_sync(0xffffffffu, e0, 16));
+          for (int j = 0; j < 2; ++j) {
+            const int k = 8 * r + 2 * q + j;
+            const float sa = __uint_as_float(sr[4 * r + j]), sb = __uint_as_float(sr[4 * r + 2 + j]);
+            if (c >= 0.f) {
+              if (k < valid_a) ea = fmaxf(ea, sa);
+              if (k < valid_b) eb = fmaxf(eb, sb);
+            } else {
+              if (k < valid_a) ea = fminf(ea, sa);
+              if (k < valid_b) eb = fminf(eb, sb);
+            }
           }
+        if (c >= 0.f) {
+          ea = fmaxf(ea, __shfl_xor_sync(0xffffffffu, ea, 1));
+          ea = fmaxf(ea, __shfl_xor_sync(0xffffffffu, ea, 2));
+          eb = fmaxf(eb, __shfl_xor_sync(0xffffffffu, eb, 1));
+          eb = fmaxf(eb, __shfl_xor_sync(0xffffffffu, eb, 2));
+        } else {
+          ea = fminf(ea, __shfl_xor_sync(0xffffffffu, ea, 1));
+          ea = fminf(ea, __shfl_xor_sync(0xffffffffu, ea, 2));
+          eb = fminf(eb, __shfl_xor_sync(0xffffffffu, eb, 1));
+          eb = fminf(eb, __shfl_xor_sync(0xffffffffu, eb, 2));
         }
-        const float m_cand = ext * c;
-        const bool need = m_cand > m_ref + kLazyThreshold;  // always true on the first tile
-        float alpha = 1.f;
-        if (need) {
-          alpha = ex2_approx(m_ref - m_cand);  // 0 when m_ref = -inf
-          m_ref = m_cand;
-          l *= alpha;
+        const float mca = ea * c, mcb = eb * c;
+        const bool need_a = mca > m_a + kLazyThreshold, need_b = mcb > m_b + kLazyThreshold;  // always on the first tile
+        float alpha_a = 1.f, alpha_b = 1.f;
+        if (need_a) {
+          alpha_a = ex2_approx(m_a - mca);  // 0 when m* = -inf
+          m_a = mca;
+          l_a *= alpha_a;
         }
-        if (t > 0 && __any_sync(0xffffffffu, need)) {
-          // v* <- v* alpha (lanes 0-15: O columns [0,32), lanes 16-31: [32,64)), once PV_{t-1}
-          // has finished.
+        if (need_b) {
+          alpha_b = ex2_approx(m_b - mcb);
+          m_b = mcb;
+          l_b *= alpha_b;
+        }
+        if (t > 0 && __any_sync(0xffffffffu, need_a || need_b)) {
+          // v* <- v* alpha once PV_{t-1} has finished (O in the same .16x256b layout)
           mbar_wait(&sm.pv_done[qt], (t - 1) & 1);
           tc_fence_after();
+          uint32_t o[32];
+          tmem_ld_16x256b_x8(lane_base + colO, o);
+          tmem_ld_wait();
 #pragma unroll
-          for (int part = 0; part < 2; ++part) {
-            uint32_t o[16];
-            tmem_ld16_split<32>(lane_base + colO + part * 16, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16_split<32>(lane_base + colO + part * 16, o);
+          for (int r = 0; r < 8; ++r) {
+            o[4 * r] = __float_as_uint(__uint_as_float(o[4 * r]) * alpha_a);
+            o[4 * r + 1] = __float_as_uint(__uint_as_float(o[4 * r + 1]) * alpha_a);
+            o[4 * r + 2] = __float_as_uint(__uint_as_float(o[4 * r + 2]) * alpha_b);
+            o[4 * r + 3] = __float_as_uint(__uint_as_float(o[4 * r + 3]) * alpha_b);
           }
+          tmem_st_16x256b_x8(lane_base + colO, o);
         }
         // P = 2^(s c - m*) in bf16 pairs; s* += rowsum P
-        const float neg_m = -m_ref;
-        float rs0 = 0.f, rs1 = 0.f;
+        float sa0 = 0.f, sa1 = 0.f, sb0 = 0.f, sb1 = 0.f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float p0 = (2 * i < valid) ? ex2_approx(fmaf(__uint_as_float(sr[2 * i]), c, neg_m)) : 0.f;
-          const float p1 = (2 * i + 1 < valid) ? ex2_approx(fmaf(__uint_as_float(sr[2 * i + 1]), c, neg_m)) : 0.f;
-          rs0 += p0;
-          rs1 += p1;
-          pk[i] = pack_bf16x2(p0, p1);
+        for (int r = 0; r < 16; ++r) {
+          const int k = 8 * r + 2 * q;
+          const float pa0 = k < valid_a ? ex2_approx(fmaf(__uint_as_float(sr[4 * r]), c, -m_a)) : 0.f;
+          const float pa1 = k + 1 < valid_a ? ex2_approx(fmaf(__uint_as_float(sr[4 * r + 1]), c, -m_a)) : 0.f;
+          const float pb0 = k < valid_b ? ex2_approx(fmaf(__uint_as_float(sr[4 * r + 2]), c, -m_b)) : 0.f;
+          const float pb1 = k + 1 < valid_b ? ex2_approx(fmaf(__uint_as_float(sr[4 * r + 3]), c, -m_b)) : 0.f;
+          sa0 += pa0;
+          sa1 += pa1;
+          sb0 += pb0;
+          sb1 += pb1;
+          pk[2 * r] = pack_bf16x2(pa0, pa1);
+          pk[2 * r + 1] = pack_bf16x2(pb0, pb1);
         }
-        l += rs0 + rs1;
+        l_a += sa0 + sa1;
+        l_b += sb0 + sb1;
       }
       TPROBE(4)
       if (t > 0) mbar_wait(&sm.pv_done[qt], (t - 1) & 1);  // PV_{t-1} has consumed P_{t-1}
       tc_fence_after();
-      tmem_st32_split<32>(lane_base + colP, pk);
+      tmem_st_16x128b_x16(lane_base + colP, pk);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&sm.p_full[qt]);
       TPROBE(5)
     }
     // ------------------------------------------------------------ epilogue: out = v*/s*
-    const float lrow = l + __shfl_xor_sync(0xffffffffu, l, 16);  // s* of the whole row
+    l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);  // s* of the whole rows
+    l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
+    l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
+    l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
     mbar_wait(&sm.o_done[qt], 0);
     tc_fence_after();
-    uint32_t o[32];
-    tmem_ld32_split<32>(lane_base + colO, o);
+    uint32_t o[32];  // rows a, b; O columns 8r + 2q, 8r + 2q + 1 (r = 0..7)
+    tmem_ld_16x256b_x8(lane_base + colO, o);
     tmem_ld_wait();
     // PDL: the previous kernel (the last window's merge) reads the summaries this epilogue
     // overwrites; everything above (all of Q/K/V's streaming) overlapped its drain
     if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (row < q_end) {
+#pragma unroll
+    for (int hb = 0; hb < 2; ++hb) {
+      const int row = hb ? row_b : row_a;
+      if (row >= q_end) continue;
+      const float lrow = hb ? l_b : l_a, mrow = hb ? m_b : m_a;
       const size_t bh = (size_t)b * p.H + h;
+      auto put_f32 = [&](float* dst, float sc) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          *reinterpret_cast<float2*>(dst + 8 * r) =
+              make_float2(__uint_as_float(o[4 * r + 2 * hb]) * sc, __uint_as_float(o[4 * r + 2 * hb + 1]) * sc);
+      };
       if (p.tri_v) {
         // this call's (m*, s*, v*) per row, for a merge across key ranges
         const size_t idx = ((size_t)b * p.n_q + row) * p.H + h;
-        float4* dst = reinterpret_cast<float4*>(p.tri_v + idx * p.tri_vs + half * 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
-                               __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
-        if (half == 0) {
-          p.tri_m[idx * p.tri_ms] = m_ref * 0.6931471805599453f;
+        put_f32(p.tri_v + idx * p.tri_vs + 2 * q, 1.f);
+        if (q == 0) {
+          p.tri_m[idx * p.tri_ms] = mrow * 0.6931471805599453f;
           p.tri_s[idx * p.tri_ms] = lrow;
         }
       } else if (p.part_o) {  // key-split / tree summaries
         const size_t prow = ((size_t)split * p.B * p.H + bh) * p.q_count + (row - p.q_begin);
-        float4* dst = reinterpret_cast<float4*>(p.part_o + prow * kHeadDim + half * 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
-                               __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
-        if (half == 0) reinterpret_cast<float2*>(p.part_ml)[prow] = make_float2(m_ref, lrow);
+        put_f32(p.part_o + prow * kHeadDim + 2 * q, 1.f);
+        if (q == 0) reinterpret_cast<float2*>(p.part_ml)[prow] = make_float2(mrow, lrow);
       } else {
         const float inv = 1.f / lrow;
-        const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + half * 32;
+        const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kHeadDim + 2 * q;
         if (p.out_f32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            dst[i] = make_float4(__uint_as_float(o[4 * i]) * inv, __uint_as_float(o[4 * i + 1]) * inv,
-                                 __uint_as_float(o[4 * i + 2]) * inv, __uint_as_float(o[4 * i + 3]) * inv);
+          put_f32(static_cast<float*>(p.out) + off, inv);
         } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + off);
+          uint32_t* dst = reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(p.out) + off);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            uint4 w;
-            w.x = pack_bf16x2(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv);
-            w.y = pack_bf16x2(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv);
-            w.z = pack_bf16x2(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv);
-            w.w = pack_bf16x2(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv);
-            dst[i] = w;
-          }
+          for (int r = 0; r < 8; ++r)
+            dst[4 * r] = pack_bf16x2(__uint_as_float(o[4 * r + 2 * hb]) * inv, __uint_as_float(o[4 * r + 2 * hb + 1]) * inv);
         }
 #ifndef MEA_EXP_TIMING
-        if (p.lse && half == 0) p.lse[bh * p.n_q + row] = (m_ref + __log2f(lrow)) * 0.6931471805599453f;
+        if (p.lse && q == 0) p.lse[bh * p.n_q + row] = (mrow + __log2f(lrow)) * 0.6931471805599453f;
 #endif
       }
     }
