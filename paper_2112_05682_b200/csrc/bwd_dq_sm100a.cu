@@ -17,7 +17,7 @@
 // for dQ_{t-2} ("ds_free") before overwriting one.
 // Warps: 0 TMA producer (Q, dO once; 4-stage K/V ring), 1 MMA issuer, 2 TMEM allocator,
 // 4-19 softmax: warp (colhalf, sub, quarter) owns rows quarter*32 + sub*16 + [0,16) and key
-// columns colhalf*64 + [0,64), lanes 0-15 / 16-31 taking the two 32-column halves (16x32bx2).
+// columns colhalf*64 + [0,64) (.16x256b: a quad of threads holds two rows, see the softmax section).
 #include <cuda_bf16.h>
 
 #include "internal.h"
@@ -194,18 +194,27 @@ __global__ void __launch_bounds__(kQThreads, 1)
   } else {
     setmaxnreg_inc<kQSoftRegs>();
     // ------------------------------------------------------------------ softmax warps
+    // warp (colhalf, sub, quarter): TMEM lanes L0 = quarter*32 + sub*16 + [0,16), key columns
+    // colhalf * KT/2 + [0, KT/2). S and dP are read as .16x256b and dS written as .16x128b
+    // (ptx.cuh, as fwd_db): thread t (q = t % 4) holds rows a = L0 + t/4, b = a + 8 and key
+    // columns colhalf * KT/2 + 8r + 2q, + 1 — the keys of dS column colhalf * KT/4 + 4r + q.
     const int sw = warp - 4;
     const int colhalf = sw >> 3;
     const int sub = (sw >> 2) & 1;
     const int quarter = warp & 3;
-    const int rloc = quarter * 32 + sub * 16 + (lane & 15);
+    const int q = lane & 3, ra = lane >> 2;
+    const int L0 = quarter * 32 + sub * 16;
+    const int row_a = q0 + L0 + ra, row_b = row_a + 8;
+    const int rloc = quarter * 32 + sub * 16 + (lane & 15);  // the epilogue's row (16x32bx2 layout)
     const int row = q0 + rloc;
-    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32 + sub * 16) << 16);
+    const uint32_t lane_base = tmem + ((uint32_t)L0 << 16);
     const float c = p.scale_log2;
     const float2 c2 = make_float2(c, c);
-    const float lse2 = p.lse2[bh * nq_pad + q0 + rloc];   // +inf on padded rows -> P = 0
-    const float delta = p.delta[bh * nq_pad + q0 + rloc];
-    const float2 nl2 = make_float2(-lse2, -lse2), nd2 = make_float2(-delta, -delta);
+    // +inf lse2 on padded rows -> P = 0
+    const float lse2_a = p.lse2[bh * nq_pad + q0 + L0 + ra], lse2_b = p.lse2[bh * nq_pad + q0 + L0 + ra + 8];
+    const float delta_a = p.delta[bh * nq_pad + q0 + L0 + ra], delta_b = p.delta[bh * nq_pad + q0 + L0 + ra + 8];
+    const float2 nla = make_float2(-lse2_a, -lse2_a), nlb = make_float2(-lse2_b, -lse2_b);
+    const float2 nda = make_float2(-delta_a, -delta_a), ndb = make_float2(-delta_b, -delta_b);
 #ifdef MEA_EXP_TIMING
     unsigned long long* tdbg = reinterpret_cast<unsigned long long*>(p.dq);
     const bool probe = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && quarter == 0 && sub == 0 && lane == 0;
@@ -213,52 +222,54 @@ __global__ void __launch_bounds__(kQThreads, 1)
 #else
 #define TPROBE(k)
 #endif
+    constexpr int NR = KT / 16;  // .16x256b repetitions over this warp's KT/2 key columns
     for (int t = 0; t < T; ++t) {
       TPROBE(0)
       mbar_wait(&sm.s_full, t & 1);
       TPROBE(1)
       tc_fence_after();
-      constexpr int NE = KT / 4;  // key columns per thread: colhalf * KT/2 + (lane >> 4) * KT/4 + [0, NE)
-      uint32_t sr[NE], dr[NE];
-      if constexpr (NE == 32) {
-        tmem_ld32_split<32>(lane_base + kColS + colhalf * 64, sr);
-        tmem_ld32_split<32>(lane_base + kColDP + colhalf * 64, dr);
+      uint32_t sr[4 * NR], dr[4 * NR];
+      if constexpr (NR == 8) {
+        tmem_ld_16x256b_x8(lane_base + kColS + colhalf * (KT / 2), sr);
+        tmem_ld_16x256b_x8(lane_base + kColDP + colhalf * (KT / 2), dr);
       } else {
-        tmem_ld16_split<16>(lane_base + kColS + colhalf * 32, sr);
-        tmem_ld16_split<16>(lane_base + kColDP + colhalf * 32, dr);
+        tmem_ld_16x256b_x4(lane_base + kColS + colhalf * (KT / 2), sr);
+        tmem_ld_16x256b_x4(lane_base + kColDP + colhalf * (KT / 2), dr);
       }
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&sm.s_loaded);  // S_t, dP_t are in registers: the next scores may overwrite them
       TPROBE(2)
-      uint32_t pk[NE / 2];
+      uint32_t pk[2 * NR];  // [2r] row a, [2r + 1] row b: dS column colhalf * KT/4 + 4r + q
 #pragma unroll
-      for (int u = 0; u < NE / 2; ++u) {
-        const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
-        const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
-        const float2 x = __ffma2_rn(s2, c2, nl2);                              // s c - lse2
-        float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));             // P
-        if (p.causal) {  // key t KT + col > query row: masked
-          const int key = t * KT + colhalf * (KT / 2) + (lane >> 4) * (KT / 4) + 2 * u;
-          if (key > row) pr.x = 0.f;
-          if (key + 1 > row) pr.y = 0.f;
+      for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int hb = 0; hb < 2; ++hb) {
+          const float2 s2 = make_float2(__uint_as_float(sr[4 * r + 2 * hb]), __uint_as_float(sr[4 * r + 2 * hb + 1]));
+          const float2 d2 = make_float2(__uint_as_float(dr[4 * r + 2 * hb]), __uint_as_float(dr[4 * r + 2 * hb + 1]));
+          const float2 x = __ffma2_rn(s2, c2, hb ? nlb : nla);                   // s c - lse2
+          float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));             // P
+          const int key = t * KT + colhalf * (KT / 2) + 8 * r + 2 * q;
+          if (p.causal) {  // key > query row: masked
+            const int rr = hb ? row_b : row_a;
+            if (key > rr) pr.x = 0.f;
+            if (key + 1 > rr) pr.y = 0.f;
+          }
+          if (p.kv_lens) {  // key padding: keys >= nk masked
+            if (key >= nk) pr.x = 0.f;
+            if (key + 1 >= nk) pr.y = 0.f;
+          }
+          const float2 ds = __fmul2_rn(pr, __fadd2_rn(d2, hb ? ndb : nda));      // P (dP - delta)
+          pk[2 * r + hb] = pack_bf16x2(ds.x, ds.y);
         }
-        if (p.kv_lens) {  // key padding: keys >= nk masked
-          const int key = t * KT + colhalf * (KT / 2) + (lane >> 4) * (KT / 4) + 2 * u;
-          if (key >= nk) pr.x = 0.f;
-          if (key + 1 >= nk) pr.y = 0.f;
-        }
-        const float2 ds = __fmul2_rn(pr, __fadd2_rn(d2, nd2));                 // P (dP - delta)
-        pk[u] = pack_bf16x2(ds.x, ds.y);
-      }
       TPROBE(3)
       if (t > 1) mbar_wait(&sm.ds_free[t & 1], ((t >> 1) - 1) & 1);  // dQ_{t-2} has consumed this buffer
       TPROBE(4)
       tc_fence_after();
-      if constexpr (NE == 32) {
-        tmem_st16_split<16>(lane_base + col_ds(t & 1) + colhalf * 32, pk);
+      if constexpr (NR == 8) {
+        tmem_st_16x128b_x8(lane_base + col_ds(t & 1) + colhalf * (KT / 4), pk);
       } else {
-        tmem_st8_split<8>(lane_base + col_ds(t & 1) + colhalf * 16, pk);
+        tmem_st_16x128b_x4(lane_base + col_ds(t & 1) + colhalf * (KT / 4), pk);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -267,14 +278,16 @@ __global__ void __launch_bounds__(kQThreads, 1)
     }
     // ------------------------------------------------------------------ epilogue: dq = scale dQ
     // thread (colhalf, lane half) writes dQ columns colhalf * D/2 + (lane >> 4) * D/4 + [0, D/4)
+    // of row `row` (the 16x32bx2 layout: lanes t and t + 16 share a row)
+    const uint32_t lane_base16 = tmem + ((uint32_t)(quarter * 32 + sub * 16) << 16);
     mbar_wait(&sm.o_done, 0);
     tc_fence_after();
     constexpr int kW = D / 4;  // columns per thread
     uint32_t o[kW];
     if constexpr (D == 64) {
-      tmem_ld16_split<16>(lane_base + kColDQ + colhalf * 32, o);
+      tmem_ld16_split<16>(lane_base16 + kColDQ + colhalf * 32, o);
     } else {
-      tmem_ld32_split<32>(lane_base + kColDQ + colhalf * 64, o);
+      tmem_ld32_split<32>(lane_base16 + kColDQ + colhalf * 64, o);
     }
     tmem_ld_wait();
 #ifdef MEA_EXP_TIMING
