@@ -383,7 +383,11 @@ def main():
     if not a.no_extras and a.workload == "cfg3":
         # ---------------- HBM: read-only probe (the single query's roofline) + single query + decode batch,
         # measured first among the extras, before the compute-bound extras heat the board into its
-        # power cap (the latency-bound parts of a 50 us call run on the SM clock)
+        # power cap (the latency-bound parts of a 50 us call run on the SM clock), and after a short
+        # idle so the headline step's power-cap clock has recovered (decode-shaped calls do not run
+        # on a board that has just drawn 1 kW for the training step)
+        torch.cuda.synchronize()
+        time.sleep(0.5)
         buf = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
         probe_ms = statistics.median(timed(lambda: api.debug_read_probe(buf, 296), 10, 2))
         read_gbs = buf.numel() / (probe_ms * 1e-3) / 1e9
