@@ -334,8 +334,9 @@ def main():
         return [e0.elapsed_time(e1) for e0, e1 in evs]
 
     def tmean(fn, steps, warmup=1):
-        """mean event time of fn over `steps` (ms), max over ranks"""
-        return max_over_ranks(statistics.mean(timed(fn, steps, warmup)))
+        """median event time of fn over `steps` (ms), max over ranks (the extras: a median, so one
+        stalled call among a few does not move the number; the headline step keeps its own timing)"""
+        return max_over_ranks(statistics.median(timed(fn, steps, warmup)))
 
     # ---------------- the timed step (headline)
     for _ in range(a.warmup):
