@@ -26,6 +26,8 @@
 // warpgroup g owns query columns [32g, 32g+32) of each tile; thread = key row), 20-23 dQ drain.
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -270,6 +272,7 @@ __global__ void __launch_bounds__(kBThreads, 1)
     const int quarter = warp & 3;
     const int j = quarter * 32 + lane;       // key row within the tile (TMEM lane)
     const bool key_ok = k0 + j < (kPad ? keys_of(p.kv_lens, b, p.n_k) : p.n_k);  // padding: P = 0 -> dK = dV = 0
+    const bool keys_all_ok = __all_sync(0xffffffffu, key_ok);
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     const float c = p.scale_log2;
     const float2 c2 = make_float2(c, c);
@@ -297,23 +300,30 @@ __global__ void __launch_bounds__(kBThreads, 1)
       mbar_arrive(&sm.s_loaded);  // ST_i / dPT_i are in registers: the next scores may overwrite
       const bool diag = p.causal && i == 0;
       uint32_t pk[16], dk[16];
+      auto tile = [&](auto masked) {
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
-        const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
-        const float2 x = __fmul2_rn(s2, c2);  // c (s - lse/scale) = s c - lse log2 e
-        // P (padded query rows: lse/scale = +-inf -> 0). MUFU for every pair: moving some pairs
-        // to the FMA-pipe polynomial measured +-1 % here (MUFU is not what bounds this kernel).
-        float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-        if (!key_ok) pr = make_float2(0.f, 0.f);
-        if (diag) {  // causal diagonal tile: key j > query (32 g + 2 u + {0, 1}) is masked
-          if (j > 32 * g + 2 * u) pr.x = 0.f;
-          if (j > 32 * g + 2 * u + 1) pr.y = 0.f;
+        for (int u = 0; u < 16; ++u) {
+          const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
+          const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
+          const float2 x = __fmul2_rn(s2, c2);  // c (s - lse/scale) = s c - lse log2 e
+          // P (padded query rows: lse/scale = +-inf -> 0). MUFU for every pair: moving some pairs
+          // to the FMA-pipe polynomial measured +-1 % here (MUFU is not what bounds this kernel).
+          float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          if constexpr (decltype(masked)::value) {
+            if (!key_ok) pr = make_float2(0.f, 0.f);
+            if (diag) {  // causal diagonal tile: key j > query (32 g + 2 u + {0, 1}) is masked
+              if (j > 32 * g + 2 * u) pr.x = 0.f;
+              if (j > 32 * g + 2 * u + 1) pr.y = 0.f;
+            }
+          }
+          const float2 ds = __fmul2_rn(pr, d2);  // P (dP - delta)
+          pk[u] = pack_bf16x2(pr.x, pr.y);
+          dk[u] = pack_bf16x2(ds.x, ds.y);
         }
-        const float2 ds = __fmul2_rn(pr, d2);  // P (dP - delta)
-        pk[u] = pack_bf16x2(pr.x, pr.y);
-        dk[u] = pack_bf16x2(ds.x, ds.y);
-      }
+      };
+      // no per-element selects unless this warp's tile has padded keys or is a causal diagonal
+      if (diag || !keys_all_ok) tile(std::true_type{});
+      else tile(std::false_type{});
       TPROBE(2)
       if (i > 0) mbar_wait(&sm.p_free, (i - 1) & 1);  // tile i-1's MMAs no longer read P / dS
       TPROBE(3)
