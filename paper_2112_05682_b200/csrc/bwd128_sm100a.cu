@@ -28,6 +28,8 @@
 // halves x four lane quarters; thread = key row, 32 query columns), 12-15 dQ drain.
 #include <cuda_bf16.h>
 
+#include <type_traits>
+
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -228,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int j = quarter * 32 + lane;       // key row within the tile (TMEM lane)
     const bool key_ok = k0 + j < (kPad ? keys_of(p.kv_lens, b, p.n_k) : p.n_k);
+    const bool keys_all_ok = __all_sync(0xffffffffu, key_ok);
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     const float c = p.scale_log2;
     const float2 c2 = make_float2(c, c);
@@ -247,23 +250,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int qbase = (i0 + i) * QT + 32 * g;                     // this thread's first query column
       const bool overlap = p.causal && (i0 + i) * QT < k0 + KT;     // tile crosses the diagonal
       uint32_t pk[16], dk[16];
+      auto tile = [&](auto masked) {
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
-        const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
-        const float2 lq = *reinterpret_cast<const float2*>(l2 + 2 * u);
-        const float2 de = *reinterpret_cast<const float2*>(dl + 2 * u);
-        const float2 x = __ffma2_rn(s2, c2, make_float2(-lq.x, -lq.y));  // s c - lse2
-        float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));        // P (padded rows: lse2 = +inf -> 0)
-        if (!key_ok) pr = make_float2(0.f, 0.f);
-        if (overlap) {  // causal: key k0 + j > query qbase + 2u (+1) is masked
-          if (k0 + j > qbase + 2 * u) pr.x = 0.f;
-          if (k0 + j > qbase + 2 * u + 1) pr.y = 0.f;
+        for (int u = 0; u < 16; ++u) {
+          const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
+          const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
+          const float2 lq = *reinterpret_cast<const float2*>(l2 + 2 * u);
+          const float2 de = *reinterpret_cast<const float2*>(dl + 2 * u);
+          const float2 x = __ffma2_rn(s2, c2, make_float2(-lq.x, -lq.y));  // s c - lse2
+          float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));        // P (padded rows: lse2 = +inf -> 0)
+          if constexpr (decltype(masked)::value) {
+            if (!key_ok) pr = make_float2(0.f, 0.f);
+            if (overlap) {  // causal: key k0 + j > query qbase + 2u (+1) is masked
+              if (k0 + j > qbase + 2 * u) pr.x = 0.f;
+              if (k0 + j > qbase + 2 * u + 1) pr.y = 0.f;
+            }
+          }
+          const float2 ds = __fmul2_rn(pr, __fadd2_rn(d2, make_float2(-de.x, -de.y)));  // P (dP - delta)
+          pk[u] = pack_bf16x2(pr.x, pr.y);
+          dk[u] = pack_bf16x2(ds.x, ds.y);
         }
-        const float2 ds = __fmul2_rn(pr, __fadd2_rn(d2, make_float2(-de.x, -de.y)));  // P (dP - delta)
-        pk[u] = pack_bf16x2(pr.x, pr.y);
-        dk[u] = pack_bf16x2(ds.x, ds.y);
-      }
+      };
+      // no per-element selects unless this warp has padded keys or the tile crosses the diagonal
+      if (overlap || !keys_all_ok) tile(std::true_type{});
+      else tile(std::false_type{});
       if (i > 0) mbar_wait(&sm.p_free, (i - 1) & 1);  // tile i-1's MMAs no longer read P / dS
       tc_fence_after();
       tmem_st16(lane_base + kColP + g * 16, pk);
