@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kThreads128, 1)
       if (half == 0) reinterpret_cast<float2*>(p.part_ml)[prow] = make_float2(m_ref, lrow);
     } else if (row < q_end) {
       const size_t bh = (size_t)b * p.H + h;
-      const float inv = 1.f / lrow;
+      const float inv = lrow > 0.f ? 1.f / lrow : 0.f;  // a row with no keys (padding): out = 0, lse = -inf
       const size_t off = (((size_t)b * p.n_q + row) * p.H + h) * kD + half * 64;
       if (p.out_f32) {
         float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + off);

@@ -6,6 +6,7 @@ for the oracle; the point is breadth — a schedule or mask combination that bre
 even if no hand-written case hits it.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -16,11 +17,13 @@ from tests import helpers as Hh
 
 pytestmark = pytest.mark.gpu
 
-N_CASES = 150
+# MEA_FUZZ_CASES / MEA_FUZZ_BASE widen the sweep for a soak run (defaults: the 150 committed cases)
+N_CASES = int(os.environ.get("MEA_FUZZ_CASES", "150"))
+BASE = int(os.environ.get("MEA_FUZZ_BASE", "1000"))
 
 
 def _case(i):
-    r = np.random.default_rng(1000 + i)
+    r = np.random.default_rng(BASE + i)
     d = int(r.choice([64, 128]))
     B, H = int(r.integers(1, 3)), int(r.integers(1, 3))
     n_q, n_k = int(r.integers(1, 520)), int(r.integers(1, 700))

@@ -38,12 +38,15 @@ def test_padded_forward_matches_oracle(d, B, n_q, n_k, H, lens):
         assert np.abs(lse[b:b + 1] - ref_lse).max() < 1e-3
 
 
-def test_padded_forward_empty_batch_element():
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
+def test_padded_forward_empty_batch_element(d, out_dtype):
     from paper_2112_05682_b200 import api
-    B, n, H, d = 2, 200, 2, 64
+    B, n, H = 2, 200, 2
     q, k, v = Hh.host_inputs(B, n, n, H, d, seed=52)
     out, lse = api.mea_attention_fwd_padded(Hh.to_dev(q, torch.bfloat16), Hh.to_dev(k, torch.bfloat16),
-                                            Hh.to_dev(v, torch.bfloat16), _lens([0, 150]), want_lse=True)
+                                            Hh.to_dev(v, torch.bfloat16), _lens([0, 150]), want_lse=True,
+                                            out_dtype=out_dtype)
     torch.cuda.synchronize()
     assert (out[0] == 0).all() and torch.isinf(lse[0]).all() and (lse[0] < 0).all()
     ref, _ = O.mha_forward(q[1:], k[1:, :150], v[1:, :150], 1 / math.sqrt(d))
