@@ -89,20 +89,30 @@ def test_forward_and_backward_random_case(i):
         for b in range(B):
             L = lens[b] if mode == "padded" else n_k
             rq, rk, rv = O.mha_backward(q[b:b + 1], k[b:b + 1, :L], v[b:b + 1, :L], do[b:b + 1], scale, causal=causal)
+            # the relative-norm guard on dq / dk widens like their absolute bar (reading 16): the
+            # bf16 roundings of out (in delta = dO . out) and of dS cancel against dP in peaked rows
+            # (soak case 766 of MEA_FUZZ_BASE=40000 — d = 128, n = 6, causal, scale 0.5 — is 3.0 % off
+            # for the kernel and for fp64 arithmetic with only out and dS rounded to bf16 alike,
+            # tools/dbg_case766.py)
+            gw = max(1.0, abs(scale) * math.sqrt(d))
+            rel = {"dq": Hh.REL_NORM_GRAD * gw, "dk": Hh.REL_NORM_GRAD * gw, "dv": Hh.REL_NORM_GRAD}
             for g, r, nm in ((dq[b:b + 1], rq, "dq"), (dk[b:b + 1, :L], rk, "dk"), (dv[b:b + 1, :L], rv, "dv")):
-                Hh.assert_close_bf16(g, r, abs_tol=gtol if nm != "dv" else Hh.TOL_BF16_GRAD, rel_tol=Hh.REL_NORM_GRAD,
+                Hh.assert_close_bf16(g, r, abs_tol=gtol if nm != "dv" else Hh.TOL_BF16_GRAD, rel_tol=rel[nm],
                                      strict=nm == "dv" or gtol == Hh.TOL_BF16_GRAD,
                                      what=f"case {i} {nm}")
             if L < n_k:
                 assert (dk[b, L:] == 0).all() and (dv[b, L:] == 0).all()
 
 
-@pytest.mark.parametrize("i", range(60))
+N_OTHER = int(os.environ.get("MEA_FUZZ_OTHER_CASES", "60"))
+
+
+@pytest.mark.parametrize("i", range(N_OTHER))
 def test_other_entry_points_random_case(i):
     """Single query (bf16 d 64/128, f32), key-range partials merged, the deterministic backward
     and the fp32 forwards (exact SIMT and split-precision) on random shapes."""
     from paper_2112_05682_b200 import api
-    r = np.random.default_rng(5000 + i)
+    r = np.random.default_rng(BASE + 4000 + i)
     kind = ["single_query", "partial_merge", "bwd_det", "f32"][i % 4]
     d = int(r.choice([64, 128]))
     B, H = int(r.integers(1, 3)), int(r.integers(1, 4))
