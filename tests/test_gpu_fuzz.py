@@ -20,13 +20,14 @@ pytestmark = pytest.mark.gpu
 # MEA_FUZZ_CASES / MEA_FUZZ_BASE widen the sweep for a soak run (defaults: the 150 committed cases)
 N_CASES = int(os.environ.get("MEA_FUZZ_CASES", "150"))
 BASE = int(os.environ.get("MEA_FUZZ_BASE", "1000"))
+NMAX = int(os.environ.get("MEA_FUZZ_NMAX", "0"))   # > 0: lengths up to NMAX instead of 520 / 700
 
 
 def _case(i):
     r = np.random.default_rng(BASE + i)
     d = int(r.choice([64, 128]))
     B, H = int(r.integers(1, 3)), int(r.integers(1, 3))
-    n_q, n_k = int(r.integers(1, 520)), int(r.integers(1, 700))
+    n_q, n_k = int(r.integers(1, NMAX or 520)), int(r.integers(1, NMAX or 700))
     scale = float(r.choice([1 / math.sqrt(d), 0.5, -0.2, 0.0, 0.02]))
     mode = str(r.choice(["plain", "chunks", "causal", "padded", "tree"]))
     out_f32 = bool(r.integers(0, 2))
