@@ -163,3 +163,37 @@ def test_single_query_head_blocks_and_split_counts(d):
     finally:
         api.debug_set_option("sq_heads_per_cta", 0)
         api.debug_set_option("sq_ctas_per_sm", 0)
+
+
+N_SQ_FUZZ = int(__import__("os").environ.get("MEA_SQ_FUZZ_CASES", "12"))
+
+
+@pytest.mark.parametrize("i", range(N_SQ_FUZZ))
+def test_single_query_random_batches(i):
+    """Seeded random decode-shaped batches: B up to 16, H up to 40, n_k log-uniform up to 2^18
+    (B H n_k d capped at 2^26 elements), d in {64, 128}, scales of either sign; every call on a
+    reused workspace; the oracle on up to 6 sampled (b, h) rows, at the fp32-output bar of
+    test_config2_single_query_full. MEA_SQ_FUZZ_CASES widens it for a soak run."""
+    from paper_2112_05682_b200 import api
+    r = np.random.default_rng(90000 + i)
+    d = int(r.choice([64, 128]))
+    n_k = max(1, int(2.0 ** r.uniform(0, 18)))
+    B = int(r.integers(1, 17))
+    H = int(r.integers(1, 41))
+    while B * H * n_k * d > 1 << 26 and B * H > 1:
+        B, H = max(1, B // 2), max(1, H - (H + 1) // 3)
+    n_k = min(n_k, (1 << 26) // (B * H * d))
+    scale = float(r.choice([1 / math.sqrt(d), -0.3, 0.05, 0.0]))
+    q, k, v = _sq_inputs(B, H, n_k, d, seed=i + 77)
+    qd, kd, vd = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v))
+    ws = torch.empty(api.mea_single_query_workspace_size(B, H, n_k, d, api.MEA_BF16), dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        out = api.mea_single_query_fwd(qd, kd, vd, scale=scale, out_dtype=torch.float32, workspace=ws)
+    torch.cuda.synchronize()
+    got = out.double().cpu().numpy()
+    pairs = {(int(r.integers(0, B)), int(r.integers(0, H))) for _ in range(6)}
+    for b, h in sorted(pairs):
+        ref = O.naive(q[b, h][None], k[b, :, h], v[b, :, h], scale)[0][0]
+        err = np.abs(got[b, h] - ref)
+        assert (err <= 1e-3 * np.abs(ref) + 1e-5).all(), \
+            f"case {i} B={B} H={H} n_k={n_k} d={d} scale={scale} (b, h)=({b}, {h}): {err.max():.3e}"
