@@ -165,7 +165,7 @@ def test_single_query_head_blocks_and_split_counts(d):
         api.debug_set_option("sq_ctas_per_sm", 0)
 
 
-N_SQ_FUZZ = int(__import__("os").environ.get("MEA_SQ_FUZZ_CASES", "12"))
+N_SQ_FUZZ = int(__import__("os").environ.get("MEA_SQ_FUZZ_CASES", "6"))
 
 
 @pytest.mark.parametrize("i", range(N_SQ_FUZZ))
