@@ -1,10 +1,13 @@
-"""The bench.py JSON contract, checked on CPU through the reference arm (the float64 oracle on a
-bounded sample): one JSON line with the driver's keys, the same metric / config as the mea arm,
-and the reference-arm extras (impl, cpu_baseline, e2e with zero copies)."""
+"""The bench.py JSON contract: on CPU through the reference arm (the float64 oracle on a bounded
+sample) — one JSON line with the driver's keys, the same metric / config as the mea arm, and the
+reference-arm extras (impl, cpu_baseline, e2e with zero copies); on the GPU (marked gpu) through
+the mea arm's headline step (roofline, e2e with host copies, clocks, kernel-launch count)."""
 import json
 import os
 import subprocess
 import sys
+
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -43,3 +46,28 @@ def test_gpus_flag_must_match_world_size():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
                         "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 2 and "WORLD_SIZE" in r.stderr
+
+
+@pytest.mark.gpu
+def test_mea_arm_prints_one_contract_line():
+    """The mea arm on the GPU (headline step only, no CPU baseline): one JSON line with the
+    driver's keys, the roofline / e2e / clocks objects and a positive kernel-launch count."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3",
+                        "--no-extras", "--no-cpu-baseline"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "clocks", "gpu_launches"):
+        assert key in d, key
+    assert d["metric"] == "attention TFLOP/s (fwd 4*n^2*d + bwd 10*n^2*d per head)"
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
+    assert d["config"]["workload"].startswith("cfg3+cfg4") and d["config"]["n"] == 16384
+    rf = d["roofline"]
+    assert rf["bound"] in ("tensor", "hbm", "alu") and rf["achieved"] > 0 and rf["peak"] > 0
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    assert d["gpu_launches"] > 0
