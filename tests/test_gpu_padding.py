@@ -53,6 +53,28 @@ def test_padded_forward_empty_batch_element(d, out_dtype):
     Hh.assert_close_bf16(out[1:].double().cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("d,lse_given", [(64, True), (64, False), (128, True), (128, False)])
+def test_padded_backward_empty_batch_element(d, lse_given):
+    """A batch element with no keys: its dq, dk and dv are exactly 0 (P = 0 everywhere, and the
+    recomputed lse is -inf), the other element matches the oracle."""
+    from paper_2112_05682_b200 import api
+    B, n, H = 2, 200, 2
+    lens = [0, 150]
+    q, k, v, do = Hh.host_inputs(B, n, n, H, d, seed=54, with_dout=True)
+    qd, kd, vd, dod = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v, do))
+    kl = _lens(lens)
+    out, lse = api.mea_attention_fwd_padded(qd, kd, vd, kl, want_lse=True)
+    dq, dk, dv = api.mea_attention_bwd_padded(qd, kd, vd, out, dod, kl, lse=lse if lse_given else None)
+    torch.cuda.synchronize()
+    for x, nm in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+        assert (x[0] == 0).all(), f"{nm} of the empty element"
+        assert (x[1, 150:] == 0).all() if nm != "dq" else True
+    dq, dk, dv = (x.double().cpu().numpy() for x in (dq, dk, dv))
+    rq, rk, rv = O.mha_backward(q[1:], k[1:, :150], v[1:, :150], do[1:], 1 / math.sqrt(d))
+    for got, ref, nm in ((dq[1:], rq, "dq"), (dk[1:, :150], rk, "dk"), (dv[1:, :150], rv, "dv")):
+        Hh.assert_close_bf16(got, ref, abs_tol=Hh.TOL_BF16_GRAD, rel_tol=Hh.REL_NORM_GRAD, what=nm)
+
+
 @pytest.mark.parametrize("d,lse_given", [(64, True), (64, False), (128, True)])
 def test_padded_backward_matches_oracle(d, lse_given):
     from paper_2112_05682_b200 import api
