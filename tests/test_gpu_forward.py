@@ -222,3 +222,26 @@ def test_config5_length_sampled_rows():
     ref, ref_lse = O.naive(qr, kk, vv, 1 / 8)
     Hh.assert_close_bf16(out[0, rows, 0].double().cpu().numpy(), ref)
     assert np.abs(lse[0, 0, rows].double().cpu().numpy() - ref_lse).max() < 1e-3
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_many_heads_tiny_lengths(d):
+    """B H = 1536 (b, h) pairs of a few rows each: grid indexing over b and h, ragged single tiles,
+    forward (plain and causal) and backward against the oracle."""
+    from paper_2112_05682_b200 import api
+    B, H, n = 32, 48, 5
+    q, k, v, do = Hh.host_inputs(B, n, n, H, d, seed=61, with_dout=True)
+    qd, kd, vd, dod = (Hh.to_dev(x, torch.bfloat16) for x in (q, k, v, do))
+    scale = 1 / math.sqrt(d)
+    for causal in (False, True):
+        fwd = api.mea_attention_fwd_causal if causal else api.mea_attention_fwd
+        bwd = api.mea_attention_bwd_causal if causal else api.mea_attention_bwd
+        out, lse = fwd(qd, kd, vd, want_lse=True)
+        dq, dk, dv = bwd(qd, kd, vd, out, dod, lse=lse)
+        torch.cuda.synchronize()
+        ref, ref_lse = O.mha_forward(q, k, v, scale, causal=causal)
+        Hh.assert_close_bf16(out.double().cpu().numpy(), ref, what=f"out causal={causal}")
+        assert np.abs(lse.double().cpu().numpy() - ref_lse).max() < 1e-3
+        for got, r, nm in zip((dq, dk, dv), O.mha_backward(q, k, v, do, scale, causal=causal), ("dq", "dk", "dv")):
+            Hh.assert_close_bf16(got.double().cpu().numpy(), r, abs_tol=Hh.TOL_BF16_GRAD, rel_tol=Hh.REL_NORM_GRAD,
+                                 what=f"{nm} causal={causal}")
