@@ -306,8 +306,9 @@ __global__ void __launch_bounds__(kBThreads, 1)
           const float2 s2 = make_float2(__uint_as_float(sr[2 * u]), __uint_as_float(sr[2 * u + 1]));
           const float2 d2 = make_float2(__uint_as_float(dr[2 * u]), __uint_as_float(dr[2 * u + 1]));
           const float2 x = __fmul2_rn(s2, c2);  // c (s - lse/scale) = s c - lse log2 e
-          // P (padded query rows: lse/scale = +-inf -> 0). MUFU for every pair: moving some pairs
-          // to the FMA-pipe polynomial measured +-1 % here (MUFU is not what bounds this kernel).
+          // P (padded query rows: lse/scale = +-inf -> 0). MUFU for every pair: moving 2 or 4 of
+          // the 16 pairs to the FMA-pipe polynomial measured +2.5 to +3.7 % (the longer
+          // instruction stream costs more than the MUFU queue; profiles/r02_bwd_ab_poly.txt).
           float2 pr = make_float2(ex2_approx(x.x), ex2_approx(x.y));
           if constexpr (decltype(masked)::value) {
             if (!key_ok) pr = make_float2(0.f, 0.f);
