@@ -35,8 +35,9 @@ int g_sq_l2_256 = 1;          // L2::256B prefetch hint on the K/V loads
 int g_sq_static_pct = -1;     // keys in static per-CTA ranges (%), the rest a dynamic pool (-1: auto)
 
 #ifdef MEA_SQ_TIMING
-// timeline probe build only: per CTA {start, streaming done, record written, merge done} (ns)
-__device__ unsigned long long g_sq_times[8192][4];
+// timeline probe build only: per CTA {start, streaming done, record written, merge done, ticket
+// taken (merging CTA), merge loads done, merge combined} (ns)
+__device__ unsigned long long g_sq_times[8192][8];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -145,6 +146,7 @@ __device__ void merge_group(const SqParams& p, const float* __restrict__ rec, in
     sm_l[j * O + o] = l;
     sm_a[j * O + o] = a;
   }
+  SQ_T(5)
   __syncthreads();
   for (int o = threadIdx.x; o < O; o += NT) {
     float M = -INFINITY;
@@ -220,6 +222,7 @@ __device__ __forceinline__ void finish_cta(const SqParams& p, int group, int bh0
   }
   __syncthreads();
   if (!s_last) return;
+  SQ_T(4)
   merge_group<NT>(p, p.rec, bh0, HC, d, smem);
   if (threadIdx.x == 0) {   // every CTA of the group has arrived (and made its last claim)
     p.tickets[group] = kClean << 24;
@@ -645,7 +648,7 @@ cudaError_t launch_merge_partials(const float* m, const float* s, const float* v
 
 #ifdef MEA_SQ_TIMING
 extern "C" __attribute__((visibility("default"))) int mea_debug_sq_times(unsigned long long* host, int n) {
-  return (int)cudaMemcpyFromSymbol(host, g_sq_times, sizeof(unsigned long long) * 4 * (n < 8192 ? n : 8192));
+  return (int)cudaMemcpyFromSymbol(host, g_sq_times, sizeof(unsigned long long) * 8 * (n < 8192 ? n : 8192));
 }
 #endif
 

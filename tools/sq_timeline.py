@@ -25,9 +25,9 @@ for it in range(6):
     api.mea_single_query_fwd(q, k, v, workspace=ws)
     torch.cuda.synchronize()
 n = 148 * 16
-buf = (ctypes.c_ulonglong * (4 * n))()
+buf = (ctypes.c_ulonglong * (8 * n))()
 lib.mea_debug_sq_times(buf, n)
-a = np.frombuffer(buf, dtype=np.uint64).reshape(n, 4).astype(np.int64)
+a = np.frombuffer(buf, dtype=np.uint64).reshape(n, 8).astype(np.int64)
 splits = api.mea_single_query_workspace_size  # noqa
 nz = a[:, 0] > 0
 a = a[nz]
@@ -38,6 +38,9 @@ print(f"CTAs {len(a)}: start  min {np.nanmin(r[:,0]):.2f} max {np.nanmax(r[:,0])
 print(f"stream done: min {np.nanmin(r[:,1]):.2f} med {np.nanmedian(r[:,1]):.2f} max {np.nanmax(r[:,1]):.2f}")
 print(f"record done: min {np.nanmin(r[:,2]):.2f} med {np.nanmedian(r[:,2]):.2f} max {np.nanmax(r[:,2]):.2f}")
 print(f"merge done : {np.nanmax(r[:,3]):.2f}")
+m = int(np.nanargmax(r[:, 3]))
+print(f"merging CTA {m}: record {r[m, 2]:.2f}, ticket taken {r[m, 4]:.2f}, merge loads (thread 0) {r[m, 5]:.2f}, "
+      f"done {r[m, 3]:.2f}; last record of any CTA {np.nanmax(r[:, 2]):.2f}")
 print("stream done deciles:", np.round(np.nanpercentile(r[:, 1], [0, 10, 25, 50, 75, 90, 100]), 2))
 print("per-CTA stream time (done - start) deciles:", np.round(np.nanpercentile(r[:, 1] - r[:, 0], [0, 10, 50, 90, 100]), 2))
 order = np.argsort(r[:, 1])
