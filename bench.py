@@ -72,6 +72,9 @@ def parse():
     return ap.parse_args()
 
 
+EXTRA_IDLE_S = 0.3   # idle before each extra's timing (tmean)
+
+
 def free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -335,7 +338,12 @@ def main():
 
     def tmean(fn, steps, warmup=1):
         """median event time of fn over `steps` (ms), max over ranks (the extras: a median, so one
-        stalled call among a few does not move the number; the headline step keeps its own timing)"""
+        stalled call among a few does not move the number; the headline step keeps its own timing).
+        Each extra starts after EXTRA_IDLE_S of idle, so it meets the board in the state the headline
+        step starts in, not in the power cap the previous extra drove it into (measured: the causal
+        forward 0.74 ms right after the other extras, 0.62 ms from idle)."""
+        torch.cuda.synchronize()
+        time.sleep(EXTRA_IDLE_S)
         return max_over_ranks(statistics.median(timed(fn, steps, warmup)))
 
     # ---------------- the timed step (headline)
@@ -723,7 +731,8 @@ def main():
             "data": "synthetic (counter-based Irwin-Hall(12), N(0,1)-like, PAPER.md:231)",
             "config": config,
             "clocks": clk, "gpu_launches": gpu_launches, "roofline": roofline, "kernels": kernels,
-            "cpu_baseline": cpu, "e2e": e2e, "scratch": scratch, **extras,
+            "cpu_baseline": cpu, "e2e": e2e, "scratch": scratch,
+            **({"extras_idle_s": EXTRA_IDLE_S} if extras else {}), **extras,
             "paper_context": {"tpu_v3_fwd_ms_n16384_h1": 11.3, "tpu_v3_diff_ms_n16384_h1": 21.0,
                               "memory_reduction_fwd": "59x", "memory_reduction_diff": "32x"},
         }
