@@ -97,12 +97,39 @@ def test_forward_and_backward_random_case(i):
             # tools/dbg_case766.py)
             gw = max(1.0, abs(scale) * math.sqrt(d))
             rel = {"dq": Hh.REL_NORM_GRAD * gw, "dk": Hh.REL_NORM_GRAD * gw, "dv": Hh.REL_NORM_GRAD}
+            aq, ak, av = _operand_allowance(q[b:b + 1], k[b:b + 1, :L], v[b:b + 1, :L], do[b:b + 1], scale, causal)
+            ex = {"dq": aq, "dk": ak, "dv": av}
             for g, r, nm in ((dq[b:b + 1], rq, "dq"), (dk[b:b + 1, :L], rk, "dk"), (dv[b:b + 1, :L], rv, "dv")):
-                Hh.assert_close_bf16(g, r, abs_tol=gtol if nm != "dv" else Hh.TOL_BF16_GRAD, rel_tol=rel[nm],
+                Hh.assert_close_bf16(g, r, abs_tol=gtol if nm != "dv" else Hh.TOL_BF16_GRAD, rel_tol=rel[nm], extra=ex[nm],
                                      strict=nm == "dv" or gtol == Hh.TOL_BF16_GRAD,
                                      what=f"case {i} {nm}")
             if L < n_k:
                 assert (dk[b, L:] == 0).all() and (dv[b, L:] == 0).all()
+
+
+def _operand_allowance(q, k, v, do, scale, causal):
+    """First-order bound of what bf16 rounding of the backward's inputs can move dq and dk by
+    (reading 16), element-wise, in fp64 from one batch element ([1, n, H, d]): dS is an
+    MMA operand rounded to bf16 (|err| <= 2^-8 |dS|), and delta = dO . out is formed from the
+    bf16-stored out (|err delta_i| <= 2^-8 (|dO| . |out|)_i, entering dS_ij as P_ij err delta_i);
+    then |err dq| <= |scale| e |K| and |err dk| <= |scale| e^T |Q| with e the dS error bound;
+    P is the dV MMA's bf16 operand, |err dv| <= 2^-8 P^T |dO|. Negligible for long rows; large for
+    a few keys under many queries, where dk and dv sum many terms."""
+    aq, ak, av = np.zeros_like(q), np.zeros_like(k), np.zeros_like(k)
+    for h in range(q.shape[2]):
+        qh, kh, vh, doh = q[0, :, h], k[0, :, h], v[0, :, h], do[0, :, h]
+        s = scale * (qh @ kh.T)
+        if causal:
+            s = np.where(np.tril(np.ones(s.shape, dtype=bool)), s, -np.inf)
+        p = np.exp(s - s.max(axis=1, keepdims=True))
+        p /= p.sum(axis=1, keepdims=True)
+        oh = p @ vh
+        ds = p * (doh @ vh.T - (doh * oh).sum(axis=1, keepdims=True))
+        e = 2.0 ** -8 * (np.abs(ds) + p * (np.abs(doh) * np.abs(oh)).sum(axis=1, keepdims=True))
+        aq[0, :, h] = abs(scale) * (e @ np.abs(kh))
+        ak[0, :, h] = abs(scale) * (e.T @ np.abs(qh))
+        av[0, :, h] = 2.0 ** -8 * (p.T @ np.abs(doh))
+    return aq, ak, av
 
 
 N_OTHER = int(os.environ.get("MEA_FUZZ_OTHER_CASES", "60"))
