@@ -166,6 +166,7 @@ def test_single_query_head_blocks_and_split_counts(d):
 
 
 N_SQ_FUZZ = int(__import__("os").environ.get("MEA_SQ_FUZZ_CASES", "6"))
+SQ_FUZZ_BASE = int(__import__("os").environ.get("MEA_SQ_FUZZ_BASE", "90000"))
 
 
 @pytest.mark.parametrize("i", range(N_SQ_FUZZ))
@@ -175,7 +176,7 @@ def test_single_query_random_batches(i):
     reused workspace; the oracle on up to 6 sampled (b, h) rows, at the fp32-output bar of
     test_config2_single_query_full. MEA_SQ_FUZZ_CASES widens it for a soak run."""
     from paper_2112_05682_b200 import api
-    r = np.random.default_rng(90000 + i)
+    r = np.random.default_rng(SQ_FUZZ_BASE + i)
     d = int(r.choice([64, 128]))
     n_k = max(1, int(2.0 ** r.uniform(0, 18)))
     B = int(r.integers(1, 17))
