@@ -44,3 +44,6 @@ for b in range(B):
     for nm, got, ref, emu in (("dq", gq[b:b + 1], rq, eq), ("dk", gk[b:b + 1, :L], rk, ek)):
         print(f"b={b} {nm}: max|got-exact| {np.abs(got - ref).max():.4f}  max|emu-exact| {np.abs(emu - ref).max():.4f}  "
               f"max|got-emu| {np.abs(got - emu).max():.4f}  max|ref| {np.abs(ref).max():.3f}")
+    for nm, got, ref, emu in (("dq", gq[b:b + 1], rq, eq), ("dk", gk[b:b + 1, :L], rk, ek)):
+        print(f"b={b} {nm}: rel-norm got-exact {Hh.rel_norm(got, ref):.4f}  emu-exact {Hh.rel_norm(emu, ref):.4f}  "
+              f"got-emu {Hh.rel_norm(got, emu):.4f}")
